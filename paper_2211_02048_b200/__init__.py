@@ -1,1 +1,427 @@
-"""SIGE sparse-update path on B200."""
+"""SIGE spatially sparse update path on B200 (sm_100a).
+
+Python mirror of the reference's C++ operator API (``proj/include/sige/*.hpp``,
+namespace ``sige``) over the C-ABI library ``lib/libsige_b200.so``: the same
+function names, argument meaning and error behaviour (``ConfigError`` with the
+reference's messages), on CUDA tensors. Device memory and streams come from
+PyTorch; every computation runs in this package's own sm_100a kernels.
+
+Layouts follow the reference: tensors NCHW float32, masks uint8 (H, W), index
+sets int32 (G, 3) rows {n, r, c}, block stacks (G, C, bh, bw).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _capi
+from ._capi import (  # noqa: F401  (re-exported constants)
+    ACT_NONE,
+    ACT_RELU,
+    ACT_SILU,
+    MATH_EXACT,
+    MATH_FP32_FMA,
+    MATH_TF32,
+    RunConfig,
+    default_config,
+)
+
+__all__ = [
+    "ConfigError", "Epilogue", "Model", "Engine", "RunConfig", "default_config",
+    "compute_difference_mask", "downsample_mask", "dilate_mask", "mask_to_block_indices",
+    "gather", "scatter", "scatter_inplace", "scatter_add_inplace", "build_scatter_map",
+    "scatter_gather", "scatter_with_block_residual", "scatter_with_block_residual_unfused",
+    "add_blocks", "subtract_blocks", "apply_epilogue_on_blocks", "conv_on_blocks", "conv2d",
+    "make_edit_fixture", "kernel_launch_count",
+]
+
+
+class ConfigError(ValueError):
+    """The reference's sige::ConfigError (proj/include/sige/common.hpp:14-17)."""
+
+
+class SigeCudaError(RuntimeError):
+    pass
+
+
+def _lib():
+    return _capi.lib()
+
+
+def _check(rc: int) -> None:
+    if rc == _capi.SIGE_OK:
+        return
+    msg = _lib().sige_last_error().decode()
+    if rc == _capi.SIGE_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise SigeCudaError(msg)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ConfigError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise ConfigError(f"{name}: expected {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def kernel_launch_count() -> int:
+    """How many kernels of libsige_b200 have launched in this process."""
+    return int(_lib().sige_kernel_launch_count())
+
+
+@dataclass
+class Epilogue:
+    """Deferred element-wise chain (proj/include/sige/eltwise.hpp:30-59)."""
+
+    steps: list = field(default_factory=list)
+
+    def add_scale_shift(self, scale: torch.Tensor, shift: torch.Tensor) -> "Epilogue":
+        self.steps.append(("ss", scale.float().contiguous().cuda(), shift.float().contiguous().cuda()))
+        return self
+
+    def add_activation(self, kind: int) -> "Epilogue":
+        if kind != ACT_NONE:  # eltwise.cpp:99-105
+            self.steps.append(("act", int(kind)))
+        return self
+
+    def struct(self) -> _capi.Epilogue:
+        e = _capi.Epilogue()
+        e.num_steps = len(self.steps)
+        for k, st in enumerate(self.steps):
+            if st[0] == "ss":
+                e.steps[k].kind = _capi.EPI_SCALE_SHIFT
+                e.steps[k].nparams = st[1].numel()
+                e.steps[k].scale = st[1].data_ptr()
+                e.steps[k].shift = st[2].data_ptr()
+            else:
+                e.steps[k].kind = _capi.EPI_ACTIVATION
+                e.steps[k].act = st[1]
+        return e
+
+
+def _epi(e: Epilogue | None) -> _capi.Epilogue:
+    return (e or Epilogue()).struct()
+
+
+# ------------------------------------------------------------ masks ------
+
+def compute_difference_mask(original: torch.Tensor, edited: torch.Tensor, threshold: float) -> torch.Tensor:
+    """mask.hpp:31-32 — (H, W) uint8, 1 where max_{n,c} |edited - original| > threshold."""
+    o = _dev(original, torch.float32, "compute_difference_mask")
+    e = _dev(edited, torch.float32, "compute_difference_mask")
+    if o.shape != e.shape or o.dim() != 4:
+        raise ConfigError(f"compute_difference_mask: shape mismatch {tuple(o.shape)} vs {tuple(e.shape)}")
+    n, c, h, w = o.shape
+    m = torch.empty((h, w), dtype=torch.uint8, device=o.device)
+    _check(_lib().sige_compute_difference_mask(o.data_ptr(), e.data_ptr(), n, c, h, w, threshold, m.data_ptr(), _stream()))
+    return m
+
+
+def downsample_mask(mask: torch.Tensor, out_h: int, out_w: int) -> torch.Tensor:
+    m = _dev(mask, torch.uint8, "downsample_mask")
+    out = torch.empty((max(out_h, 1), max(out_w, 1)), dtype=torch.uint8, device=m.device)
+    _check(_lib().sige_downsample_mask(m.data_ptr(), m.shape[0], m.shape[1], out_h, out_w, out.data_ptr(), _stream()))
+    return out
+
+
+def dilate_mask(mask: torch.Tensor, radius: int) -> torch.Tensor:
+    m = _dev(mask, torch.uint8, "dilate_mask")
+    out = torch.empty_like(m)
+    _check(_lib().sige_dilate_mask(m.data_ptr(), m.shape[0], m.shape[1], radius, out.data_ptr(), _stream()))
+    return out
+
+
+def mask_to_block_indices(mask: torch.Tensor, block_size: int, batch: int = 1) -> torch.Tensor:
+    """mask.hpp:62-63 — (G, 3) int32 {n, r, c}, tiles row-major then n-major."""
+    m = _dev(mask, torch.uint8, "mask_to_block_indices")
+    h, w = m.shape
+    b = max(block_size, 1)
+    cap = ((h + b - 1) // b) * ((w + b - 1) // b) * max(batch, 1)
+    idx = torch.empty((max(cap, 1), 3), dtype=torch.int32, device=m.device)
+    cnt = C.c_int(0)
+    _check(_lib().sige_mask_to_block_indices(m.data_ptr(), h, w, block_size, batch, idx.data_ptr(), cap, C.byref(cnt), _stream()))
+    return idx[: cnt.value]
+
+
+# ----------------------------------------------------------- blocks ------
+
+def _conv_out(n: int, k: int, s: int) -> int:
+    return (n + 2 * ((k - 1) // 2) - k) // s + 1
+
+
+def gather(x: torch.Tensor, idx: torch.Tensor, block_size: int, k: int, stride: int,
+           epilogue: Epilogue | None = None, idx_hw: tuple[int, int] | None = None) -> torch.Tensor:
+    """kernels.hpp:48-49 — (G, C, win, win), win = s*b + k - s."""
+    x = _dev(x, torch.float32, "gather")
+    idx = _dev(idx, torch.int32, "gather")
+    n, c, h, w = x.shape
+    ih, iw = idx_hw or (_conv_out(h, k, stride), _conv_out(w, k, stride))
+    win = stride * block_size + k - stride
+    out = torch.empty((idx.shape[0], c, max(win, 1), max(win, 1)), dtype=torch.float32, device=x.device)
+    e = _epi(epilogue)
+    _check(_lib().sige_gather(x.data_ptr(), n, c, h, w, idx.data_ptr(), idx.shape[0], block_size, ih, iw, k, stride, C.byref(e), out.data_ptr(), _stream()))
+    return out
+
+
+def scatter_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> None:
+    b = _dev(blocks, torch.float32, "scatter")
+    i = _dev(idx, torch.int32, "scatter")
+    if not base.is_contiguous():
+        raise ConfigError("scatter: base must be contiguous")
+    _check(_lib().sige_scatter_inplace(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.data_ptr(), *base.shape, _stream()))
+
+
+def scatter(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(_dev(base, torch.float32, "scatter"))
+    b = _dev(blocks, torch.float32, "scatter")
+    i = _dev(idx, torch.int32, "scatter")
+    _check(_lib().sige_scatter(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.contiguous().data_ptr(), out.data_ptr(), *out.shape, _stream()))
+    return out
+
+
+def scatter_add_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> None:
+    b = _dev(blocks, torch.float32, "scatter_add")
+    i = _dev(idx, torch.int32, "scatter_add")
+    _check(_lib().sige_scatter_add_inplace(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.data_ptr(), *base.shape, _stream()))
+
+
+def build_scatter_map(idx: torch.Tensor, block_size: int, h: int, w: int):
+    """kernels.hpp:77 — ((H, W, 2) int32 view of {block, dy|dx<<16}, blocks_per_sample)."""
+    i = _dev(idx, torch.int32, "build_scatter_map")
+    m = torch.empty((h, w, 2), dtype=torch.int32, device=i.device)
+    bps = C.c_int(0)
+    _check(_lib().sige_build_scatter_map(i.data_ptr(), i.shape[0], block_size, h, w, m.data_ptr(), C.byref(bps), _stream()))
+    return m, bps.value
+
+
+def scatter_gather(blocks: torch.Tensor, original_out: torch.Tensor, scatter_map, consumer_idx: torch.Tensor,
+                   consumer_block: int, k: int, stride: int, epilogue: Epilogue | None = None) -> torch.Tensor:
+    """kernels.hpp:98-100."""
+    b = _dev(blocks, torch.float32, "scatter_gather")
+    o = _dev(original_out, torch.float32, "scatter_gather")
+    ci = _dev(consumer_idx, torch.int32, "scatter_gather")
+    m, bps = scatter_map
+    n, c, h, w = o.shape
+    win = stride * consumer_block + k - stride
+    out = torch.empty((ci.shape[0], c, win, win), dtype=torch.float32, device=o.device)
+    e = _epi(epilogue)
+    _check(_lib().sige_scatter_gather(b.data_ptr(), b.shape[0], b.shape[2], o.data_ptr(), n, c, h, w, m.data_ptr(), bps,
+                                      ci.data_ptr(), ci.shape[0], consumer_block, _conv_out(h, k, stride), _conv_out(w, k, stride),
+                                      k, stride, C.byref(e), out.data_ptr(), _stream()))
+    return out
+
+
+def _residual(fn, main_blocks, main_idx, shortcut_blocks, shortcut_idx, precomputed_sum, original_shortcut):
+    mb = _dev(main_blocks, torch.float32, "block_residual")
+    sb = _dev(shortcut_blocks, torch.float32, "block_residual")
+    mi = _dev(main_idx, torch.int32, "block_residual")
+    si = _dev(shortcut_idx, torch.int32, "block_residual")
+    s = _dev(precomputed_sum, torch.float32, "block_residual")
+    o = _dev(original_shortcut, torch.float32, "block_residual")
+    out = torch.empty_like(s)
+    _check(fn(mb.data_ptr(), mi.shape[0], mb.shape[2], mi.data_ptr(), sb.data_ptr(), si.shape[0], sb.shape[2], si.data_ptr(),
+              s.data_ptr(), o.data_ptr(), out.data_ptr(), *s.shape, _stream()))
+    return out
+
+
+def scatter_with_block_residual(main_blocks, main_idx, shortcut_blocks, shortcut_idx, precomputed_sum, original_shortcut):
+    """kernels.hpp:107-110."""
+    return _residual(_lib().sige_scatter_with_block_residual, main_blocks, main_idx, shortcut_blocks, shortcut_idx, precomputed_sum, original_shortcut)
+
+
+def scatter_with_block_residual_unfused(main_blocks, main_idx, shortcut_blocks, shortcut_idx, precomputed_sum, original_shortcut):
+    """kernels.hpp:115-118."""
+    return _residual(_lib().sige_scatter_with_block_residual_unfused, main_blocks, main_idx, shortcut_blocks, shortcut_idx, precomputed_sum, original_shortcut)
+
+
+def _combine(a, b, sign):
+    a = _dev(a, torch.float32, "combine_blocks")
+    b = _dev(b, torch.float32, "combine_blocks")
+    if a.shape != b.shape:
+        raise ConfigError("add_blocks: block stack geometry mismatch" if sign > 0 else "subtract_blocks: block stack geometry mismatch")
+    out = torch.empty_like(a)
+    _check(_lib().sige_combine_blocks(a.data_ptr(), b.data_ptr(), sign, a.numel(), out.data_ptr(), _stream()))
+    return out
+
+
+def add_blocks(a, b):
+    return _combine(a, b, 1.0)
+
+
+def subtract_blocks(a, b):
+    return _combine(a, b, -1.0)
+
+
+def apply_epilogue_on_blocks(blocks: torch.Tensor, idx: torch.Tensor, epilogue: Epilogue) -> None:
+    b = _dev(blocks, torch.float32, "apply_epilogue_on_blocks")
+    i = _dev(idx, torch.int32, "apply_epilogue_on_blocks")
+    e = _epi(epilogue)
+    _check(_lib().sige_apply_epilogue_on_blocks(b.data_ptr(), b.shape[0], b.shape[1], b.shape[2], i.data_ptr(), C.byref(e), _stream()))
+    if b.data_ptr() != blocks.data_ptr():
+        blocks.copy_(b)
+
+
+def _conv_desc(weight: torch.Tensor, bias: torch.Tensor | None, stride: int):
+    w = _dev(weight, torch.float32, "conv")
+    b = _dev(bias, torch.float32, "conv") if bias is not None else None
+    cd = _capi.ConvDesc(w.shape[1], w.shape[0], w.shape[2], stride, w.data_ptr(), b.data_ptr() if b is not None else None)
+    return cd, (w, b)
+
+
+def conv_on_blocks(blocks: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, stride: int, block: int,
+                   with_bias: bool = True, math: int = MATH_EXACT) -> torch.Tensor:
+    """kernels.hpp:130-131."""
+    x = _dev(blocks, torch.float32, "conv_on_blocks")
+    cd, keep = _conv_desc(weight, bias, stride)
+    out = torch.empty((x.shape[0], cd.c_out, block, block), dtype=torch.float32, device=x.device)
+    _check(_lib().sige_conv_on_blocks(x.data_ptr(), x.shape[0], x.shape[2], C.byref(cd), int(with_bias), math, out.data_ptr(), block, _stream()))
+    return out
+
+
+def conv2d(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, stride: int = 1,
+           with_bias: bool = True, math: int = MATH_EXACT) -> torch.Tensor:
+    """conv.hpp:35 — zero padding (k-1)/2."""
+    x = _dev(x, torch.float32, "conv2d")
+    cd, keep = _conv_desc(weight, bias, stride)
+    n, c, h, w = x.shape
+    out = torch.empty((n, cd.c_out, _conv_out(h, cd.k, stride), _conv_out(w, cd.k, stride)), dtype=torch.float32, device=x.device)
+    _check(_lib().sige_conv2d(x.data_ptr(), n, c, h, w, C.byref(cd), int(with_bias), math, out.data_ptr(), _stream()))
+    return out
+
+
+# ----------------------------------------------------------- inputs ------
+
+def make_edit_fixture(kind: str, n: int, c: int, h: int, w: int, seed: int):
+    """fixtures.hpp:23-24 — (original, edited) host float32 tensors."""
+    o = torch.empty((n, c, h, w), dtype=torch.float32)
+    e = torch.empty((n, c, h, w), dtype=torch.float32)
+    _check(_lib().sige_make_edit_fixture(kind.encode(), n, c, h, w, seed, o.data_ptr(), e.data_ptr()))
+    return o, e
+
+
+class Model:
+    """A model description (graph.hpp:63-71): a named synthetic model or a
+    ModelDesc pointer supplied by the caller (kept alive by ``owner``)."""
+
+    def __init__(self, name_or_desc, owner=None):
+        self._own = False
+        if isinstance(name_or_desc, str):
+            p = C.POINTER(_capi.ModelDesc)()
+            _check(_lib().sige_model_build(name_or_desc.encode(), C.byref(p)))
+            self.desc = p
+            self._own = True
+        else:
+            self.desc = name_or_desc
+        self.owner = owner
+
+    def __del__(self):
+        try:
+            if self._own:
+                _lib().sige_model_free(self.desc)
+        except Exception:
+            pass
+
+    @property
+    def name(self) -> str:
+        return self.desc.contents.name.decode()
+
+    @property
+    def in_shape(self):
+        d = self.desc.contents
+        return d.in_channels, d.in_h, d.in_w
+
+    def weight_hash(self) -> int:
+        return int(_lib().sige_model_weight_hash(self.desc))
+
+    def required_dilation(self) -> int:
+        v = C.c_int(0)
+        _check(_lib().sige_model_required_dilation(self.desc, C.byref(v)))
+        return v.value
+
+
+class Engine:
+    """Device ActivationCache + sparse executor (graph.hpp:116-226)."""
+
+    def __init__(self, model: Model, batch: int = 1, math: int = MATH_TF32):
+        self.model = model
+        self.batch = batch
+        self.math = math
+        h = C.c_void_p()
+        _check(_lib().sige_engine_create(model.desc, batch, math, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().sige_engine_destroy(self.h)
+        except Exception:
+            pass
+
+    def output_shape(self):
+        n, c, h, w = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(_lib().sige_engine_output_shape(self.h, C.byref(n), C.byref(c), C.byref(h), C.byref(w)))
+        return n.value, c.value, h.value, w.value
+
+    def precompute(self, original: torch.Tensor, step: int = 0) -> None:
+        o = _dev(original, torch.float32, "precompute")
+        _check(_lib().sige_engine_precompute(self.h, o.data_ptr(), step, _stream()))
+
+    def put_tensor(self, key: str, host_nchw, step: int = 0) -> None:
+        t = torch.as_tensor(host_nchw, dtype=torch.float32).contiguous().cpu()
+        _check(_lib().sige_engine_put_tensor(self.h, step, key.encode(), t.data_ptr(), t.numel()))
+
+    def put_norm(self, key: str, scale, shift, step: int = 0) -> None:
+        s = torch.as_tensor(scale, dtype=torch.float32).contiguous().cpu()
+        t = torch.as_tensor(shift, dtype=torch.float32).contiguous().cpu()
+        _check(_lib().sige_engine_put_norm(self.h, step, key.encode(), s.data_ptr(), t.data_ptr(), s.numel()))
+
+    def get_tensor(self, key: str, shape, step: int = 0) -> torch.Tensor:
+        out = torch.empty(shape, dtype=torch.float32)
+        _check(_lib().sige_engine_get_tensor(self.h, step, key.encode(), out.data_ptr(), out.numel()))
+        return out
+
+    def sparse_forward(self, edited: torch.Tensor, mask: torch.Tensor | None = None,
+                       config: RunConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        e = _dev(edited, torch.float32, "sparse_forward")
+        m = _dev(mask, torch.uint8, "sparse_forward") if mask is not None else None
+        if out is None:
+            out = torch.empty(self.output_shape(), dtype=torch.float32, device=e.device)
+        cfg = config or default_config()
+        _check(_lib().sige_engine_sparse_forward(self.h, e.data_ptr(), m.data_ptr() if m is not None else None,
+                                                 C.byref(cfg), out.data_ptr(), _stream()))
+        return out
+
+    def sparse_forward_host(self, edited_host: torch.Tensor, mask_host: torch.Tensor | None = None,
+                            config: RunConfig | None = None, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        e = edited_host.contiguous()
+        if out_host is None:
+            out_host = torch.empty(self.output_shape(), dtype=torch.float32)
+        cfg = config or default_config()
+        mp = mask_host.contiguous().data_ptr() if mask_host is not None else None
+        _check(_lib().sige_engine_sparse_forward_host(self.h, e.data_ptr(), mp, C.byref(cfg), out_host.data_ptr(), _stream()))
+        return out_host
+
+    def dense_forward(self, x: torch.Tensor, reused_stats: bool = False, step: int = 0) -> torch.Tensor:
+        x = _dev(x, torch.float32, "dense_forward")
+        out = torch.empty(self.output_shape(), dtype=torch.float32, device=x.device)
+        _check(_lib().sige_engine_dense_forward(self.h, x.data_ptr(), int(reused_stats), step, out.data_ptr(), _stream()))
+        return out
+
+    def last_launch_count(self) -> int:
+        return int(_lib().sige_engine_last_launch_count(self.h))
+
+    def trace(self, cap: int = 1024):
+        rows = torch.zeros((cap, 6), dtype=torch.int64)
+        n = C.c_int(0)
+        _check(_lib().sige_engine_trace(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
+        return rows[: n.value].clone()
+
+    def cache_bytes(self) -> int:
+        return int(_lib().sige_engine_cache_bytes(self.h))

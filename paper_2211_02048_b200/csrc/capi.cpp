@@ -1,0 +1,420 @@
+// capi.cpp — the extern "C" boundary declared in include/sige_b200.h.
+// Every entry point validates like the reference (ConfigError messages with
+// the reference's op prefixes), converts exceptions into status codes and
+// keeps the message in a thread-local for sige_last_error().
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "engine.hpp"
+#include "models.hpp"
+#include "ops.hpp"
+#include "sige_b200.h"
+
+using namespace sige_b200;
+
+struct sige_engine {
+  Engine* impl;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SIGE_OK;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return SIGE_ERR_CONFIG;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return SIGE_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SIGE_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw ConfigError(std::string(what) + ": null pointer");
+}
+
+// Scratch device buffer for small temporaries of op-level calls.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  explicit DevBuf(size_t n) { SIGE_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+  ~DevBuf() { cudaFree(p); }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* sige_last_error(void) { return g_err.c_str(); }
+const char* sige_version(void) { return "sige_b200 0.1 (sm_100a)"; }
+uint64_t sige_kernel_launch_count(void) { return g_launches.load(); }
+
+void sige_run_config_default(sige_run_config* c) {  // graph.hpp:87-101
+  c->step = 0;
+  c->mask_threshold = 1e-3f;
+  c->dilate_full = 1;
+  c->dilate_scale = 1;
+  c->block3 = 6;
+  c->block1 = 4;
+  c->min_sparse_res = -1;
+  c->sparse = 1;
+  c->norm_precompute = 1;
+  c->elem_fusion = 1;
+  c->scatter_fusion = 1;
+  c->seed = 42;
+}
+
+int sige_compute_difference_mask(const float* original, const float* edited, int n, int c, int h,
+                                 int w, float threshold, uint8_t* mask_out, sige_stream_t s) {
+  return guarded([&] {
+    need(original, "compute_difference_mask");
+    need(edited, "compute_difference_mask");
+    need(mask_out, "compute_difference_mask");
+    op_difference_mask(original, edited, n, c, h, w, threshold, mask_out, as_stream(s));
+  });
+}
+
+int sige_downsample_mask(const uint8_t* mask, int h, int w, int out_h, int out_w, uint8_t* out,
+                         sige_stream_t s) {
+  return guarded([&] { op_downsample_mask(mask, h, w, out_h, out_w, out, as_stream(s)); });
+}
+
+int sige_dilate_mask(const uint8_t* mask, int h, int w, int radius, uint8_t* out, sige_stream_t s) {
+  return guarded([&] {
+    if (radius < 0) throw ConfigError("dilate_mask: radius must be >= 0");
+    DevBuf<uint8_t> tmp(static_cast<size_t>(h) * w);
+    op_dilate_mask(mask, h, w, radius, out, tmp.p, as_stream(s));
+    SIGE_CUDA(cudaStreamSynchronize(as_stream(s)));
+  });
+}
+
+int sige_mask_to_block_indices_async(const uint8_t* mask, int h, int w, int block_size, int batch,
+                                     int32_t* indices, int capacity, int32_t* count_device,
+                                     sige_stream_t s) {
+  return guarded([&] {
+    op_mask_to_block_indices(mask, h, w, block_size, batch, indices, capacity, count_device,
+                             as_stream(s));
+  });
+}
+
+int sige_mask_to_block_indices(const uint8_t* mask, int h, int w, int block_size, int batch,
+                               int32_t* indices, int capacity, int* count_host, sige_stream_t s) {
+  return guarded([&] {
+    DevBuf<int32_t> cnt(1);
+    op_mask_to_block_indices(mask, h, w, block_size, batch, indices, capacity, cnt.p, as_stream(s));
+    int32_t v = 0;
+    SIGE_CUDA(cudaMemcpyAsync(&v, cnt.p, sizeof v, cudaMemcpyDeviceToHost, as_stream(s)));
+    SIGE_CUDA(cudaStreamSynchronize(as_stream(s)));
+    *count_host = v;
+  });
+}
+
+int sige_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, int count,
+                int block_size, int idx_h, int idx_w, int k, int stride,
+                const sige_epilogue* epilogue, float* out, sige_stream_t s) {
+  return guarded([&] {
+    DevEpilogue e = make_dev_epilogue(epilogue, c, n);
+    op_gather(x, n, c, h, w, idx, count, block_size, idx_h, idx_w, k, stride, e, out, as_stream(s));
+  });
+}
+
+namespace {
+void check_scatter_res(int idx_h, int idx_w, int n, int c, int h, int w, const char* op) {
+  if (idx_h != h || idx_w != w)
+    throw ConfigError(std::string(op) + ": index resolution " + std::to_string(idx_h) + "x" +
+                      std::to_string(idx_w) + " does not match tensor (" + std::to_string(n) +
+                      ", " + std::to_string(c) + ", " + std::to_string(h) + ", " +
+                      std::to_string(w) + ")");
+}
+}  // namespace
+
+int sige_scatter_inplace(const float* blocks, int count, int channels, int block, const int32_t* idx,
+                         float* base, int n, int c, int h, int w, sige_stream_t s) {
+  return guarded([&] { op_scatter(blocks, count, channels, block, idx, base, n, c, h, w, false, as_stream(s)); });
+}
+
+int sige_scatter(const float* blocks, int count, int channels, int block, const int32_t* idx,
+                 const float* base, float* out, int n, int c, int h, int w, sige_stream_t s) {
+  return guarded([&] {
+    if (out != base)
+      SIGE_CUDA(cudaMemcpyAsync(out, base, sizeof(float) * n * c * h * w, cudaMemcpyDeviceToDevice,
+                                as_stream(s)));
+    op_scatter(blocks, count, channels, block, idx, out, n, c, h, w, false, as_stream(s));
+  });
+}
+
+int sige_scatter_add_inplace(const float* blocks, int count, int channels, int block,
+                             const int32_t* idx, float* base, int n, int c, int h, int w,
+                             sige_stream_t s) {
+  return guarded([&] { op_scatter(blocks, count, channels, block, idx, base, n, c, h, w, true, as_stream(s)); });
+}
+
+int sige_build_scatter_map(const int32_t* idx, int count, int block, int h, int w,
+                           sige_scatter_entry* map_out, int* bps, sige_stream_t s) {
+  return guarded([&] {
+    DevBuf<int> scratch(2);
+    *bps = op_build_scatter_map(idx, count, block, h, w, map_out, scratch.p, as_stream(s));
+  });
+}
+
+int sige_scatter_gather(const float* blocks, int count, int block, const float* original_out, int n,
+                        int c, int h, int w, const sige_scatter_entry* map, int blocks_per_sample,
+                        const int32_t* consumer_idx, int consumer_count, int consumer_block,
+                        int consumer_h, int consumer_w, int k, int stride,
+                        const sige_epilogue* epilogue, float* out, sige_stream_t s) {
+  return guarded([&] {
+    DevEpilogue e = make_dev_epilogue(epilogue, c, n);
+    op_scatter_gather(blocks, count, block, original_out, n, c, h, w, map, blocks_per_sample,
+                      consumer_idx, consumer_count, consumer_block, consumer_h, consumer_w, k,
+                      stride, e, out, as_stream(s));
+  });
+}
+
+int sige_scatter_with_block_residual(const float* mb, int mcount, int mblock, const int32_t* midx,
+                                     const float* sb, int scount, int sblock, const int32_t* sidx,
+                                     const float* sum, const float* orig_sc, float* out, int n,
+                                     int c, int h, int w, sige_stream_t s) {
+  return guarded([&] {
+    cudaStream_t st = as_stream(s);
+    SIGE_CUDA(cudaMemcpyAsync(out, sum, sizeof(float) * n * c * h * w, cudaMemcpyDeviceToDevice, st));
+    op_residual_pass(mb, mcount, c, mblock, midx, orig_sc, out, h, w, false, st);
+    op_residual_pass(sb, scount, c, sblock, sidx, orig_sc, out, h, w, true, st);
+  });
+}
+
+int sige_scatter_with_block_residual_unfused(const float* mb, int mcount, int mblock,
+                                             const int32_t* midx, const float* sb, int scount,
+                                             int sblock, const int32_t* sidx, const float* sum,
+                                             const float* orig_sc, float* out, int n, int c, int h,
+                                             int w, sige_stream_t s) {
+  // kernels.cpp:339-355: gather(orig_sc) -> add -> scatter; gather -> subtract -> scatter_add.
+  return guarded([&] {
+    cudaStream_t st = as_stream(s);
+    SIGE_CUDA(cudaMemcpyAsync(out, sum, sizeof(float) * n * c * h * w, cudaMemcpyDeviceToDevice, st));
+    DevEpilogue none = make_dev_epilogue(nullptr, c, n);
+    size_t mz = static_cast<size_t>(mcount) * c * mblock * mblock;
+    size_t sz = static_cast<size_t>(scount) * c * sblock * sblock;
+    DevBuf<float> g(std::max(mz, sz)), t(std::max(mz, sz));
+    op_gather(orig_sc, n, c, h, w, midx, mcount, mblock, h, w, 1, 1, none, g.p, st);
+    op_combine(mb, g.p, 1.0f, mz, t.p, st);
+    op_scatter(t.p, mcount, c, mblock, midx, out, n, c, h, w, false, st);
+    op_gather(orig_sc, n, c, h, w, sidx, scount, sblock, h, w, 1, 1, none, g.p, st);
+    op_combine(sb, g.p, -1.0f, sz, t.p, st);
+    op_scatter(t.p, scount, c, sblock, sidx, out, n, c, h, w, true, st);
+    SIGE_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int sige_combine_blocks(const float* a, const float* b, float sign, size_t numel, float* out,
+                        sige_stream_t s) {
+  return guarded([&] { op_combine(a, b, sign, numel, out, as_stream(s)); });
+}
+
+int sige_apply_epilogue_on_blocks(float* blocks, int count, int channels, int bh,
+                                  const int32_t* idx, const sige_epilogue* epilogue,
+                                  sige_stream_t s) {
+  return guarded([&] {
+    // per-sample params are indexed by each block's own n (eltwise.cpp:48-58)
+    DevEpilogue e = make_dev_epilogue(epilogue, channels, 1);
+    op_epilogue_blocks(blocks, count, channels, bh, idx, e, as_stream(s));
+  });
+}
+
+int sige_conv_on_blocks(const float* blocks, int count, int window, const sige_conv_desc* conv,
+                        int with_bias, int math_mode, float* out, int block, sige_stream_t s) {
+  return guarded([&] {
+    need(conv, "conv_on_blocks");
+    const sige_conv_desc& cv = *conv;
+    if (cv.k != 1 && cv.k != 3) throw ConfigError("conv: kernel size must be 1 or 3, got " + std::to_string(cv.k));
+    if (cv.stride != 1 && cv.stride != 2)
+      throw ConfigError("conv: stride must be 1 or 2, got " + std::to_string(cv.stride));
+    int b_out = (window - cv.k) / cv.stride + 1;  // kernels.cpp:397-405
+    if (b_out != block)
+      throw ConfigError("conv_on_blocks: window " + std::to_string(window) + " with k=" +
+                        std::to_string(cv.k) + " s=" + std::to_string(cv.stride) + " yields " +
+                        std::to_string(b_out) + ", expected block " + std::to_string(block));
+    if (math_mode == SIGE_MATH_TF32)
+      throw ConfigError("conv_on_blocks: SIGE_MATH_TF32 runs through the engine (fused path)");
+    op_conv_cc(blocks, static_cast<long long>(cv.c_in) * window * window, cv.c_in, window, window,
+               cv.weight, with_bias ? cv.bias : nullptr, cv.c_out, cv.k, cv.stride, 0, out,
+               static_cast<long long>(cv.c_out) * block * block, block, block, count, math_mode,
+               as_stream(s));
+  });
+}
+
+int sige_conv2d(const float* x, int n, int c, int h, int w, const sige_conv_desc* conv, int with_bias,
+                int math_mode, float* out, sige_stream_t s) {
+  return guarded([&] {
+    need(conv, "conv2d");
+    const sige_conv_desc& cv = *conv;
+    if (c != cv.c_in)
+      throw ConfigError("conv2d: input has " + std::to_string(c) + " channels, layer expects " +
+                        std::to_string(cv.c_in));
+    if (math_mode == SIGE_MATH_TF32)
+      throw ConfigError("conv2d: SIGE_MATH_TF32 runs through the engine (fused path)");
+    int oh = conv_out_dim(h, cv.k, cv.stride), ow = conv_out_dim(w, cv.k, cv.stride);
+    op_conv_cc(x, static_cast<long long>(c) * h * w, c, h, w, cv.weight, with_bias ? cv.bias : nullptr,
+               cv.c_out, cv.k, cv.stride, (cv.k - 1) / 2, out,
+               static_cast<long long>(cv.c_out) * oh * ow, oh, ow, n, math_mode, as_stream(s));
+  });
+}
+
+// ---- engine
+int sige_engine_create(const sige_model_desc* model, int batch, int math_mode, sige_engine** out) {
+  return guarded([&] {
+    need(model, "engine");
+    need(out, "engine");
+    *out = new sige_engine{new Engine(model, batch, math_mode)};
+  });
+}
+
+void sige_engine_destroy(sige_engine* eng) {
+  if (!eng) return;
+  delete eng->impl;
+  delete eng;
+}
+
+int sige_engine_precompute(sige_engine* eng, const float* original, int step, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    need(original, "precompute");
+    eng->impl->precompute(original, step, as_stream(s));
+  });
+}
+
+int sige_engine_put_tensor(sige_engine* eng, int step, const char* key, const float* host,
+                           size_t numel) {
+  return guarded([&] { eng->impl->put_tensor(step, key, host, numel); });
+}
+
+int sige_engine_put_norm(sige_engine* eng, int step, const char* key, const float* sc,
+                         const float* sh, size_t numel) {
+  return guarded([&] { eng->impl->put_norm(step, key, sc, sh, numel); });
+}
+
+int sige_engine_get_tensor(sige_engine* eng, int step, const char* key, float* host, size_t numel) {
+  return guarded([&] { eng->impl->get_tensor(step, key, host, numel); });
+}
+
+int sige_engine_sparse_forward(sige_engine* eng, const float* edited, const uint8_t* mask,
+                               const sige_run_config* cfg, float* out, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    need(edited, "sparse_forward");
+    need(out, "sparse_forward");
+    sige_run_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      sige_run_config_default(&c);
+    eng->impl->sparse_forward(edited, mask, c, out, as_stream(s));
+  });
+}
+
+namespace {
+struct HostStage {  // per-engine pinned/device staging for the host-buffer API
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  uint8_t* d_mask = nullptr;
+  size_t in_n = 0, out_n = 0, mask_n = 0;
+};
+thread_local std::vector<std::pair<const sige_engine*, HostStage>> g_stage;
+HostStage& stage_for(const sige_engine* e) {
+  for (auto& kv : g_stage)
+    if (kv.first == e) return kv.second;
+  g_stage.push_back({e, HostStage{}});
+  return g_stage.back().second;
+}
+}  // namespace
+
+int sige_engine_sparse_forward_host(sige_engine* eng, const float* edited_host,
+                                    const uint8_t* mask_host, const sige_run_config* cfg,
+                                    float* out_host, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    Engine& E = *eng->impl;
+    cudaStream_t st = as_stream(s);
+    int n, c, h, w;
+    E.output_shape(&n, &c, &h, &w);
+    const size_t in_n = static_cast<size_t>(E.batch()) * E.in_channels() * E.in_h() * E.in_w();
+    const size_t out_n = static_cast<size_t>(n) * c * h * w;
+    const size_t mask_n = static_cast<size_t>(E.in_h()) * E.in_w();
+    HostStage& S = stage_for(eng);
+    if (S.in_n < in_n) {
+      cudaFree(S.d_in);
+      SIGE_CUDA(cudaMalloc(&S.d_in, in_n * sizeof(float)));
+      S.in_n = in_n;
+    }
+    if (S.out_n < out_n) {
+      cudaFree(S.d_out);
+      SIGE_CUDA(cudaMalloc(&S.d_out, out_n * sizeof(float)));
+      S.out_n = out_n;
+    }
+    if (mask_host && S.mask_n < mask_n) {
+      cudaFree(S.d_mask);
+      SIGE_CUDA(cudaMalloc(&S.d_mask, mask_n));
+      S.mask_n = mask_n;
+    }
+    SIGE_CUDA(cudaMemcpyAsync(S.d_in, edited_host, in_n * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (mask_host) SIGE_CUDA(cudaMemcpyAsync(S.d_mask, mask_host, mask_n, cudaMemcpyHostToDevice, st));
+    sige_run_config c2;
+    if (cfg)
+      c2 = *cfg;
+    else
+      sige_run_config_default(&c2);
+    E.sparse_forward(S.d_in, mask_host ? S.d_mask : nullptr, c2, S.d_out, st);
+    SIGE_CUDA(cudaMemcpyAsync(out_host, S.d_out, out_n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    SIGE_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int sige_engine_dense_forward(sige_engine* eng, const float* input, int reused_stats, int step,
+                              float* out, sige_stream_t s) {
+  return guarded([&] { eng->impl->dense_forward(input, reused_stats != 0, step, out, as_stream(s)); });
+}
+
+int sige_engine_output_shape(const sige_engine* eng, int* n, int* c, int* h, int* w) {
+  return guarded([&] { eng->impl->output_shape(n, c, h, w); });
+}
+
+int sige_engine_last_launch_count(const sige_engine* eng) { return eng ? eng->impl->last_launch_count() : 0; }
+
+int sige_engine_trace(sige_engine* eng, uint64_t* rows, int cap, int* nrows, sige_stream_t s) {
+  return guarded([&] { *nrows = eng->impl->trace(rows, cap, as_stream(s)); });
+}
+
+size_t sige_engine_cache_bytes(const sige_engine* eng) { return eng ? eng->impl->cache_bytes() : 0; }
+
+// ---- synthetic inputs
+int sige_make_edit_fixture(const char* kind, int n, int c, int h, int w, uint32_t seed,
+                           float* original_host, float* edited_host) {
+  return guarded([&] { make_edit_fixture(kind, n, c, h, w, seed, original_host, edited_host); });
+}
+
+int sige_model_build(const char* name, sige_model_desc** out) {
+  return guarded([&] { *out = build_model(name); });
+}
+
+void sige_model_free(sige_model_desc* model) {
+  if (model) free_model(model);
+}
+
+int sige_model_required_dilation(const sige_model_desc* model, int* out) {
+  return guarded([&] { *out = required_dilation(model); });
+}
+
+uint64_t sige_model_weight_hash(const sige_model_desc* model) { return model_weight_hash(model); }
+
+}  // extern "C"

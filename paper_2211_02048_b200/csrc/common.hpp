@@ -1,0 +1,108 @@
+// common.hpp — shared host/device infrastructure of libsige_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+
+#include "glibc_expf.h"
+#include "sige_b200.h"
+
+namespace sige_b200 {
+
+// ConfigError of the reference (proj/include/sige/common.hpp:14-17): every
+// geometry / configuration violation. Mapped to SIGE_ERR_CONFIG at the C ABI.
+class ConfigError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define SIGE_CUDA(x)                                                      \
+  do {                                                                    \
+    cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess) ::sige_b200::throw_cuda(e_, #x, __FILE__, __LINE__); \
+  } while (0)
+
+// Every kernel launch goes through this so the library can report how many of
+// its own kernels ran (sige_kernel_launch_count) and fail loudly on launch errors.
+extern std::atomic<uint64_t> g_launches;
+inline void after_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw_cuda(e, name, __FILE__, __LINE__);
+}
+
+inline cudaStream_t as_stream(sige_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+inline int conv_out_dim(int in, int k, int stride) {
+  int pad = (k - 1) / 2;
+  return (in + 2 * pad - k) / stride + 1;
+}
+
+// Which glibc expf build the host uses (decides SiLU bits). Probed once from
+// the live libm by the C ABI layer (see capi.cpp: detect_expf_variant).
+bool host_expf_is_fma();
+
+// Number of SMs of the current device (cached).
+int sm_count();
+
+// ---------------------------------------------------------------- epilogue
+// Device form of `sige::Epilogue` (proj/include/sige/eltwise.hpp:30-59): up
+// to SIGE_MAX_EPI_STEPS ordered steps, each a per-channel ScaleShift (with C
+// or N*C params, eltwise.cpp:48-58) or an activation. Passed by value.
+struct DevEpilogue {
+  int num_steps = 0;
+  int fma_expf = 1;  // glibc expf variant to reproduce
+  int kind[SIGE_MAX_EPI_STEPS] = {};
+  int act[SIGE_MAX_EPI_STEPS] = {};
+  int per_sample[SIGE_MAX_EPI_STEPS] = {};  // 1 if params are N*C (sample-major)
+  const float* scale[SIGE_MAX_EPI_STEPS] = {};
+  const float* shift[SIGE_MAX_EPI_STEPS] = {};
+};
+
+// Validates and converts a C-ABI epilogue for `channels` and `batch`, with
+// the reference's "epilogue: affine param size ..." message (eltwise.cpp:55-57).
+DevEpilogue make_dev_epilogue(const sige_epilogue* e, int channels, int batch);
+
+#ifdef __CUDACC__
+// Reference activation arithmetic (eltwise.cpp:23-36), no FMA contraction.
+__device__ __forceinline__ float dev_act(float v, int kind, int fma_expf) {
+  if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;  // NaN -> 0, -0 -> +0
+  if (kind == SIGE_ACT_SILU) {
+    float e = glibc_expf(-v, fma_expf != 0);
+    return __fdiv_rn(v, __fadd_rn(1.0f, e));
+  }
+  return v;
+}
+
+// Applies the chain to one value of channel ch of sample n (apply_span /
+// apply_cell / apply_slab are all per-value maps, eltwise.cpp:110-150).
+__device__ __forceinline__ float dev_epi(const DevEpilogue& e, float v, int ch, int channels,
+                                         int n) {
+#pragma unroll
+  for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
+    if (s >= e.num_steps) break;
+    if (e.kind[s] == SIGE_EPI_ACTIVATION) {
+      v = dev_act(v, e.act[s], e.fma_expf);
+    } else {
+      int off = e.per_sample[s] ? n * channels + ch : ch;
+      v = __fadd_rn(__fmul_rn(__ldg(e.scale[s] + off), v), __ldg(e.shift[s] + off));
+    }
+  }
+  return v;
+}
+#endif
+
+}  // namespace sige_b200

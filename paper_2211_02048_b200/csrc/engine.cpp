@@ -1,0 +1,872 @@
+// engine.cpp — device ActivationCache, dense walk (precompute / dense_forward)
+// and the compiled sparse_forward executor. See engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <tuple>
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+namespace sige_b200 {
+
+namespace {
+
+std::string lk(int i) { return "L" + std::to_string(i); }
+
+// layer_runs_sparse (graph.cpp:478-483).
+bool runs_sparse(const LayerDev& L, int h, int w, const sige_run_config& cfg) {
+  if (!cfg.sparse || !L.policy_sparse) return false;
+  int thr = cfg.min_sparse_res >= 0 ? cfg.min_sparse_res : L.min_resolution;
+  return std::min(h, w) >= thr;
+}
+
+void epi_push_ss(DevEpilogue& e, const float* sc, const float* sh, int np, int channels) {
+  if (e.num_steps >= SIGE_MAX_EPI_STEPS)
+    throw ConfigError("epilogue: more than " + std::to_string(SIGE_MAX_EPI_STEPS) +
+                      " pending element-wise steps");
+  const int s = e.num_steps++;
+  e.kind[s] = SIGE_EPI_SCALE_SHIFT;
+  e.per_sample[s] = np != channels ? 1 : 0;
+  e.scale[s] = sc;
+  e.shift[s] = sh;
+}
+
+void epi_push_act(DevEpilogue& e, int act) {
+  if (act == SIGE_ACT_NONE) return;  // Epilogue::add_activation (eltwise.cpp:99-105)
+  if (e.num_steps >= SIGE_MAX_EPI_STEPS)
+    throw ConfigError("epilogue: more than " + std::to_string(SIGE_MAX_EPI_STEPS) +
+                      " pending element-wise steps");
+  const int s = e.num_steps++;
+  e.kind[s] = SIGE_EPI_ACTIVATION;
+  e.act[s] = act;
+}
+
+Src plain(const DevTensor& t) {
+  Src s;
+  s.ptr = t.p;
+  s.layout = t.layout;
+  s.n = t.n;
+  s.c = t.c;
+  s.h = t.h;
+  s.w = t.w;
+  s.epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+  return s;
+}
+
+Dst to_dst(const DevTensor& t, int mode = kStore) {
+  Dst d;
+  d.ptr = t.p;
+  d.n = t.n;
+  d.c = t.c;
+  d.h = t.h;
+  d.w = t.w;
+  d.mode = mode;
+  return d;
+}
+
+}  // namespace
+
+// A compiled sparse_forward for one (step, RunConfig): plan entries, ordered
+// launches, restore jobs, trace metadata.
+struct Program {
+  std::vector<PlanEntryDev> entries;
+  PlanEntryDev* entries_dev = nullptr;
+  std::vector<std::function<void(cudaStream_t)>> steps;
+  std::vector<RestoreJob> restores;
+  RestoreJob* restores_dev = nullptr;
+  long long restore_max = 0;
+  std::vector<TraceInfo> trace;
+  uint32_t* bits = nullptr;
+  int32_t* any = nullptr;
+  int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
+  int launches = 0;
+};
+
+// ----------------------------------------------------------- basics -----
+
+Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), math_(math) {
+  if (batch < 1) throw ConfigError("engine: batch must be >= 1");
+  if (math != SIGE_MATH_EXACT && math != SIGE_MATH_TF32 && math != SIGE_MATH_FP32_FMA)
+    throw ConfigError("engine: unknown math mode " + std::to_string(math));
+  shapes_ = walk_shapes(m);
+  name_ = m->name ? m->name : "";
+  in_c_ = m->in_channels;
+  in_h_ = m->in_h;
+  in_w_ = m->in_w;
+  out_c_ = shapes_.back().c_out;
+  out_h_ = shapes_.back().h_out;
+  out_w_ = shapes_.back().w_out;
+  auto upload = [&](const float* host, size_t n) -> float* {
+    if (!host) return nullptr;
+    float* d = static_cast<float*>(alloc(n * sizeof(float)));
+    SIGE_CUDA(cudaMemcpy(d, host, n * sizeof(float), cudaMemcpyHostToDevice));
+    return d;
+  };
+  auto up_conv = [&](const sige_conv_desc& c) {
+    ConvW w;
+    w.c_in = c.c_in;
+    w.c_out = c.c_out;
+    w.k = c.k;
+    w.stride = c.stride;
+    w.w = upload(c.weight, static_cast<size_t>(c.c_out) * c.c_in * c.k * c.k);
+    w.bias = upload(c.bias, c.c_out);
+    if (math_ == SIGE_MATH_TF32) {
+      w.w_tc = pack_weights_tc(w.w, c.c_out, c.c_in, c.k, &w.n_pad, &w.k_pad, nullptr);
+      allocations_.push_back(const_cast<float*>(w.w_tc));
+    }
+    return w;
+  };
+  for (int i = 0; i < m->num_layers; ++i) {
+    const sige_layer_desc& d = m->layers[i];
+    LayerDev L;
+    L.kind = d.kind;
+    L.act = d.act;
+    L.policy_sparse = d.policy_sparse;
+    L.min_resolution = d.min_resolution;
+    if (d.kind == SIGE_LAYER_CONV || d.kind == SIGE_LAYER_DOWNSAMPLE || d.kind == SIGE_LAYER_RESBLOCK)
+      L.conv = up_conv(d.conv);
+    if (d.kind == SIGE_LAYER_RESBLOCK) {
+      L.conv2 = up_conv(d.conv2);
+      L.has_shortcut = d.has_shortcut;
+      if (d.has_shortcut) L.shortcut = up_conv(d.shortcut);
+    }
+    if (d.kind == SIGE_LAYER_NORM || d.kind == SIGE_LAYER_RESBLOCK) {
+      const sige_norm_desc& n = d.norm;
+      L.norm_kind = n.kind;
+      L.groups = n.groups;
+      L.channels = n.channels;
+      L.eps = n.eps;
+      L.gamma = upload(n.gamma, n.channels);
+      L.beta = upload(n.beta, n.channels);
+      L.rmean = upload(n.running_mean, n.channels);
+      L.rvar = upload(n.running_var, n.channels);
+      if (n.kind == SIGE_NORM_BATCH && (!L.rmean || !L.rvar))
+        throw ConfigError("norm: batch kind requires per-channel running stats");
+    }
+    layers_.push_back(L);
+  }
+}
+
+Engine::~Engine() {
+  for (auto& kv : programs_) {
+    (void)kv;
+  }
+  for (void* p : allocations_) cudaFree(p);
+}
+
+void* Engine::alloc(size_t bytes) {
+  void* p = nullptr;
+  SIGE_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  allocations_.push_back(p);
+  return p;
+}
+
+void Engine::output_shape(int* n, int* c, int* h, int* w) const {
+  *n = batch_;
+  *c = out_c_;
+  *h = out_h_;
+  *w = out_w_;
+}
+
+size_t Engine::cache_bytes() const {
+  size_t b = 0;
+  for (auto& kv : cache_)
+    if (kv.first.second != "input") b += kv.second.numel() * sizeof(float);
+  for (auto& kv : norms_) b += 2 * sizeof(float) * kv.second.np;
+  return b;
+}
+
+const DevTensor& Engine::cache_tensor(int step, const std::string& key) const {
+  auto it = cache_.find({step, key});
+  if (it == cache_.end())
+    throw ConfigError("precompute required: no cache entry for step " + std::to_string(step) +
+                      ", layer " + key);  // graph.cpp:242-248
+  return it->second;
+}
+
+const DevNorm& Engine::cache_norm(int step, const std::string& key) const {
+  auto it = norms_.find({step, key});
+  if (it == norms_.end())
+    throw ConfigError("precompute required: no cached norm params for step " +
+                      std::to_string(step) + ", layer " + key);  // graph.cpp:250-258
+  return it->second;
+}
+
+DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, int w, int layout) {
+  DevTensor& t = cache_[{step, key}];
+  if (!t.p || t.c != c || t.h != h || t.w != w || t.n != batch_ || t.layout != layout) {
+    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * sizeof(float)));
+    t.n = batch_;
+    t.c = c;
+    t.h = h;
+    t.w = w;
+    t.layout = layout;
+  }
+  return t;
+}
+
+DevNorm& Engine::norm_slot(int step, const std::string& key, int np) {
+  DevNorm& n = norms_[{step, key}];
+  if (!n.scale || n.np != np) {
+    n.scale = static_cast<float*>(alloc(np * sizeof(float)));
+    n.shift = static_cast<float*>(alloc(np * sizeof(float)));
+    n.np = np;
+  }
+  return n;
+}
+
+DevTensor& Engine::scratch(const std::string& key, int c, int h, int w, int layout) {
+  DevTensor& t = scratch_[key];
+  if (!t.p || t.c != c || t.h != h || t.w != w || t.layout != layout) {
+    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * sizeof(float)));
+    t.n = batch_;
+    t.c = c;
+    t.h = h;
+    t.w = w;
+    t.layout = layout;
+  }
+  return t;
+}
+
+DevNorm& Engine::scratch_norm(const std::string& key, int np) {
+  DevNorm& n = scratch_norms_[key];
+  if (!n.scale || n.np < np) {
+    n.scale = static_cast<float*>(alloc(np * sizeof(float)));
+    n.shift = static_cast<float*>(alloc(np * sizeof(float)));
+  }
+  n.np = np;
+  return n;
+}
+
+// Working copy of a cached output: equals the cache entry except for the
+// tiles the current call scattered (restored at the start of the next call).
+DevTensor& Engine::work_buffer(int step, const std::string& key) {
+  auto it = work_.find({step, key});
+  if (it != work_.end()) return it->second;
+  const DevTensor& src = cache_tensor(step, key);
+  DevTensor w = src;
+  w.p = static_cast<float*>(alloc(src.numel() * sizeof(float)));
+  SIGE_CUDA(cudaMemcpy(w.p, src.p, src.numel() * sizeof(float), cudaMemcpyDeviceToDevice));
+  return work_[{step, key}] = w;
+}
+
+// All tiles of an (oh, ow) grid, 8x8, n-major: the dense path runs the same
+// fused kernels over every tile (equal to conv2d, test_kernels.cpp:288-351).
+Tiles Engine::dense_tiles(int oh, int ow) {
+  constexpr int kB = 8;
+  auto key = std::make_pair(oh, ow);
+  auto it = dense_tiles_.find(key);
+  if (it == dense_tiles_.end()) {
+    std::vector<int32_t> idx;
+    for (int n = 0; n < batch_; ++n)
+      for (int r = 0; r < oh; r += kB)
+        for (int c = 0; c < ow; c += kB) {
+          idx.push_back(n);
+          idx.push_back(r);
+          idx.push_back(c);
+        }
+    int32_t* d = static_cast<int32_t*>(alloc(idx.size() * sizeof(int32_t)));
+    SIGE_CUDA(cudaMemcpy(d, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    it = dense_tiles_.emplace(key, std::make_pair(d, static_cast<int>(idx.size() / 3))).first;
+  }
+  Tiles t;
+  t.idx = it->second.first;
+  t.count = it->second.second;
+  t.capacity = t.count;
+  t.bh = t.bw = kB;
+  return t;
+}
+
+void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& dst,
+                  cudaStream_t st) const {
+  if (math_ == SIGE_MATH_TF32)
+    launch_conv_tc(src, t, cw, dst, st);
+  else
+    launch_conv_exact(src, t, cw, dst, math_, st);
+}
+
+// fold_norm_layer (graph.cpp:310-322).
+void Engine::fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st) {
+  if (L.norm_kind == SIGE_NORM_BATCH) {
+    launch_bn_fold(L.channels, L.eps, L.gamma, L.beta, L.rmean, L.rvar, out.scale, out.shift, st);
+  } else {
+    launch_gn_fold(x, L.groups, L.eps, L.gamma, L.beta, out.scale, out.shift, nullptr,
+                   math_ == SIGE_MATH_TF32 ? 0 : 1, st);
+  }
+}
+
+void Engine::invalidate_programs() {
+  // Working buffers mirror cache contents; any cache write drops them. The
+  // memory stays in allocations_ until the engine dies (cache writes are rare).
+  work_.clear();
+  programs_.clear();
+  last_program_ = nullptr;
+}
+
+// ---------------------------------------------------------- dense walk --
+// dense_walk (graph.cpp:343-412) on the device. capture=true stores every
+// cache entry (precompute); reused=true takes folded norms from the cache.
+void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
+                        cudaStream_t st) {
+  Src x = input;
+  for (size_t i = 0; i < layers_.size(); ++i) {
+    const LayerDev& L = layers_[i];
+    const LayerShape& sh = shapes_[i];
+    const std::string key = lk(static_cast<int>(i));
+    switch (L.kind) {
+      case SIGE_LAYER_CONV:
+      case SIGE_LAYER_DOWNSAMPLE: {
+        DevTensor& o = capture ? cache_slot(step, key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC)
+                               : scratch("dense." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
+        conv(x, dense_tiles(sh.h_out, sh.w_out), L.conv, to_dst(o), st);
+        x = plain(o);
+        break;
+      }
+      case SIGE_LAYER_NORM: {
+        DevNorm* f;
+        const int np = L.norm_kind == SIGE_NORM_BATCH ? L.channels : batch_ * L.channels;
+        if (reused) {
+          f = const_cast<DevNorm*>(&cache_norm(step, key + ".norm"));
+        } else {
+          f = capture ? &norm_slot(step, key + ".norm", np) : &scratch_norm("dense." + key + ".norm", np);
+          fold_norm(L, x, *f, st);
+        }
+        epi_push_ss(x.epi, f->scale, f->shift, f->np, x.c);
+        break;
+      }
+      case SIGE_LAYER_ACTIVATION:
+        epi_push_act(x.epi, L.act);
+        break;
+      case SIGE_LAYER_UPSAMPLE:
+        x.up += 1;
+        x.h *= 2;
+        x.w *= 2;
+        break;
+      case SIGE_LAYER_RESBLOCK: {
+        const int c1 = L.conv.c_out, co = L.conv2.c_out, h = sh.h_in, w = sh.w_in;
+        DevTensor& m1 = capture ? cache_slot(step, key + ".conv1.out", c1, h, w, kNHWC)
+                                : scratch("dense." + key + ".conv1.out", c1, h, w, kNHWC);
+        conv(x, dense_tiles(h, w), L.conv, to_dst(m1), st);
+        const int np = L.norm_kind == SIGE_NORM_BATCH ? L.channels : batch_ * L.channels;
+        DevNorm* f;
+        if (reused) {
+          f = const_cast<DevNorm*>(&cache_norm(step, key + ".norm1"));
+        } else {
+          f = capture ? &norm_slot(step, key + ".norm1", np) : &scratch_norm("dense." + key + ".norm1", np);
+          fold_norm(L, plain(m1), *f, st);
+        }
+        Src mid = plain(m1);
+        epi_push_ss(mid.epi, f->scale, f->shift, f->np, c1);
+        epi_push_act(mid.epi, L.act);
+        DevTensor& sc = capture ? cache_slot(step, key + ".shortcut.out", co, h, w, kNHWC)
+                                : scratch("dense." + key + ".shortcut.out", co, h, w, kNHWC);
+        if (L.has_shortcut)
+          conv(x, dense_tiles(h, w), L.shortcut, to_dst(sc), st);
+        else
+          launch_materialize(x, sc.p, kNHWC, st);
+        DevTensor& sum = capture ? cache_slot(step, key + ".sum", co, h, w, kNHWC)
+                                 : scratch("dense." + key + ".sum", co, h, w, kNHWC);
+        if (capture) {
+          DevTensor& m2 = cache_slot(step, key + ".conv2.out", co, h, w, kNHWC);
+          conv(mid, dense_tiles(h, w), L.conv2, to_dst(m2), st);
+          launch_add(m2.p, sc.p, sum.p, sum.numel(), st);  // add(m, sc), graph.cpp:404
+        } else {
+          Dst d = to_dst(sum, kAddSrc);
+          d.addend = plain(sc);
+          conv(mid, dense_tiles(h, w), L.conv2, d, st);
+        }
+        x = plain(sum);
+        break;
+      }
+    }
+  }
+  if (capture) {
+    DevTensor& fin = cache_slot(step, "final", out_c_, out_h_, out_w_, kNCHW);
+    launch_materialize(x, fin.p, kNCHW, st);
+    if (out_nchw) SIGE_CUDA(cudaMemcpyAsync(out_nchw, fin.p, fin.numel() * sizeof(float),
+                                            cudaMemcpyDeviceToDevice, st));
+  } else {
+    launch_materialize(x, out_nchw, kNCHW, st);
+  }
+}
+
+void Engine::precompute(const float* original, int step, cudaStream_t st) {
+  invalidate_programs();
+  DevTensor& in = cache_slot(step, "input", in_c_, in_h_, in_w_, kNCHW);
+  SIGE_CUDA(cudaMemcpyAsync(in.p, original, in.numel() * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  dense_walk(plain(in), step, /*capture=*/true, /*reused=*/false, nullptr, st);
+}
+
+void Engine::dense_forward(const float* input, bool reused, int step, float* out, cudaStream_t st) {
+  DevTensor in;
+  in.p = const_cast<float*>(input);
+  in.n = batch_;
+  in.c = in_c_;
+  in.h = in_h_;
+  in.w = in_w_;
+  in.layout = kNCHW;
+  dense_walk(plain(in), step, false, reused, out, st);
+}
+
+// ------------------------------------------------------ cache exchange --
+namespace {
+bool is_nchw_key(const std::string& key) { return key == "final" || key == "input"; }
+}  // namespace
+
+void Engine::put_tensor(int step, const std::string& key, const float* host, size_t numel) {
+  // Shape from the model walk (graph.cpp:356-410 keys).
+  int c = 0, h = 0, w = 0;
+  if (key == "final") {
+    c = out_c_, h = out_h_, w = out_w_;
+  } else if (key == "input") {
+    c = in_c_, h = in_h_, w = in_w_;
+  } else {
+    int li = -1;
+    char rest[64] = {0};
+    if (std::sscanf(key.c_str(), "L%d.%63s", &li, rest) != 2 || li < 0 ||
+        li >= static_cast<int>(layers_.size()))
+      throw ConfigError("cache: unknown key " + key);
+    const LayerShape& s = shapes_[li];
+    const std::string r = rest;
+    if (r == "out") {
+      c = s.c_out, h = s.h_out, w = s.w_out;
+    } else if (r == "conv1.out") {
+      c = layers_[li].conv.c_out, h = s.h_in, w = s.w_in;
+    } else if (r == "conv2.out" || r == "shortcut.out" || r == "sum") {
+      c = s.c_out, h = s.h_out, w = s.w_out;
+    } else {
+      throw ConfigError("cache: unknown key " + key);
+    }
+  }
+  if (numel != static_cast<size_t>(batch_) * c * h * w)
+    throw ConfigError("cache entry " + key + ": expected " +
+                      std::to_string(static_cast<size_t>(batch_) * c * h * w) + " values");
+  invalidate_programs();
+  const int layout = is_nchw_key(key) ? kNCHW : kNHWC;
+  DevTensor& t = cache_slot(step, key, c, h, w, layout);
+  std::vector<float> buf(numel);
+  if (layout == kNHWC) {
+    for (int n = 0; n < batch_; ++n)
+      for (int ch = 0; ch < c; ++ch)
+        for (int y = 0; y < h; ++y)
+          for (int x = 0; x < w; ++x)
+            buf[((static_cast<size_t>(n) * h + y) * w + x) * c + ch] =
+                host[((static_cast<size_t>(n) * c + ch) * h + y) * w + x];
+  } else {
+    std::memcpy(buf.data(), host, numel * sizeof(float));
+  }
+  SIGE_CUDA(cudaMemcpy(t.p, buf.data(), numel * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void Engine::put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np) {
+  invalidate_programs();
+  DevNorm& n = norm_slot(step, key, static_cast<int>(np));
+  SIGE_CUDA(cudaMemcpy(n.scale, sc, np * sizeof(float), cudaMemcpyHostToDevice));
+  SIGE_CUDA(cudaMemcpy(n.shift, sh, np * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void Engine::get_tensor(int step, const std::string& key, float* host, size_t numel) {
+  const DevTensor& t = cache_tensor(step, key);
+  if (numel != t.numel()) throw ConfigError("cache entry " + key + ": size mismatch");
+  std::vector<float> buf(numel);
+  SIGE_CUDA(cudaDeviceSynchronize());
+  SIGE_CUDA(cudaMemcpy(buf.data(), t.p, numel * sizeof(float), cudaMemcpyDeviceToHost));
+  if (t.layout == kNHWC) {
+    for (int n = 0; n < t.n; ++n)
+      for (int ch = 0; ch < t.c; ++ch)
+        for (int y = 0; y < t.h; ++y)
+          for (int x = 0; x < t.w; ++x)
+            host[((static_cast<size_t>(n) * t.c + ch) * t.h + y) * t.w + x] =
+                buf[((static_cast<size_t>(n) * t.h + y) * t.w + x) * t.c + ch];
+  } else {
+    std::memcpy(host, buf.data(), numel * sizeof(float));
+  }
+}
+
+// ------------------------------------------------------- sparse program --
+namespace {
+std::string config_key(const sige_run_config& c) {
+  std::ostringstream o;
+  o << c.step << '|' << c.dilate_full << '|' << c.dilate_scale << '|' << c.block3 << '|' << c.block1
+    << '|' << c.min_sparse_res << '|' << c.norm_precompute;
+  return o.str();
+}
+}  // namespace
+
+struct ProgramBuilder {
+  Engine& E;
+  Program& P;
+  const sige_run_config& cfg;
+  std::map<std::tuple<int, int, int>, int> memo;
+
+  int entry(int h, int w, int b) {  // IndexPlan::at (graph.cpp:517-528)
+    auto key = std::make_tuple(h, w, b);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    const int H = E.in_h_, W = E.in_w_;
+    if (h <= H && w <= W) {
+      if (H % h != 0 || W % w != 0)
+        throw ConfigError("downsample_mask: non-integer scale factor (" + std::to_string(H) + "x" +
+                          std::to_string(W) + " -> " + std::to_string(h) + "x" + std::to_string(w) + ")");
+    } else if (h % H != 0 || w % W != 0) {
+      throw ConfigError("mask: cannot scale " + std::to_string(H) + "x" + std::to_string(W) +
+                        " up to " + std::to_string(h) + "x" + std::to_string(w) +
+                        " (non-integer factor)");
+    }
+    PlanEntryDev e;
+    e.h = h;
+    e.w = w;
+    e.b = b;
+    e.capacity = ((h + b - 1) / b) * ((w + b - 1) / b) * E.batch_;
+    e.idx = static_cast<int32_t*>(E.alloc(static_cast<size_t>(e.capacity) * 3 * sizeof(int32_t)));
+    e.count = static_cast<int32_t*>(E.alloc(sizeof(int32_t)));
+    SIGE_CUDA(cudaMemset(e.count, 0, sizeof(int32_t)));
+    P.entries.push_back(e);
+    return memo[key] = static_cast<int>(P.entries.size()) - 1;
+  }
+
+  Tiles tiles(int ei) const {
+    const PlanEntryDev& e = P.entries[ei];
+    Tiles t;
+    t.idx = e.idx;
+    t.count_dev = e.count;
+    t.capacity = e.capacity;
+    t.bh = t.bw = e.b;
+    return t;
+  }
+
+  void restore(const DevTensor& wbuf, const DevTensor& cache, int ei) {
+    const PlanEntryDev& e = P.entries[ei];
+    RestoreJob j;
+    j.dst = wbuf.p;
+    j.src = cache.p;
+    j.idx = e.idx;
+    j.count = e.count;
+    j.n = wbuf.n;
+    j.c = wbuf.c;
+    j.h = wbuf.h;
+    j.w = wbuf.w;
+    j.b = e.b;
+    j.layout = wbuf.layout;
+    P.restores.push_back(j);
+    P.restore_max = std::max<long long>(P.restore_max, static_cast<long long>(e.capacity) * e.b * e.b * wbuf.c);
+  }
+
+  void add(std::function<void(cudaStream_t)> f, int launches = 1) {
+    P.steps.push_back(std::move(f));
+    P.launches += launches;
+  }
+
+  void conv_step(const Src& s, const Tiles& t, const ConvW& cw, const Dst& d) {
+    Engine* eng = &E;
+    add([eng, s, t, cw, d](cudaStream_t st) { eng->conv(s, t, cw, d, st); });
+  }
+
+  void build() {
+    const int step = cfg.step;
+    const int N = E.batch_;
+    // Flow (graph.cpp:538-569). The input source pointer is bound per call.
+    Src flow;
+    flow.ptr = nullptr;  // bound to cur_in_ below
+    flow.layout = kNCHW;
+    flow.n = N;
+    flow.c = E.in_c_;
+    flow.h = E.in_h_;
+    flow.w = E.in_w_;
+    flow.epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+    bool flow_is_input = true;
+    bool has_blocks = false;
+    int blocks_entry = -1;
+    Engine* eng = &E;
+    // Source pointer resolution at launch time for steps that read the input.
+    auto bind = [eng](Src s, bool is_input) {
+      if (is_input) s.ptr = eng->cur_in_;
+      return s;
+    };
+    for (size_t i = 0; i < E.layers_.size(); ++i) {
+      const LayerDev& L = E.layers_[i];
+      const LayerShape& sh = E.shapes_[i];
+      const std::string key = lk(static_cast<int>(i));
+      const bool fin = flow_is_input;
+      switch (L.kind) {
+        case SIGE_LAYER_CONV:
+        case SIGE_LAYER_DOWNSAMPLE: {
+          const ConvW cw = L.conv;
+          TraceInfo tr{-1, cw.c_in, cw.c_out, cw.k, cw.stride, sh.h_out, sh.w_out, N};
+          Src s = flow;
+          if (!runs_sparse(L, flow.h, flow.w, cfg)) {
+            DevTensor& o = E.scratch("sparse." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
+            Tiles t = E.dense_tiles(sh.h_out, sh.w_out);
+            Dst d = to_dst(o);
+            add([eng, s, t, cw, d, fin, bind](cudaStream_t st) { eng->conv(bind(s, fin), t, cw, d, st); });
+            flow = plain(o);
+            has_blocks = false;
+          } else {
+            const int ei = entry(sh.h_out, sh.w_out, cw.k == 3 ? cfg.block3 : cfg.block1);
+            tr.entry = ei;
+            DevTensor& wb = E.work_buffer(step, key + ".out");
+            const DevTensor& cb = E.cache_tensor(step, key + ".out");
+            Tiles t = tiles(ei);
+            Dst d = to_dst(wb);
+            add([eng, s, t, cw, d, fin, bind](cudaStream_t st) { eng->conv(bind(s, fin), t, cw, d, st); });
+            restore(wb, cb, ei);
+            flow = plain(wb);
+            has_blocks = true;
+            blocks_entry = ei;
+          }
+          P.trace.push_back(tr);
+          flow_is_input = false;
+          break;
+        }
+        case SIGE_LAYER_NORM: {
+          if (L.norm_kind == SIGE_NORM_BATCH || cfg.norm_precompute) {
+            const DevNorm& f = E.cache_norm(step, key + ".norm");
+            epi_push_ss(flow.epi, f.scale, f.shift, f.np, flow.c);
+          } else {
+            // flush + fresh statistics (graph.cpp:745-750).
+            DevTensor& full = E.scratch("sparse." + key + ".flush", flow.c, flow.h, flow.w, kNHWC);
+            const int np = N * L.channels;
+            DevNorm& f = E.scratch_norm("sparse." + key + ".norm", np);
+            Src s = flow;
+            DevTensor fullc = full;
+            DevNorm fc = f;
+            LayerDev Lc = L;
+            add([eng, s, fullc, fc, Lc, fin, bind](cudaStream_t st) mutable {
+              launch_materialize(bind(s, fin), fullc.p, kNHWC, st);
+              eng->fold_norm(Lc, plain(fullc), fc, st);
+            }, 2);
+            flow = plain(full);
+            epi_push_ss(flow.epi, f.scale, f.shift, np, flow.c);
+            flow_is_input = false;
+            has_blocks = false;
+          }
+          break;
+        }
+        case SIGE_LAYER_ACTIVATION:
+          epi_push_act(flow.epi, L.act);
+          break;
+        case SIGE_LAYER_UPSAMPLE:
+          flow.up += 1;
+          flow.h *= 2;
+          flow.w *= 2;
+          has_blocks = false;  // materialize (graph.cpp:762-770)
+          break;
+        case SIGE_LAYER_RESBLOCK: {
+          const int h = flow.h, w = flow.w, c1 = L.conv.c_out, co = L.conv2.c_out;
+          Src x0 = flow;
+          if (!runs_sparse(L, h, w, cfg)) {
+            // Dense fallback (graph.cpp:799-815): fresh statistics always.
+            DevTensor& m1 = E.scratch("sparse." + key + ".conv1", c1, h, w, kNHWC);
+            DevTensor& o = E.scratch("sparse." + key + ".sum", co, h, w, kNHWC);
+            const int np = L.norm_kind == SIGE_NORM_BATCH ? L.channels : N * L.channels;
+            DevNorm& f = E.scratch_norm("sparse." + key + ".norm1", np);
+            Tiles t = E.dense_tiles(h, w);
+            ConvW c1w = L.conv, c2w = L.conv2, scw = L.shortcut;
+            LayerDev Lc = L;
+            DevTensor m1c = m1;
+            DevNorm fc = f;
+            Src mid = plain(m1);
+            epi_push_ss(mid.epi, f.scale, f.shift, np, c1);
+            epi_push_act(mid.epi, L.act);
+            Dst d = to_dst(o, kAddSrc);
+            DevTensor* scd = nullptr;
+            if (L.has_shortcut) scd = &E.scratch("sparse." + key + ".shortcut", co, h, w, kNHWC);
+            DevTensor scc = scd ? *scd : DevTensor{};
+            const bool has_sc = L.has_shortcut != 0;
+            add([eng, x0, t, c1w, c2w, scw, Lc, m1c, fc, mid, d, scc, has_sc, fin, bind](cudaStream_t st) mutable {
+              Src xin = bind(x0, fin);
+              eng->conv(xin, t, c1w, to_dst(m1c), st);
+              eng->fold_norm(Lc, plain(m1c), fc, st);
+              Dst dd = d;
+              if (has_sc) {
+                eng->conv(xin, t, scw, to_dst(scc), st);
+                dd.addend = plain(scc);
+              } else {
+                dd.addend = xin;
+              }
+              eng->conv(mid, t, c2w, dd, st);
+            }, L.has_shortcut ? 4 : 3);
+            P.trace.push_back({-1, L.conv.c_in, c1, 3, 1, h, w, N});
+            P.trace.push_back({-1, c1, co, 3, 1, h, w, N});
+            if (L.has_shortcut) P.trace.push_back({-1, L.shortcut.c_in, co, 1, 1, h, w, N});
+            flow = plain(o);
+          } else {
+            const int em = entry(h, w, cfg.block3), es = entry(h, w, cfg.block1);
+            DevTensor& w1 = E.work_buffer(step, key + ".conv1.out");
+            const DevTensor& c1c = E.cache_tensor(step, key + ".conv1.out");
+            DevTensor& ws = E.work_buffer(step, key + ".sum");
+            const DevTensor& csum = E.cache_tensor(step, key + ".sum");
+            const DevTensor& osc = E.cache_tensor(step, key + ".shortcut.out");
+            Tiles tm = tiles(em), ts = tiles(es);
+            ConvW c1w = L.conv, c2w = L.conv2, scw = L.shortcut;
+            // 1. conv1 over main tiles -> W(conv1.out)
+            Dst d1 = to_dst(w1);
+            add([eng, x0, tm, c1w, d1, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), tm, c1w, d1, st); });
+            restore(w1, c1c, em);
+            // 2. conv2 on scatter_gather(m1) with norm1 + act (graph.cpp:821-846)
+            Src mid = plain(w1);
+            if (L.norm_kind == SIGE_NORM_BATCH || cfg.norm_precompute) {
+              const DevNorm& f = E.cache_norm(step, key + ".norm1");
+              epi_push_ss(mid.epi, f.scale, f.shift, f.np, c1);
+            } else {
+              const int np = N * L.channels;
+              DevNorm& f = E.scratch_norm("sparse." + key + ".norm1", np);
+              LayerDev Lc = L;
+              DevNorm fc = f;
+              Src w1s = plain(w1);
+              add([eng, Lc, fc, w1s](cudaStream_t st) mutable { eng->fold_norm(Lc, w1s, fc, st); });
+              epi_push_ss(mid.epi, f.scale, f.shift, np, c1);
+            }
+            epi_push_act(mid.epi, L.act);
+            Dst d2 = to_dst(ws, kResMain);
+            d2.aux = osc.p;
+            conv_step(mid, tm, c2w, d2);
+            restore(ws, csum, em);
+            // 3. shortcut tiles (graph.cpp:854-879)
+            Dst d3 = to_dst(ws, kResShortcut);
+            d3.aux = osc.p;
+            if (L.has_shortcut) {
+              add([eng, x0, ts, scw, d3, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), ts, scw, d3, st); });
+            } else {
+              add([x0, ts, d3, fin, bind](cudaStream_t st) { launch_identity_join(bind(x0, fin), ts, d3, st); });
+            }
+            restore(ws, csum, es);
+            P.trace.push_back({em, L.conv.c_in, c1, 3, 1, h, w, N});
+            P.trace.push_back({em, c1, co, 3, 1, h, w, N});
+            if (L.has_shortcut) P.trace.push_back({es, L.shortcut.c_in, co, 1, 1, h, w, N});
+            flow = plain(ws);
+          }
+          flow_is_input = false;
+          has_blocks = false;
+          break;
+        }
+      }
+    }
+    // Final output (graph.cpp:891-900).
+    const DevTensor& cfin = E.cache_tensor(step, "final");
+    Src result = flow;
+    bool result_is_input = flow_is_input;
+    if (has_blocks) {
+      DevTensor& wf = E.work_buffer(step, "final");
+      Tiles t = tiles(blocks_entry);
+      Src s = flow;
+      DevTensor wfc = wf;
+      add([s, t, wfc](cudaStream_t st) { launch_tiles_apply(s, t, wfc.p, kNCHW, st); });
+      restore(wf, cfin, blocks_entry);
+      result = plain(wf);
+      result_is_input = false;
+    }
+    // finalize: out = any(mask) ? result : cached final (empty-mask
+    // short-circuit, graph.cpp:665-668), full NCHW copy.
+    const float* cfp = cfin.p;
+    int32_t* anyp = P.any;
+    add([eng, result, result_is_input, cfp, anyp, bind](cudaStream_t st) {
+      launch_finalize(bind(result, result_is_input), cfp, anyp, eng->cur_out_, st);
+    });
+  }
+};
+
+Program& Engine::program(const sige_run_config& cfg) {
+  const std::string key = config_key(cfg);
+  auto it = programs_.find(key);
+  if (it != programs_.end()) return *it->second;
+  auto P = std::make_unique<Program>();
+  P->full_h = in_h_;
+  P->full_w = in_w_;
+  P->dilate_full = cfg.dilate_full;
+  P->dilate_scale = cfg.dilate_scale;
+  P->bits = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * in_h_ * ((in_w_ + 31) / 32)));
+  P->any = static_cast<int32_t*>(alloc(sizeof(int32_t)));
+  ProgramBuilder b{*this, *P, cfg, {}};
+  b.build();
+  if (!P->entries.empty()) {
+    P->entries_dev = static_cast<PlanEntryDev*>(alloc(P->entries.size() * sizeof(PlanEntryDev)));
+    SIGE_CUDA(cudaMemcpy(P->entries_dev, P->entries.data(), P->entries.size() * sizeof(PlanEntryDev),
+                         cudaMemcpyHostToDevice));
+  }
+  if (!P->restores.empty()) {
+    P->restores_dev = static_cast<RestoreJob*>(alloc(P->restores.size() * sizeof(RestoreJob)));
+    SIGE_CUDA(cudaMemcpy(P->restores_dev, P->restores.data(), P->restores.size() * sizeof(RestoreJob),
+                         cudaMemcpyHostToDevice));
+  }
+  Program& ref = *P;
+  programs_[key] = std::move(P);
+  return ref;
+}
+
+void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige_run_config& cfg,
+                            float* out, cudaStream_t st) {
+  // RunConfig::validate (graph.cpp:220-227)
+  if (cfg.mask_threshold < 0.0f) throw ConfigError("config: threshold must be >= 0");
+  if (cfg.dilate_full < 0 || cfg.dilate_scale < 0) throw ConfigError("config: dilation radii must be >= 0");
+  if (cfg.block3 < 1 || cfg.block1 < 1) throw ConfigError("config: block sizes must be >= 1");
+  if (cfg.step < 0) throw ConfigError("config: step must be >= 0");
+  const uint64_t before = g_launches.load();
+  if (!cfg.sparse) {  // graph.cpp:626-663: plain dense forward
+    dense_forward(edited, false, cfg.step, out, st);
+    last_launches_ = static_cast<int>(g_launches.load() - before);
+    return;
+  }
+  Program& P = program(cfg);
+  // Lazy restore of the tiles the previous call dirtied.
+  if (last_program_ && !last_program_->restores.empty())
+    launch_restore(last_program_->restores_dev, static_cast<int>(last_program_->restores.size()),
+                   static_cast<int>(std::min<long long>(last_program_->restore_max, 1LL << 30)), st);
+  cur_in_ = edited;
+  cur_out_ = out;
+  // Mask -> bits (compute_difference_mask against the cached original input
+  // when no mask is given), then the IndexPlan.
+  SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
+  if (mask) {
+    launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st);
+  } else {
+    const DevTensor& orig = cache_tensor(cfg.step, "input");
+    launch_mask_bits(orig.p, edited, batch_, in_c_, in_h_, in_w_, cfg.mask_threshold, P.bits,
+                     nullptr, P.any, st);
+  }
+  launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
+              static_cast<int>(P.entries.size()), st);
+  for (auto& f : P.steps) f(st);
+  last_program_ = &P;
+  last_launches_ = static_cast<int>(g_launches.load() - before);
+}
+
+int Engine::trace(uint64_t* rows, int cap, cudaStream_t st) {
+  if (!last_program_) return 0;
+  Program& P = *last_program_;
+  std::vector<int32_t> counts(P.entries.size());
+  for (size_t i = 0; i < P.entries.size(); ++i)
+    SIGE_CUDA(cudaMemcpyAsync(&counts[i], P.entries[i].count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  int32_t any = 0;
+  SIGE_CUDA(cudaMemcpyAsync(&any, P.any, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SIGE_CUDA(cudaStreamSynchronize(st));
+  if (!any) return 0;  // short-circuit: no trace rows (graph.cpp:665-668)
+  int n = 0;
+  for (const TraceInfo& t : P.trace) {
+    if (n < cap && rows) {
+      uint64_t* r = rows + 6 * n;
+      const uint64_t dense = static_cast<uint64_t>(t.c_out) * t.c_in * t.k * t.k * t.oh * t.ow * t.batch;
+      if (t.entry < 0) {
+        r[0] = r[1] = r[2] = 0;
+        r[3] = r[4] = dense;
+        r[5] = 0;
+      } else {
+        const int b = P.entries[t.entry].b;
+        const uint64_t g = static_cast<uint64_t>(counts[t.entry]);
+        const int win = t.stride * b + t.k - t.stride;
+        r[0] = g;
+        r[1] = g * t.c_in * win * win;
+        r[2] = g * t.c_out * b * b;
+        r[3] = g * t.c_out * t.c_in * t.k * t.k * b * b;
+        r[4] = dense;
+        r[5] = 1;
+      }
+    }
+    ++n;
+  }
+  return n;
+}
+
+}  // namespace sige_b200

@@ -1,0 +1,122 @@
+// engine.hpp — device-resident ActivationCache + sparse executor.
+//
+// Mirrors, on the device, the reference's graph layer
+// (proj/include/sige/graph.hpp:116-226, proj/src/graph.cpp:343-901):
+//   * ActivationCache: (step, key) -> NHWC device tensor / folded norm params;
+//   * precompute / dense_forward(_reused_stats): the dense walk;
+//   * sparse_forward: the Flow executor, compiled once per (step, RunConfig)
+//     into a "program" — an ordered list of kernel launches over device-side
+//     index sets produced by the on-device IndexPlan, so a call never
+//     synchronises with the host.
+// Scatters write tiles into per-key working copies of the cached outputs
+// ("W" buffers) instead of copying whole tensors (kernels.cpp:108-112); the
+// tiles a call dirtied are restored from the cache at the start of the next
+// call, so the cache itself stays immutable.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.hpp"
+#include "engine_kernels.hpp"
+#include "models.hpp"
+
+namespace sige_b200 {
+
+struct DevTensor {
+  float* p = nullptr;
+  int n = 0, c = 0, h = 0, w = 0;
+  int layout = kNHWC;
+  size_t numel() const { return static_cast<size_t>(n) * c * h * w; }
+};
+
+struct DevNorm {
+  float* scale = nullptr;
+  float* shift = nullptr;
+  int np = 0;
+};
+
+struct LayerDev {
+  int kind = 0, act = 0, has_shortcut = 0, policy_sparse = 1, min_resolution = 16;
+  ConvW conv, conv2, shortcut;
+  int norm_kind = 0, groups = 1, channels = 0;
+  float eps = 1e-5f;
+  float *gamma = nullptr, *beta = nullptr, *rmean = nullptr, *rvar = nullptr;
+};
+
+struct TraceInfo {
+  int entry = -1;  // plan entry (sparse) or -1 (dense)
+  int c_in = 0, c_out = 0, k = 1, stride = 1, oh = 0, ow = 0, batch = 1;
+};
+
+struct Program;
+
+class Engine {
+ public:
+  Engine(const sige_model_desc* model, int batch, int math);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  void precompute(const float* original_nchw, int step, cudaStream_t st);
+  void put_tensor(int step, const std::string& key, const float* host_nchw, size_t numel);
+  void put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np);
+  void get_tensor(int step, const std::string& key, float* host_nchw, size_t numel);
+  void sparse_forward(const float* edited, const uint8_t* mask, const sige_run_config& cfg,
+                      float* out, cudaStream_t st);
+  void dense_forward(const float* in, bool reused_stats, int step, float* out, cudaStream_t st);
+
+  void output_shape(int* n, int* c, int* h, int* w) const;
+  int last_launch_count() const { return last_launches_; }
+  int trace(uint64_t* rows, int cap, cudaStream_t st);
+  size_t cache_bytes() const;
+  int in_channels() const { return in_c_; }
+  int in_h() const { return in_h_; }
+  int in_w() const { return in_w_; }
+  int batch() const { return batch_; }
+
+ private:
+  friend struct ProgramBuilder;
+  // conv dispatch by math mode
+  void conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& dst, cudaStream_t st) const;
+  const DevTensor& cache_tensor(int step, const std::string& key) const;
+  const DevNorm& cache_norm(int step, const std::string& key) const;
+  DevTensor& cache_slot(int step, const std::string& key, int c, int h, int w, int layout);
+  DevNorm& norm_slot(int step, const std::string& key, int np);
+  DevTensor& work_buffer(int step, const std::string& key);
+  DevTensor& scratch(const std::string& key, int c, int h, int w, int layout);
+  DevNorm& scratch_norm(const std::string& key, int np);
+  Tiles dense_tiles(int oh, int ow);
+  void invalidate_programs();
+  void dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
+                  cudaStream_t st);
+  Program& program(const sige_run_config& cfg);
+  void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
+
+  std::string name_;
+  int batch_, math_, in_c_, in_h_, in_w_;
+  int out_c_ = 0, out_h_ = 0, out_w_ = 0;
+  std::vector<LayerDev> layers_;
+  std::vector<LayerShape> shapes_;
+  std::vector<void*> allocations_;
+  std::map<std::pair<int, std::string>, DevTensor> cache_;
+  std::map<std::pair<int, std::string>, DevNorm> norms_;
+  std::map<std::pair<int, std::string>, DevTensor> work_;
+  std::map<std::string, DevTensor> scratch_;
+  std::map<std::string, DevNorm> scratch_norms_;
+  std::map<std::pair<int, int>, std::pair<int32_t*, int>> dense_tiles_;
+  std::map<std::string, std::unique_ptr<Program>> programs_;
+  Program* last_program_ = nullptr;
+  int last_launches_ = 0;
+  // per-call bindings read by program steps
+  const float* cur_in_ = nullptr;
+  float* cur_out_ = nullptr;
+  void* alloc(size_t bytes);
+};
+
+}  // namespace sige_b200

@@ -1,0 +1,539 @@
+// engine_kernels.cu — the engine's HBM-bound kernels: difference mask to a
+// bit mask, the on-device IndexPlan (deterministic tile compaction), GroupNorm
+// statistics, final-tile application, restores and layout conversions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "common.hpp"
+#include "engine_kernels.hpp"
+
+namespace sige_b200 {
+
+namespace {
+
+inline int grid_cap(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  long long cap = static_cast<long long>(sm_count()) * 16;
+  return static_cast<int>(std::max(1LL, std::min(g, cap)));
+}
+
+// ------------------------------------------------------ difference mask --
+// compute_difference_mask (mask.cpp:14-32) straight into a row-major bit mask
+// (ceil(W/32) words per row). grid.y splits the N*C planes; set bits are
+// merged with atomicOr, so the result is order-independent.
+__global__ void k_mask_bits(const float* __restrict__ o, const float* __restrict__ e, int planes,
+                            int ppy, int h, int w, float thr, uint32_t* __restrict__ bits,
+                            uint8_t* __restrict__ mask_u8, int32_t* __restrict__ any) {
+  const long long hw = static_cast<long long>(h) * w;
+  const int wpr = (w + 31) >> 5;
+  const int p0 = blockIdx.y * ppy, p1 = min(planes, p0 + ppy);
+  const bool vec = (w & 3) == 0;
+  const long long nq = vec ? hw >> 2 : hw;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq;
+       q += (long long)gridDim.x * blockDim.x) {
+    uint32_t set = 0;  // bit j: pixel (vec ? 4q + j : q)
+    if (vec) {
+      for (int p = p0; p < p1; ++p) {
+        float4 a = __ldg(reinterpret_cast<const float4*>(o + p * hw) + q);
+        float4 b = __ldg(reinterpret_cast<const float4*>(e + p * hw) + q);
+        set |= (fabsf(__fsub_rn(b.x, a.x)) > thr ? 1u : 0u) | (fabsf(__fsub_rn(b.y, a.y)) > thr ? 2u : 0u) |
+               (fabsf(__fsub_rn(b.z, a.z)) > thr ? 4u : 0u) | (fabsf(__fsub_rn(b.w, a.w)) > thr ? 8u : 0u);
+        if (set == 15u) break;
+      }
+    } else {
+      for (int p = p0; p < p1 && !set; ++p)
+        set = fabsf(__fsub_rn(__ldg(e + p * hw + q), __ldg(o + p * hw + q))) > thr ? 1u : 0u;
+    }
+    if (!set) continue;
+    *any = 1;
+    long long pix = vec ? (q << 2) : q;
+    int y = static_cast<int>(pix / w), x = static_cast<int>(pix % w);
+    for (int j = 0; j < (vec ? 4 : 1); ++j) {
+      if (!(set >> j & 1u)) continue;
+      atomicOr(bits + static_cast<long long>(y) * wpr + ((x + j) >> 5), 1u << ((x + j) & 31));
+      if (mask_u8) mask_u8[pix + j] = 1;
+    }
+  }
+}
+
+__global__ void k_mask_u8_to_bits(const uint8_t* __restrict__ m, int h, int w, uint32_t* bits,
+                                  int32_t* __restrict__ any) {
+  const int wpr = (w + 31) >> 5;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)h * wpr;
+       q += (long long)gridDim.x * blockDim.x) {
+    int y = static_cast<int>(q / wpr), wd = static_cast<int>(q % wpr);
+    uint32_t v = 0;
+    for (int j = 0; j < 32; ++j) {
+      int x = wd * 32 + j;
+      if (x < w && m[static_cast<long long>(y) * w + x]) v |= 1u << j;
+    }
+    bits[q] = v;
+    if (v) *any = 1;
+  }
+}
+
+// -------------------------------------------------------------- plan ----
+__device__ __forceinline__ bool rect_any(const uint32_t* bits, int wpr, int y0, int y1, int x0,
+                                         int x1) {
+  int wa = x0 >> 5, wb = x1 >> 5;
+  uint32_t ma = 0xffffffffu << (x0 & 31);
+  uint32_t mb = 0xffffffffu >> (31 - (x1 & 31));
+  for (int y = y0; y <= y1; ++y) {
+    const uint32_t* row = bits + static_cast<long long>(y) * wpr;
+    if (wa == wb) {
+      if (row[wa] & ma & mb) return true;
+    } else {
+      if (row[wa] & ma) return true;
+      for (int k = wa + 1; k < wb; ++k)
+        if (row[k]) return true;
+      if (row[wb] & mb) return true;
+    }
+  }
+  return false;
+}
+
+// One CTA per plan entry. The rectangle for tile (R, C): its clipped pixels
+// dilated by dilate_scale at the entry resolution, mapped to full resolution
+// (max-pool down: factor f rows per cell; replicate up: y/u), dilated by
+// dilate_full, clipped — composition of dilate_mask (mask.cpp:55-80),
+// downsample_mask (mask.cpp:34-53) / replicate_mask (graph.cpp:485-500) and
+// the "any pixel in tile" test of mask_to_block_indices (mask.cpp:113-127).
+__global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df, int ds, int batch,
+                       const PlanEntryDev* __restrict__ entries, int use_smem) {
+  extern __shared__ uint32_t sbits[];
+  __shared__ int warp_sums[32];
+  __shared__ int base;
+  const int wpr = (W + 31) >> 5;
+  const uint32_t* bits = gbits;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < H * wpr; i += blockDim.x) sbits[i] = gbits[i];
+    bits = sbits;
+  }
+  const PlanEntryDev e = entries[blockIdx.x];
+  const int h = e.h, w = e.w, b = e.b;
+  const int ty = (h + b - 1) / b, tx = (w + b - 1) / b, tiles = ty * tx;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool down_y = h <= H, down_x = w <= W;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    bool on = false;
+    int R = 0, Cc = 0;
+    if (t < tiles) {
+      R = (t / tx) * b;
+      Cc = (t % tx) * b;
+      int ly0 = max(0, R - ds), ly1 = min(h - 1, min(h, R + b) - 1 + ds);
+      int lx0 = max(0, Cc - ds), lx1 = min(w - 1, min(w, Cc + b) - 1 + ds);
+      int fy0, fy1, fx0, fx1;
+      if (down_y) {
+        int f = H / h;
+        fy0 = ly0 * f;
+        fy1 = ly1 * f + f - 1;
+      } else {
+        int u = h / H;
+        fy0 = ly0 / u;
+        fy1 = ly1 / u;
+      }
+      if (down_x) {
+        int f = W / w;
+        fx0 = lx0 * f;
+        fx1 = lx1 * f + f - 1;
+      } else {
+        int u = w / W;
+        fx0 = lx0 / u;
+        fx1 = lx1 / u;
+      }
+      fy0 = max(0, fy0 - df);
+      fy1 = min(H - 1, fy1 + df);
+      fx0 = max(0, fx0 - df);
+      fx1 = min(W - 1, fx1 + df);
+      on = rect_any(bits, wpr, fy0, fy1, fx0, fx1);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) warp_sums[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
+      }
+      if (lane < nw) warp_sums[lane] = v;
+    }
+    __syncthreads();
+    const int slot = base + (wid ? warp_sums[wid - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+    if (on && slot < e.capacity) {
+      e.idx[3 * slot] = 0;
+      e.idx[3 * slot + 1] = R;
+      e.idx[3 * slot + 2] = Cc;
+    }
+    const int chunk_total = warp_sums[nw - 1];
+    __syncthreads();
+    if (threadIdx.x == 0) base += chunk_total;
+    __syncthreads();
+  }
+  const int per = base;
+  for (int n = 1; n < batch; ++n)
+    for (int i = threadIdx.x; i < per; i += blockDim.x) {
+      const int d = n * per + i;
+      if (d < e.capacity) {
+        e.idx[3 * d] = n;
+        e.idx[3 * d + 1] = e.idx[3 * i + 1];
+        e.idx[3 * d + 2] = e.idx[3 * i + 2];
+      }
+    }
+  if (threadIdx.x == 0) *e.count = min(per * batch, e.capacity);
+}
+
+// ------------------------------------------------------------ GroupNorm --
+// compute_norm_stats + fold_stats (norm.cpp:25-90). Exact: one thread per
+// (n, group) with the reference's sequential double sums (channel in group,
+// rows, columns), so mean/var round identically.
+__global__ void k_gn_exact(Src x, int groups, float eps, const float* __restrict__ gamma,
+                           const float* __restrict__ beta, float* __restrict__ scale,
+                           float* __restrict__ shift) {
+  const int cpg = x.c / groups;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < x.n * groups; q += gridDim.x * blockDim.x) {
+    const int n = q / groups, g = q % groups;
+    const double count = static_cast<double>(cpg) * x.h * x.w;
+    double sum = 0.0;
+    for (int ic = g * cpg; ic < (g + 1) * cpg; ++ic)
+      for (int y = 0; y < x.h; ++y)
+        for (int xx = 0; xx < x.w; ++xx) sum = __dadd_rn(sum, static_cast<double>(src_val(x, n, ic, y, xx)));
+    const double mean = __ddiv_rn(sum, count);
+    double sq = 0.0;
+    for (int ic = g * cpg; ic < (g + 1) * cpg; ++ic)
+      for (int y = 0; y < x.h; ++y)
+        for (int xx = 0; xx < x.w; ++xx) {
+          double d = __dadd_rn(static_cast<double>(src_val(x, n, ic, y, xx)), -mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+    const float fmean = __double2float_rn(mean), fvar = __double2float_rn(__ddiv_rn(sq, count));
+    for (int ic = g * cpg; ic < (g + 1) * cpg; ++ic) {
+      const float s = __fdiv_rn(gamma[ic], __fsqrt_rn(__fadd_rn(fvar, eps)));
+      scale[n * x.c + ic] = s;
+      shift[n * x.c + ic] = __fsub_rn(beta[ic], __fmul_rn(fmean, s));
+    }
+  }
+}
+
+// Parallel tree version: CTA per (n, group), double partial sums.
+__global__ void k_gn_fast(Src x, int groups, float eps, const float* __restrict__ gamma,
+                          const float* __restrict__ beta, float* __restrict__ scale,
+                          float* __restrict__ shift) {
+  __shared__ double red[32];
+  __shared__ double s_mean;
+  const int n = blockIdx.x / groups, g = blockIdx.x % groups;
+  const int cpg = x.c / groups;
+  const long long per = static_cast<long long>(cpg) * x.h * x.w;
+  const double count = static_cast<double>(per);
+  auto reduce = [&](double v) -> double {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+      t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    __syncthreads();
+    return t;
+  };
+  // element q of the group: channel-fastest for NHWC coalescing
+  double s = 0.0;
+  for (long long q = threadIdx.x; q < per; q += blockDim.x) {
+    int ic = g * cpg + static_cast<int>(q % cpg);
+    long long pix = q / cpg;
+    s += static_cast<double>(src_val(x, n, ic, static_cast<int>(pix / x.w), static_cast<int>(pix % x.w)));
+  }
+  s = reduce(s);
+  if (threadIdx.x == 0) s_mean = s / count;
+  __syncthreads();
+  const double mean = s_mean;
+  double sq = 0.0;
+  for (long long q = threadIdx.x; q < per; q += blockDim.x) {
+    int ic = g * cpg + static_cast<int>(q % cpg);
+    long long pix = q / cpg;
+    double d = static_cast<double>(src_val(x, n, ic, static_cast<int>(pix / x.w), static_cast<int>(pix % x.w))) - mean;
+    sq += d * d;
+  }
+  sq = reduce(sq);
+  if (threadIdx.x < cpg) {
+    const int ic = g * cpg + threadIdx.x;
+    const float fmean = static_cast<float>(mean), fvar = static_cast<float>(sq / count);
+    const float sc = __fdiv_rn(gamma[ic], __fsqrt_rn(__fadd_rn(fvar, eps)));
+    scale[n * x.c + ic] = sc;
+    shift[n * x.c + ic] = __fsub_rn(beta[ic], __fmul_rn(fmean, sc));
+  }
+}
+
+__global__ void k_bn_fold(int c, float eps, const float* gamma, const float* beta, const float* rm,
+                          const float* rv, float* scale, float* shift) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const float s = __fdiv_rn(gamma[i], __fsqrt_rn(__fadd_rn(rv[i], eps)));
+    scale[i] = s;
+    shift[i] = __fsub_rn(beta[i], __fmul_rn(rm[i], s));
+  }
+}
+
+// ------------------------------------------------------- elementwise ----
+__global__ void k_materialize(Src s, float* __restrict__ dst, int dst_layout) {
+  const long long total = static_cast<long long>(s.n) * s.c * s.h * s.w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int n, ch, y, x;
+    if (dst_layout == kNHWC) {
+      ch = static_cast<int>(q % s.c);
+      long long p = q / s.c;
+      x = static_cast<int>(p % s.w);
+      p /= s.w;
+      y = static_cast<int>(p % s.h);
+      n = static_cast<int>(p / s.h);
+    } else {
+      x = static_cast<int>(q % s.w);
+      long long p = q / s.w;
+      y = static_cast<int>(p % s.h);
+      p /= s.h;
+      ch = static_cast<int>(p % s.c);
+      n = static_cast<int>(p / s.c);
+    }
+    dst[q] = src_val(s, n, ch, y, x);
+  }
+}
+
+// Per tile element helper: maps a flat index over (tile, pixel, channel) with
+// channel fastest; returns false when the tile is inactive or the pixel is
+// outside the canvas (fringe clipping, kernels.cpp:93-95).
+__device__ __forceinline__ bool tile_elem(const Tiles& t, int count, int c, int h, int w,
+                                          long long q, int& n, int& y, int& x, int& ch) {
+  const long long per = static_cast<long long>(t.bh) * t.bw * c;
+  const long long g = q / per;
+  if (g >= count) return false;
+  int rem = static_cast<int>(q - g * per);
+  ch = rem % c;
+  int cell = rem / c;
+  n = t.idx[3 * g];
+  y = t.idx[3 * g + 1] + cell / t.bw;
+  x = t.idx[3 * g + 2] + cell % t.bw;
+  return y < h && x < w;
+}
+
+__global__ void k_tiles_apply(Src s, Tiles t, float* __restrict__ dst, int dst_layout) {
+  const int count = t.count_dev ? *t.count_dev : t.count;
+  const long long total = static_cast<long long>(count) * t.bh * t.bw * s.c;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int n, y, x, ch;
+    if (!tile_elem(t, count, s.c, s.h, s.w, q, n, y, x, ch)) continue;
+    size_t off = dst_layout == kNHWC ? ((static_cast<size_t>(n) * s.h + y) * s.w + x) * s.c + ch
+                                     : ((static_cast<size_t>(n) * s.c + ch) * s.h + y) * s.w + x;
+    dst[off] = src_val(s, n, ch, y, x);
+  }
+}
+
+__global__ void k_identity_join(Src s, Tiles t, Dst d) {
+  const int count = t.count_dev ? *t.count_dev : t.count;
+  const long long total = static_cast<long long>(count) * t.bh * t.bw * d.c;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int n, y, x, ch;
+    if (!tile_elem(t, count, d.c, d.h, d.w, q, n, y, x, ch)) continue;
+    const size_t p = ((static_cast<size_t>(n) * d.h + y) * d.w + x) * d.c + ch;
+    d.ptr[p] = __fadd_rn(d.ptr[p], __fsub_rn(src_val(s, n, ch, y, x), d.aux[p]));
+  }
+}
+
+__global__ void k_restore(const RestoreJob* __restrict__ jobs, int max_tiles) {
+  const RestoreJob j = jobs[blockIdx.y];
+  const int count = min(*j.count, max_tiles);
+  const long long per = static_cast<long long>(j.b) * j.b * j.c;
+  const long long total = static_cast<long long>(count) * per;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long g = q / per;
+    int rem = static_cast<int>(q - g * per);
+    int ch, cell;
+    if (j.layout == kNHWC) {
+      ch = rem % j.c;
+      cell = rem / j.c;
+    } else {
+      cell = rem % (j.b * j.b);
+      ch = rem / (j.b * j.b);
+    }
+    const int n = j.idx[3 * g], y = j.idx[3 * g + 1] + cell / j.b, x = j.idx[3 * g + 2] + cell % j.b;
+    if (y >= j.h || x >= j.w) continue;
+    const size_t off = j.layout == kNHWC ? ((static_cast<size_t>(n) * j.h + y) * j.w + x) * j.c + ch
+                                         : ((static_cast<size_t>(n) * j.c + ch) * j.h + y) * j.w + x;
+    j.dst[off] = j.src[off];
+  }
+}
+
+__global__ void k_finalize(Src r, const float* __restrict__ cached, const int32_t* __restrict__ any,
+                           float* __restrict__ out) {
+  const bool use = *any != 0;
+  const long long total = static_cast<long long>(r.n) * r.c * r.h * r.w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    if (!use) {
+      out[q] = cached[q];
+      continue;
+    }
+    const int x = static_cast<int>(q % r.w);
+    long long p = q / r.w;
+    const int y = static_cast<int>(p % r.h);
+    p /= r.h;
+    out[q] = src_val(r, static_cast<int>(p / r.c), static_cast<int>(p % r.c), y, x);
+  }
+}
+
+__global__ void k_add(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ o,
+                      long long n) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    o[q] = __fadd_rn(a[q], b[q]);
+}
+
+__global__ void k_nchw_to_nhwc(const float* __restrict__ in, float* __restrict__ out, int n, int c,
+                               int h, int w) {
+  const long long total = static_cast<long long>(n) * c * h * w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int ch = static_cast<int>(q % c);
+    long long p = q / c;  // (n, y, x)
+    long long hw = static_cast<long long>(h) * w;
+    long long nn = p / hw, pix = p % hw;
+    out[q] = in[(nn * c + ch) * hw + pix];
+  }
+}
+
+__global__ void k_nhwc_to_nchw(const float* __restrict__ in, float* __restrict__ out, int n, int c,
+                               int h, int w) {
+  const long long total = static_cast<long long>(n) * c * h * w;
+  const long long hw = static_cast<long long>(h) * w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long pix = q % hw;
+    long long p = q / hw;
+    int ch = static_cast<int>(p % c);
+    long long nn = p / c;
+    out[q] = in[(nn * hw + pix) * c + ch];
+  }
+}
+
+}  // namespace
+
+void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
+                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st) {
+  const int wpr = (w + 31) >> 5;
+  SIGE_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * h * wpr, st));
+  if (mask_u8) SIGE_CUDA(cudaMemsetAsync(mask_u8, 0, static_cast<size_t>(h) * w, st));
+  const long long hw = static_cast<long long>(h) * w;
+  const long long nq = (w & 3) == 0 ? hw / 4 : hw;
+  const int planes = n * c;
+  const int gx = static_cast<int>(std::min<long long>((nq + 255) / 256, 4096));
+  int gy = std::min(planes, std::max(1, sm_count() * 8 / gx));
+  const int ppy = (planes + gy - 1) / gy;
+  gy = (planes + ppy - 1) / ppy;
+  k_mask_bits<<<dim3(gx, gy), 256, 0, st>>>(orig, edited, planes, ppy, h, w, thr, bits, mask_u8, any);
+  after_launch("k_mask_bits");
+}
+
+void launch_mask_u8_to_bits(const uint8_t* mask, int h, int w, uint32_t* bits, int32_t* any,
+                            cudaStream_t st) {
+  const int wpr = (w + 31) >> 5;
+  k_mask_u8_to_bits<<<grid_cap(static_cast<long long>(h) * wpr, 256), 256, 0, st>>>(mask, h, w, bits, any);
+  after_launch("k_mask_u8_to_bits");
+}
+
+void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate_scale, int batch,
+                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st) {
+  if (num_entries == 0) return;
+  const size_t smem = sizeof(uint32_t) * H * ((W + 31) >> 5);
+  const int use_smem = smem <= 96 * 1024 ? 1 : 0;
+  static bool attr_set = false;
+  if (use_smem && smem > 48 * 1024 && !attr_set) {
+    SIGE_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr_set = true;
+  }
+  k_plan<<<num_entries, 1024, use_smem ? smem : 0, st>>>(bits, H, W, dilate_full, dilate_scale,
+                                                         batch, entries_dev, use_smem);
+  after_launch("k_plan");
+}
+
+void launch_gn_fold(const Src& x, int groups, float eps, const float* gamma, const float* beta,
+                    float* scale, float* shift, double* /*scratch*/, int exact, cudaStream_t st) {
+  if (groups < 1 || x.c % groups != 0)
+    throw ConfigError("compute_norm_stats: groups " + std::to_string(groups) +
+                      " must divide channels " + std::to_string(x.c));
+  if (exact) {
+    const int items = x.n * groups;
+    k_gn_exact<<<(items + 31) / 32, 32, 0, st>>>(x, groups, eps, gamma, beta, scale, shift);
+    after_launch("k_gn_exact");
+  } else {
+    k_gn_fast<<<x.n * groups, 512, 0, st>>>(x, groups, eps, gamma, beta, scale, shift);
+    after_launch("k_gn_fast");
+  }
+}
+
+void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, const float* rmean,
+                    const float* rvar, float* scale, float* shift, cudaStream_t st) {
+  k_bn_fold<<<(c + 255) / 256, 256, 0, st>>>(c, eps, gamma, beta, rmean, rvar, scale, shift);
+  after_launch("k_bn_fold");
+}
+
+void launch_materialize(const Src& src, float* dst, int dst_layout, cudaStream_t st) {
+  const long long total = static_cast<long long>(src.n) * src.c * src.h * src.w;
+  k_materialize<<<grid_cap(total, 256), 256, 0, st>>>(src, dst, dst_layout);
+  after_launch("k_materialize");
+}
+
+void launch_tiles_apply(const Src& src, const Tiles& tiles, float* dst, int dst_layout,
+                        cudaStream_t st) {
+  const long long total = static_cast<long long>(tiles.capacity) * tiles.bh * tiles.bw * src.c;
+  if (total == 0) return;
+  k_tiles_apply<<<grid_cap(total, 256), 256, 0, st>>>(src, tiles, dst, dst_layout);
+  after_launch("k_tiles_apply");
+}
+
+void launch_identity_join(const Src& src, const Tiles& tiles, const Dst& dst, cudaStream_t st) {
+  const long long total = static_cast<long long>(tiles.capacity) * tiles.bh * tiles.bw * dst.c;
+  if (total == 0) return;
+  k_identity_join<<<grid_cap(total, 256), 256, 0, st>>>(src, tiles, dst);
+  after_launch("k_identity_join");
+}
+
+void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_elems_per_job,
+                    cudaStream_t st) {
+  if (num_jobs == 0) return;
+  const int gx = std::min(grid_cap(max_elems_per_job, 256), 64);
+  k_restore<<<dim3(gx, num_jobs), 256, 0, st>>>(jobs_dev, 1 << 30);
+  after_launch("k_restore");
+}
+
+void launch_finalize(const Src& result, const float* cached_final, const int32_t* any, float* out,
+                     cudaStream_t st) {
+  const long long total = static_cast<long long>(result.n) * result.c * result.h * result.w;
+  k_finalize<<<grid_cap(total, 256), 256, 0, st>>>(result, cached_final, any, out);
+  after_launch("k_finalize");
+}
+
+void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st) {
+  k_add<<<grid_cap(static_cast<long long>(n), 256), 256, 0, st>>>(a, b, out, static_cast<long long>(n));
+  after_launch("k_add");
+}
+
+void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st) {
+  k_nchw_to_nhwc<<<grid_cap(static_cast<long long>(n) * c * h * w, 256), 256, 0, st>>>(in, out, n, c, h, w);
+  after_launch("k_nchw_to_nhwc");
+}
+
+void launch_nhwc_to_nchw(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st) {
+  k_nhwc_to_nchw<<<grid_cap(static_cast<long long>(n) * c * h * w, 256), 256, 0, st>>>(in, out, n, c, h, w);
+  after_launch("k_nhwc_to_nchw");
+}
+
+}  // namespace sige_b200

@@ -1,0 +1,148 @@
+// engine_kernels.hpp — device-side descriptors and launchers of the engine
+// (the production sparse_forward path). Activations inside the engine are
+// NHWC fp32 ("channels-last"): a pixel's channels are one contiguous run, so
+// gathers move whole 16-byte vectors and the tensor-core operand rows come out
+// K-contiguous. External tensors (the edited input, the final output) are
+// NCHW, the reference layout (proj/include/sige/tensor.hpp:12-39).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.hpp"
+
+namespace sige_b200 {
+
+enum Layout : int { kNHWC = 0, kNCHW = 1 };
+
+// An activation as a consumer sees it: the stored tensor (physical
+// h >> up, w >> up), its layout, the pending element-wise chain (Flow::pending,
+// graph.cpp:545-553) and the nearest-upsample shift folded into the index
+// arithmetic instead of materialising upsample_nearest2x (tensor.cpp:69-83).
+struct Src {
+  const float* ptr = nullptr;
+  int layout = kNHWC;
+  int n = 1, c = 0, h = 0, w = 0;  // logical dims
+  int up = 0;                       // log2 upsample factor
+  DevEpilogue epi;
+};
+
+#ifdef __CUDACC__
+// Raw stored value of logical pixel (n, ch, y, x) (caller bounds-checks).
+__device__ __forceinline__ float src_raw(const Src& s, int n, int ch, int y, int x) {
+  int ph = s.h >> s.up, pw = s.w >> s.up;
+  int py = y >> s.up, px = x >> s.up;
+  size_t off = s.layout == kNHWC ? ((static_cast<size_t>(n) * ph + py) * pw + px) * s.c + ch
+                                 : ((static_cast<size_t>(n) * s.c + ch) * ph + py) * pw + px;
+  return __ldg(s.ptr + off);
+}
+__device__ __forceinline__ float src_val(const Src& s, int n, int ch, int y, int x) {
+  return dev_epi(s.epi, src_raw(s, n, ch, y, x), ch, s.c, n);
+}
+#endif
+
+// What a conv does with its (acc + bias) value at output pixel p.
+enum OutMode : int {
+  kStore = 0,        // dst[p] = v                      (scatter_inplace, kernels.cpp:88-106)
+  kResMain = 1,      // dst[p] = v + aux[p]             (main tiles, kernels.cpp:306-318)
+  kResShortcut = 2,  // dst[p] = dst[p] + (v - aux[p])  (shortcut tiles, kernels.cpp:320-334)
+  kAddSrc = 3,       // dst[p] = v + addend(p)          (dense ResBlock join add(m, sc), graph.cpp:812)
+};
+
+struct Dst {
+  float* ptr = nullptr;  // NHWC, (n, h, w, c)
+  int n = 1, c = 0, h = 0, w = 0;
+  int mode = kStore;
+  const float* aux = nullptr;  // NHWC, same shape (original shortcut)
+  Src addend;                  // kAddSrc
+};
+
+// The tile list a conv runs over: `count` triplets {n, r, c} (output-res
+// tile origins, BlockIndexSet order), count read from the device when
+// count_dev != nullptr (produced by the on-device IndexPlan).
+struct Tiles {
+  const int32_t* idx = nullptr;
+  const int32_t* count_dev = nullptr;
+  int count = 0;     // used when count_dev == nullptr
+  int capacity = 0;  // upper bound for grid sizing
+  int bh = 0, bw = 0;  // tile shape at output resolution (square for sparse)
+};
+
+struct ConvW {
+  int c_in = 0, c_out = 0, k = 1, stride = 1;
+  const float* w = nullptr;     // (c_out, c_in, k, k) reference layout
+  const float* bias = nullptr;  // c_out or nullptr
+  const float* w_tc = nullptr;  // tcgen05 K-major packing (conv_tc.cu), may be nullptr
+  int n_pad = 0;                // c_out rounded up for the tensor-core N dimension
+  int k_pad = 0;                // channels rounded up per tap for the K dimension
+};
+
+// Fused gather -> conv -> scatter over tiles (exact fp32 CUDA-core path:
+// reference order, no FMA; bit-exact). conv_exact.cu.
+void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst,
+                       int math, cudaStream_t st);
+// Same contract on tcgen05 tensor cores (kind::tf32, fp32 TMEM accumulators).
+// conv_tc.cu.
+void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst,
+                    cudaStream_t st);
+// Packs reference-layout weights for launch_conv_tc; returns device buffer.
+float* pack_weights_tc(const float* w_dev_ref, int c_out, int c_in, int k, int* n_pad, int* k_pad,
+                       cudaStream_t st);
+
+// On-device IndexPlan (graph.cpp:506-528): for every entry e, tile (r, c) of
+// an (h_e, w_e, b_e) grid is active iff the full-resolution difference mask
+// has a set pixel in the rectangle that dilate_full, resampling (max-pool
+// down / replicate up) and dilate_scale map onto that tile. One CTA per entry
+// writes the active tiles in row-major order, replicated n-major.
+struct PlanEntryDev {
+  int h, w, b;
+  int32_t* idx;    // capacity triplets
+  int32_t* count;  // device int
+  int capacity;
+};
+// Both set *any = 1 when at least one pixel is set (the caller zeroes it).
+void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
+                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st);
+void launch_mask_u8_to_bits(const uint8_t* mask, int h, int w, uint32_t* bits, int32_t* any,
+                            cudaStream_t st);
+void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate_scale, int batch,
+                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st);
+
+// GroupNorm statistics + fold (norm.cpp:25-90) over a full NHWC tensor,
+// writing scale/shift (n*C). exact=1 follows the reference's sequential
+// double accumulation order (bit-exact); 0 uses a parallel tree.
+void launch_gn_fold(const Src& x, int groups, float eps, const float* gamma, const float* beta,
+                    float* scale, float* shift, double* scratch, int exact, cudaStream_t st);
+// Batch-kind fold of running statistics (graph.cpp:313-320).
+void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, const float* rmean,
+                    const float* rvar, float* scale, float* shift, cudaStream_t st);
+
+// dst (NHWC or NCHW per dst_layout, full tensor) = value of `src` at every
+// pixel (pending chain + upsample applied): flush()/materialize().
+void launch_materialize(const Src& src, float* dst, int dst_layout, cudaStream_t st);
+// Final-tile copy: dst (NCHW) at tiles = epi(src) (apply_epilogue_on_blocks +
+// scatter into the cached final output, graph.cpp:891-898).
+void launch_tiles_apply(const Src& src, const Tiles& tiles, float* dst, int dst_layout,
+                        cudaStream_t st);
+// Identity-shortcut join at shortcut tiles: dst[p] = dst[p] + (src(p) - aux[p]).
+void launch_identity_join(const Src& src, const Tiles& tiles, const Dst& dst, cudaStream_t st);
+// Restore tiles of a working buffer from its cache entry (same layout).
+struct RestoreJob {
+  float* dst;
+  const float* src;
+  const int32_t* idx;
+  const int32_t* count;
+  int n, c, h, w, b, layout;
+};
+void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_tiles, cudaStream_t st);
+// out (NCHW, full) = *any ? value of `result` : cached_final — the empty-mask
+// short-circuit of sparse_forward (graph.cpp:665-668) folded into the final copy.
+void launch_finalize(const Src& result, const float* cached_final, const int32_t* any, float* out,
+                     cudaStream_t st);
+// Elementwise a + b over n values (dense ResBlock sum in precompute).
+void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st);
+// Layout conversions.
+void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);
+void launch_nhwc_to_nchw(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);
+
+}  // namespace sige_b200

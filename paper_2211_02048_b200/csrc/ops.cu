@@ -1,0 +1,518 @@
+// ops.cu — op-level sm_100a kernels: the per-function drop-ins for
+// proj/include/sige/{mask,kernels,conv}.hpp. Layouts are the reference's
+// (NCHW tensors, (G,C,bh,bw) block stacks, {n,r,c} index triplets). These are
+// HBM-bound copies / predicates; float arithmetic uses __f*_rn intrinsics so
+// no FMA contraction happens and results are bit-exact to the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "ops.hpp"
+
+namespace sige_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(long long n, int threads = kThreads) {
+  long long g = (n + threads - 1) / threads;
+  long long cap = static_cast<long long>(sm_count()) * 32;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+// ---------------------------------------------------------------- masks --
+
+// compute_difference_mask (mask.cpp:14-32): mask[p] |= |e - o| > t over all
+// (n, c) planes. Grid.y splits the planes; writers only ever store 1, so
+// concurrent stores to one byte are benign.
+__global__ void k_difference_mask(const float* __restrict__ o, const float* __restrict__ e,
+                                  int planes, int planes_per_y, long long hw, float thr,
+                                  uint8_t* __restrict__ mask) {
+  int p0 = blockIdx.y * planes_per_y;
+  int p1 = min(planes, p0 + planes_per_y);
+  bool vec = (hw & 3) == 0;
+  long long nq = vec ? hw / 4 : hw;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq;
+       q += (long long)gridDim.x * blockDim.x) {
+    if (vec) {
+      bool b0 = false, b1 = false, b2 = false, b3 = false;
+      for (int p = p0; p < p1; ++p) {
+        float4 a = __ldg(reinterpret_cast<const float4*>(o + p * hw) + q);
+        float4 b = __ldg(reinterpret_cast<const float4*>(e + p * hw) + q);
+        b0 |= fabsf(__fsub_rn(b.x, a.x)) > thr;
+        b1 |= fabsf(__fsub_rn(b.y, a.y)) > thr;
+        b2 |= fabsf(__fsub_rn(b.z, a.z)) > thr;
+        b3 |= fabsf(__fsub_rn(b.w, a.w)) > thr;
+      }
+      if (b0) mask[4 * q] = 1;
+      if (b1) mask[4 * q + 1] = 1;
+      if (b2) mask[4 * q + 2] = 1;
+      if (b3) mask[4 * q + 3] = 1;
+    } else {
+      bool any = false;
+      for (int p = p0; p < p1; ++p)
+        any |= fabsf(__fsub_rn(__ldg(e + p * hw + q), __ldg(o + p * hw + q))) > thr;
+      if (any) mask[q] = 1;
+    }
+  }
+}
+
+// downsample_mask (mask.cpp:34-53): max-pool by integer factors.
+__global__ void k_downsample_mask(const uint8_t* __restrict__ m, int h, int w, int oh, int ow,
+                                  uint8_t* __restrict__ out) {
+  int fy = h / oh, fx = w / ow;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < oh * ow; p += gridDim.x * blockDim.x) {
+    int y = p / ow, x = p % ow;
+    uint8_t v = 0;
+    for (int dy = 0; dy < fy && !v; ++dy)
+      for (int dx = 0; dx < fx && !v; ++dx) v = m[(size_t)(y * fy + dy) * w + x * fx + dx];
+    out[p] = v ? 1 : 0;
+  }
+}
+
+// dilate_mask (mask.cpp:55-80): separable Chebyshev dilation, clipped.
+__global__ void k_dilate_rows(const uint8_t* __restrict__ m, int h, int w, int r,
+                              uint8_t* __restrict__ out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < h * w; p += gridDim.x * blockDim.x) {
+    int y = p / w, x = p % w;
+    uint8_t v = 0;
+    for (int t = max(0, x - r); t <= min(w - 1, x + r) && !v; ++t) v = m[(size_t)y * w + t];
+    out[p] = v ? 1 : 0;
+  }
+}
+__global__ void k_dilate_cols(const uint8_t* __restrict__ m, int h, int w, int r,
+                              uint8_t* __restrict__ out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < h * w; p += gridDim.x * blockDim.x) {
+    int y = p / w, x = p % w;
+    uint8_t v = 0;
+    for (int t = max(0, y - r); t <= min(h - 1, y + r) && !v; ++t) v = m[(size_t)t * w + x];
+    out[p] = v ? 1 : 0;
+  }
+}
+
+// mask_to_block_indices (mask.cpp:103-136). One CTA walks the tile grid in
+// row-major chunks of blockDim tiles; each thread tests one tile, a block
+// scan assigns output slots, so the emitted order is exactly the reference's
+// (r outer, c inner), then replicated n-major.
+__global__ void k_blockify(const uint8_t* __restrict__ m, int h, int w, int b, int batch,
+                           int32_t* __restrict__ idx, int capacity, int32_t* __restrict__ count) {
+  __shared__ int warp_sums[32];
+  __shared__ int base;
+  int ty = (h + b - 1) / b, tx = (w + b - 1) / b, tiles = ty * tx;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
+    int t = t0 + threadIdx.x;
+    bool on = false;
+    int R = 0, Cc = 0;
+    if (t < tiles) {
+      R = (t / tx) * b;
+      Cc = (t % tx) * b;
+      for (int y = R; y < min(h, R + b) && !on; ++y)
+        for (int x = Cc; x < min(w, Cc + b) && !on; ++x) on = m[(size_t)y * w + x] != 0;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) warp_sums[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+      for (int d = 1; d < 32; d <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
+      }
+      if (lane < nw) warp_sums[lane] = v;  // inclusive
+    }
+    __syncthreads();
+    int before = (wid ? warp_sums[wid - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+    int slot = base + before;
+    int total_chunk = warp_sums[nw - 1];
+    // Sample 0 first (the tile total is unknown until the walk ends); the
+    // other samples are replicated from it below.
+    if (on && slot < capacity) {
+      idx[3 * slot] = 0;
+      idx[3 * slot + 1] = R;
+      idx[3 * slot + 2] = Cc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += total_chunk;
+    __syncthreads();
+  }
+  int per = base;
+  // replicate n-major: entries [per * n, per * (n + 1)) copy sample 0 with n.
+  for (int n = 1; n < batch; ++n)
+    for (int i = threadIdx.x; i < per; i += blockDim.x) {
+      int d = n * per + i;
+      if (d < capacity && i < capacity) {
+        idx[3 * d] = n;
+        idx[3 * d + 1] = idx[3 * i + 1];
+        idx[3 * d + 2] = idx[3 * i + 2];
+      }
+    }
+  if (threadIdx.x == 0) *count = per * batch;
+}
+
+// ---------------------------------------------------------------- blocks --
+
+// gather (kernels.cpp:39-86): one thread per output value; out-of-canvas
+// cells are +0 and skip the epilogue.
+__global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
+                         const int32_t* __restrict__ idx, int count, int win, int stride, int pad,
+                         DevEpilogue epi, float* __restrict__ out) {
+  long long wsz = (long long)win * win;
+  long long total = (long long)count * c * wsz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long i = q / (c * wsz);
+    int rem = static_cast<int>(q - i * c * wsz);
+    int ch = rem / static_cast<int>(wsz);
+    int cell = rem - ch * static_cast<int>(wsz);
+    int wy = cell / win, wx = cell - wy * win;
+    int n = idx[3 * i], sy = idx[3 * i + 1] * stride - pad + wy, sx = idx[3 * i + 2] * stride - pad + wx;
+    float v = 0.0f;
+    if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
+      v = __ldg(x + (((size_t)n * c + ch) * h + sy) * w + sx);
+      v = dev_epi(epi, v, ch, c, n);
+    }
+    out[q] = v;
+  }
+}
+
+// scatter_inplace / scatter_add_inplace (kernels.cpp:88-132): tile values
+// clipped at the fringe; mode 0 writes, mode 1 adds.
+__global__ void k_scatter(const float* __restrict__ blocks, int count, int c, int b,
+                          const int32_t* __restrict__ idx, float* __restrict__ base, int h, int w,
+                          int mode) {
+  long long bsz = (long long)b * b;
+  long long total = (long long)count * c * bsz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long i = q / (c * bsz);
+    int rem = static_cast<int>(q - i * c * bsz);
+    int ch = rem / static_cast<int>(bsz);
+    int cell = rem - ch * static_cast<int>(bsz);
+    int y = idx[3 * i + 1] + cell / b, xx = idx[3 * i + 2] + cell % b;
+    if (y >= h || xx >= w) continue;
+    float* d = base + (((size_t)idx[3 * i] * c + ch) * h + y) * w + xx;
+    float v = blocks[q];
+    *d = mode ? __fadd_rn(*d, v) : v;
+  }
+}
+
+// build_scatter_map (kernels.cpp:134-169), fill then per-tile writes.
+__global__ void k_map_fill(sige_scatter_entry* map, long long hw) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < hw;
+       p += (long long)gridDim.x * blockDim.x) {
+    sige_scatter_entry e;
+    e.block = -1;
+    e.dy = 0;
+    e.dx = 0;
+    map[p] = e;
+  }
+}
+__global__ void k_map_tiles(const int32_t* __restrict__ idx, int per, int b, int h, int w,
+                            sige_scatter_entry* map) {
+  long long total = (long long)per * b * b;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int o = static_cast<int>(q / (b * b));
+    int cell = static_cast<int>(q % (b * b));
+    int dy = cell / b, dx = cell % b;
+    int y = idx[3 * o + 1] + dy, x = idx[3 * o + 2] + dx;
+    if (y >= h || x >= w) continue;
+    sige_scatter_entry e;
+    e.block = o;
+    e.dy = static_cast<int16_t>(dy);
+    e.dx = static_cast<int16_t>(dx);
+    map[(size_t)y * w + x] = e;
+  }
+}
+// per-sample count and batch-pattern check (kernels.cpp:142-152).
+__global__ void k_map_check(const int32_t* __restrict__ idx, int count, int* out) {
+  // out[0] = per-sample count, out[1] = 1 if the pattern differs.
+  __shared__ int per_s;
+  if (threadIdx.x == 0) per_s = 0;
+  __syncthreads();
+  int local = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) local += idx[3 * i] == idx[0];
+  atomicAdd(&per_s, local);
+  __syncthreads();
+  int per = per_s;
+  int bad = 0;
+  if (per > 0)
+    for (int i = per + threadIdx.x; i < count; i += blockDim.x) {
+      int r = i % per;
+      bad |= idx[3 * i + 1] != idx[3 * r + 1] || idx[3 * i + 2] != idx[3 * r + 2];
+    }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    out[0] = per;
+    out[1] = bad;
+  }
+}
+
+// scatter_gather (kernels.cpp:204-275).
+__global__ void k_scatter_gather(const float* __restrict__ blocks, int pb, const float* __restrict__ orig,
+                                 int c, int h, int w, const sige_scatter_entry* __restrict__ map,
+                                 int bps, const int32_t* __restrict__ cidx, int ccount, int win,
+                                 int stride, int pad, DevEpilogue epi, float* __restrict__ out) {
+  long long wsz = (long long)win * win;
+  long long total = (long long)ccount * c * wsz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long i = q / (c * wsz);
+    int rem = static_cast<int>(q - i * c * wsz);
+    int ch = rem / static_cast<int>(wsz);
+    int cell = rem - ch * static_cast<int>(wsz);
+    int wy = cell / win, wx = cell - wy * win;
+    int n = cidx[3 * i], sy = cidx[3 * i + 1] * stride - pad + wy, sx = cidx[3 * i + 2] * stride - pad + wx;
+    float v = 0.0f;
+    if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
+      sige_scatter_entry e = map[(size_t)sy * w + sx];
+      v = e.block < 0 ? __ldg(orig + (((size_t)n * c + ch) * h + sy) * w + sx)
+                      : __ldg(blocks + (((size_t)(n * bps + e.block) * c + ch) * pb + e.dy) * pb + e.dx);
+      v = dev_epi(epi, v, ch, c, n);
+    }
+    out[q] = v;
+  }
+}
+
+// Residual join passes (kernels.cpp:306-334): main tiles out = m + sc_orig;
+// shortcut tiles out = out + (s - sc_orig).
+__global__ void k_residual(const float* __restrict__ blocks, int count, int c, int b,
+                           const int32_t* __restrict__ idx, const float* __restrict__ orig_sc,
+                           float* __restrict__ out, int h, int w, int shortcut_pass) {
+  long long bsz = (long long)b * b;
+  long long total = (long long)count * c * bsz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long i = q / (c * bsz);
+    int rem = static_cast<int>(q - i * c * bsz);
+    int ch = rem / static_cast<int>(bsz);
+    int cell = rem - ch * static_cast<int>(bsz);
+    int y = idx[3 * i + 1] + cell / b, xx = idx[3 * i + 2] + cell % b;
+    if (y >= h || xx >= w) continue;
+    size_t p = (((size_t)idx[3 * i] * c + ch) * h + y) * w + xx;
+    float v = blocks[q];
+    out[p] = shortcut_pass ? __fadd_rn(out[p], __fsub_rn(v, orig_sc[p])) : __fadd_rn(v, orig_sc[p]);
+  }
+}
+
+// add_blocks / subtract_blocks (kernels.cpp:359-380): a + sign*b.
+__global__ void k_combine(const float* __restrict__ a, const float* __restrict__ b, float sign,
+                          long long n, float* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = __fadd_rn(a[q], __fmul_rn(sign, b[q]));
+}
+
+// apply_epilogue_on_blocks (kernels.cpp:382-389).
+__global__ void k_epilogue_blocks(float* blocks, int count, int c, int bh,
+                                  const int32_t* __restrict__ idx, DevEpilogue epi) {
+  long long bsz = (long long)bh * bh;
+  long long total = (long long)count * c * bsz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long i = q / (c * bsz);
+    int ch = static_cast<int>((q / bsz) % c);
+    blocks[q] = dev_epi(epi, blocks[q], ch, c, idx[3 * i]);
+  }
+}
+
+// conv core on CUDA cores (conv.cpp:33-79): per output acc = +0; for ic,
+// ky, kx (in-bounds taps): acc = acc + w*x (separate roundings unless
+// math == SIGE_MATH_FP32_FMA); then + bias. `in` is (planes, ih, iw) per
+// sample/block with `in_stride` floats between consecutive samples/blocks.
+template <int MATH>
+__global__ void k_conv_cc(const float* __restrict__ in, long long in_stride, int ci, int ih, int iw,
+                          const float* __restrict__ wt, const float* __restrict__ bias, int co,
+                          int k, int s, int pad, float* __restrict__ out, long long out_stride,
+                          int oh, int ow, int items) {
+  long long per = (long long)co * oh * ow;
+  long long total = per * items;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long it = q / per;
+    int rem = static_cast<int>(q - it * per);
+    int oc = rem / (oh * ow);
+    int cell = rem - oc * oh * ow;
+    int oy = cell / ow, ox = cell - oy * ow;
+    const float* src = in + it * in_stride;
+    const float* wk = wt + (size_t)oc * ci * k * k;
+    float acc = 0.0f;
+    for (int ic = 0; ic < ci; ++ic) {
+      const float* plane = src + (size_t)ic * ih * iw;
+      for (int ky = 0; ky < k; ++ky) {
+        int iy = oy * s + ky - pad;
+        if (iy < 0 || iy >= ih) continue;
+        for (int kx = 0; kx < k; ++kx) {
+          int ix = ox * s + kx - pad;
+          if (ix < 0 || ix >= iw) continue;
+          float wv = __ldg(wk + (ic * k + ky) * k + kx), xv = __ldg(plane + (size_t)iy * iw + ix);
+          if (MATH == SIGE_MATH_FP32_FMA)
+            acc = __fmaf_rn(wv, xv, acc);
+          else
+            acc = __fadd_rn(acc, __fmul_rn(wv, xv));
+        }
+      }
+    }
+    if (bias) acc = __fadd_rn(acc, __ldg(bias + oc));
+    out[it * out_stride + rem] = acc;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host side --
+
+void op_difference_mask(const float* o, const float* e, int n, int c, int h, int w, float thr,
+                        uint8_t* mask, cudaStream_t st) {
+  if (thr < 0.0f) throw ConfigError("compute_difference_mask: threshold must be >= 0");
+  if (n < 1 || c < 1 || h < 1 || w < 1)
+    throw ConfigError("compute_difference_mask: all dims must be >= 1");
+  long long hw = (long long)h * w;
+  SIGE_CUDA(cudaMemsetAsync(mask, 0, hw, st));
+  int planes = n * c;
+  long long nq = (hw & 3) == 0 ? hw / 4 : hw;
+  int gx = static_cast<int>(std::min<long long>((nq + 255) / 256, 1 << 16));
+  // enough CTAs for ~4 waves: split the planes across grid.y
+  int want_y = std::max(1, (sm_count() * 8) / std::max(1, gx));
+  int gy = std::min(planes, want_y);
+  int ppy = (planes + gy - 1) / gy;
+  gy = (planes + ppy - 1) / ppy;
+  k_difference_mask<<<dim3(gx, gy), 256, 0, st>>>(o, e, planes, ppy, hw, thr, mask);
+  after_launch("k_difference_mask");
+}
+
+void op_downsample_mask(const uint8_t* m, int h, int w, int oh, int ow, uint8_t* out,
+                        cudaStream_t st) {
+  if (oh < 1 || ow < 1 || oh > h || ow > w)
+    throw ConfigError("downsample_mask: target must be >= 1 and <= source");
+  if (h % oh != 0 || w % ow != 0)
+    throw ConfigError("downsample_mask: non-integer scale factor (" + std::to_string(h) + "x" +
+                      std::to_string(w) + " -> " + std::to_string(oh) + "x" +
+                      std::to_string(ow) + ")");
+  k_downsample_mask<<<grid_for((long long)oh * ow), kThreads, 0, st>>>(m, h, w, oh, ow, out);
+  after_launch("k_downsample_mask");
+}
+
+void op_dilate_mask(const uint8_t* m, int h, int w, int r, uint8_t* out, uint8_t* tmp,
+                    cudaStream_t st) {
+  if (r < 0) throw ConfigError("dilate_mask: radius must be >= 0");
+  if (r == 0) {
+    SIGE_CUDA(cudaMemcpyAsync(out, m, (size_t)h * w, cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  k_dilate_rows<<<grid_for((long long)h * w), kThreads, 0, st>>>(m, h, w, r, tmp);
+  after_launch("k_dilate_rows");
+  k_dilate_cols<<<grid_for((long long)h * w), kThreads, 0, st>>>(tmp, h, w, r, out);
+  after_launch("k_dilate_cols");
+}
+
+void op_mask_to_block_indices(const uint8_t* m, int h, int w, int b, int batch, int32_t* idx,
+                              int capacity, int32_t* count, cudaStream_t st) {
+  if (b < 1) throw ConfigError("mask_to_block_indices: block size must be >= 1");
+  if (batch < 1) throw ConfigError("mask_to_block_indices: batch must be >= 1");
+  k_blockify<<<1, 1024, 0, st>>>(m, h, w, b, batch, idx, capacity, count);
+  after_launch("k_blockify");
+}
+
+void op_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, int count, int b,
+               int ih, int iw, int k, int s, const DevEpilogue& epi, float* out, cudaStream_t st) {
+  if (k != 1 && k != 3) throw ConfigError("gather: kernel size must be 1 or 3");
+  if (s != 1 && s != 2) throw ConfigError("gather: stride must be 1 or 2");
+  int oh = conv_out_dim(h, k, s), ow = conv_out_dim(w, k, s);
+  if (ih != oh || iw != ow)
+    throw ConfigError("gather: index set lives at " + std::to_string(ih) + "x" + std::to_string(iw) +
+                      " but conv output of (" + std::to_string(n) + ", " + std::to_string(c) + ", " +
+                      std::to_string(h) + ", " + std::to_string(w) + ") is " + std::to_string(oh) +
+                      "x" + std::to_string(ow));
+  if (count == 0) return;
+  int win = s * b + k - s;
+  k_gather<<<grid_for((long long)count * c * win * win), kThreads, 0, st>>>(
+      x, c, h, w, idx, count, win, s, (k - 1) / 2, epi, out);
+  after_launch("k_gather");
+}
+
+void op_scatter(const float* blocks, int count, int channels, int b, const int32_t* idx, float* base,
+                int n, int c, int h, int w, bool add, cudaStream_t st) {
+  if (channels != c) throw ConfigError(std::string(add ? "scatter_add" : "scatter") + ": channel mismatch");
+  if (count == 0) return;
+  k_scatter<<<grid_for((long long)count * c * b * b), kThreads, 0, st>>>(blocks, count, c, b, idx,
+                                                                         base, h, w, add ? 1 : 0);
+  after_launch("k_scatter");
+}
+
+int op_build_scatter_map(const int32_t* idx, int count, int b, int h, int w,
+                         sige_scatter_entry* map, int* scratch2, cudaStream_t st) {
+  k_map_fill<<<grid_for((long long)h * w), kThreads, 0, st>>>(map, (long long)h * w);
+  after_launch("k_map_fill");
+  if (count == 0) return 0;
+  k_map_check<<<1, 256, 0, st>>>(idx, count, scratch2);
+  after_launch("k_map_check");
+  int host[2];
+  SIGE_CUDA(cudaMemcpyAsync(host, scratch2, sizeof host, cudaMemcpyDeviceToHost, st));
+  SIGE_CUDA(cudaStreamSynchronize(st));
+  if (host[1]) throw ConfigError("build_scatter_map: tile pattern differs across batch");
+  int per = host[0];
+  k_map_tiles<<<grid_for((long long)per * b * b), kThreads, 0, st>>>(idx, per, b, h, w, map);
+  after_launch("k_map_tiles");
+  return per;
+}
+
+void op_scatter_gather(const float* blocks, int count, int pb, const float* orig, int n, int c,
+                       int h, int w, const sige_scatter_entry* map, int bps, const int32_t* cidx,
+                       int ccount, int cb, int ch, int cw, int k, int s, const DevEpilogue& epi,
+                       float* out, cudaStream_t st) {
+  if (bps * n != count) throw ConfigError("scatter_gather: map does not describe this block stack");
+  if (ch != conv_out_dim(h, k, s) || cw != conv_out_dim(w, k, s))
+    throw ConfigError("scatter_gather: consumer index resolution mismatch");
+  if (ccount == 0) return;
+  int win = s * cb + k - s;
+  k_scatter_gather<<<grid_for((long long)ccount * c * win * win), kThreads, 0, st>>>(
+      blocks, pb, orig, c, h, w, map, bps, cidx, ccount, win, s, (k - 1) / 2, epi, out);
+  after_launch("k_scatter_gather");
+}
+
+void op_residual_pass(const float* blocks, int count, int c, int b, const int32_t* idx,
+                      const float* orig_sc, float* out, int h, int w, bool shortcut_pass,
+                      cudaStream_t st) {
+  if (count == 0) return;
+  k_residual<<<grid_for((long long)count * c * b * b), kThreads, 0, st>>>(
+      blocks, count, c, b, idx, orig_sc, out, h, w, shortcut_pass ? 1 : 0);
+  after_launch("k_residual");
+}
+
+void op_combine(const float* a, const float* b, float sign, size_t n, float* out, cudaStream_t st) {
+  if (n == 0) return;
+  k_combine<<<grid_for((long long)n), kThreads, 0, st>>>(a, b, sign, (long long)n, out);
+  after_launch("k_combine");
+}
+
+void op_epilogue_blocks(float* blocks, int count, int c, int bh, const int32_t* idx,
+                        const DevEpilogue& epi, cudaStream_t st) {
+  if (count == 0 || epi.num_steps == 0) return;
+  k_epilogue_blocks<<<grid_for((long long)count * c * bh * bh), kThreads, 0, st>>>(blocks, count, c,
+                                                                                  bh, idx, epi);
+  after_launch("k_epilogue_blocks");
+}
+
+void op_conv_cc(const float* in, long long in_stride, int ci, int ih, int iw, const float* wt,
+                const float* bias, int co, int k, int s, int pad, float* out, long long out_stride,
+                int oh, int ow, int items, int math, cudaStream_t st) {
+  if (items == 0) return;
+  long long total = (long long)co * oh * ow * items;
+  if (math == SIGE_MATH_FP32_FMA)
+    k_conv_cc<SIGE_MATH_FP32_FMA><<<grid_for(total, 128), 128, 0, st>>>(
+        in, in_stride, ci, ih, iw, wt, bias, co, k, s, pad, out, out_stride, oh, ow, items);
+  else
+    k_conv_cc<SIGE_MATH_EXACT><<<grid_for(total, 128), 128, 0, st>>>(
+        in, in_stride, ci, ih, iw, wt, bias, co, k, s, pad, out, out_stride, oh, ow, items);
+  after_launch("k_conv_cc");
+}
+
+}  // namespace sige_b200

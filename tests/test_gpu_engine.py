@@ -1,0 +1,126 @@
+"""GPU parity of the engine (device ActivationCache + sparse executor).
+
+SIGE_MATH_EXACT must reproduce the oracle's sparse_forward bit for bit (the
+oracle is itself bit-identical to the reference, tests/test_oracle_vs_ref.py),
+both with the cache uploaded from the CPU precompute and with the device
+precompute. SIGE_MATH_TF32 is held to the north-star tolerance (normalised
+max error <= 1e-2) with uncovered pixels bit-identical to the cache."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2211_02048_b200 as sb
+
+pytestmark = pytest.mark.gpu
+
+
+def upload_cache(eng, ocache, entries):
+    for kind, key, numel in entries:
+        if kind == 0:
+            eng.put_tensor(key, ocache.tensor(key))
+        else:
+            sc, sh = ocache.norm(key)
+            eng.put_norm(key, sc, sh)
+
+
+CASES = [
+    # model, fixture, batch, seed, config overrides (dilate_full None = required)
+    ("mini_unet_gn", "rect5", 1, 17, {}),
+    ("mini_unet_gn", "blob5", 2, 5, {"norm_precompute": 0}),
+    ("mini_unet_bn", "rect15", 1, 11, {"dilate_full": 3}),
+    ("gaugan_stack_in", "multi15", 1, 3, {}),
+    ("ddim_stack_64x32", "rect5", 1, 7, {"dilate_full": 5, "min_sparse_res": 16}),
+    ("ddim_stack_64x32", "rect1", 2, 8, {"dilate_full": 2, "min_sparse_res": 8, "block3": 4, "block1": 2}),
+    ("ddim_stack_64x32", "rect1", 1, 9, {"dilate_full": 2, "min_sparse_res": 8, "dilate_scale": 0}),
+]
+
+
+def run_case(orc, name, fx, n, seed, over, math, device_precompute):
+    om = orc.model(name)
+    c, h, w = sb.Model(name).in_shape
+    orig, edited = orc.make_edit_fixture(fx, n, c, h, w, seed)
+    mask = orc.difference_mask(orig, edited)
+    over = dict(over)
+    df = over.pop("dilate_full", None)
+    cfg = sb.default_config(dilate_full=om.required_dilation() if df is None else df, **over)
+    ocache = om.precompute(orig)
+    want, wtrace = om.sparse_forward(ocache, edited, mask, cfg)
+    eng = sb.Engine(sb.Model(name), batch=n, math=math)
+    if device_precompute:
+        eng.precompute(torch.from_numpy(orig).cuda())
+    else:
+        upload_cache(eng, ocache, ocache.entries())
+        eng.put_tensor("input", orig)
+    got = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg)
+    torch.cuda.synchronize()
+    return want, got.cpu().numpy(), wtrace, eng.trace().numpy().astype(np.uint64), ocache
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-n{c[2]}" for c in CASES])
+@pytest.mark.parametrize("device_precompute", [False, True])
+def test_exact_engine_bit_exact(orc, case, device_precompute):
+    want, got, wtr, gtr, _ = run_case(orc, *case, sb.MATH_EXACT, device_precompute)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"max diff {np.abs(got - want).max()}"
+    assert np.array_equal(gtr, wtr)
+
+
+def test_exact_engine_config1_full_size(orc):
+    """BASELINE config 1: 1x64x256x256, 3x3 conv, rect1, b=6 — bit-exact."""
+    want, got, wtr, gtr, _ = run_case(orc, "single_conv64", "rect1", 1, 7, {"dilate_full": 1}, sb.MATH_EXACT, True)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert gtr[0][0] == 36  # 36 active tiles
+
+
+def test_user_mask_and_empty_mask(orc):
+    om = orc.model("mini_unet_gn")
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 3)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    cfg = sb.default_config(dilate_full=25)
+    mask = orc.difference_mask(orig, edited)
+    a = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
+    b = eng.sparse_forward(torch.from_numpy(edited).cuda(), torch.from_numpy(mask).cuda(), config=cfg).cpu().numpy()
+    assert np.array_equal(a, b)
+    # all-false mask short-circuits to the cached final output (graph.cpp:665-668)
+    empty = torch.zeros((64, 64), dtype=torch.uint8, device="cuda")
+    c = eng.sparse_forward(torch.from_numpy(edited).cuda(), empty, config=cfg).cpu().numpy()
+    ocache = om.precompute(orig)
+    assert np.array_equal(c, ocache.tensor("final"))
+    # repeated calls (lazy tile restore) stay identical
+    d = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
+    assert np.array_equal(a, d)
+
+
+def test_precompute_matches_oracle_cache_exact(orc):
+    om = orc.model("mini_unet_gn")
+    orig, _ = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 2)
+    ocache = om.precompute(orig)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    torch.cuda.synchronize()
+    for kind, key, numel in ocache.entries():
+        if kind == 0:
+            want = ocache.tensor(key)
+            got = eng.get_tensor(key, want.shape).numpy()
+            assert np.array_equal(got, want), key
+
+
+def test_dense_forward_matches_oracle(orc):
+    om = orc.model("mini_unet_gn")
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 21)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    got = eng.dense_forward(torch.from_numpy(edited).cuda()).cpu().numpy()
+    assert np.array_equal(got, om.dense_forward(edited))
+    ocache = om.precompute(orig)
+    got = eng.dense_forward(torch.from_numpy(edited).cuda(), reused_stats=True).cpu().numpy()
+    assert np.array_equal(got, om.dense_forward(edited, ocache))
+
+
+def test_errors_like_reference(orc):
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+    x = torch.zeros((1, 3, 64, 64), device="cuda")
+    with pytest.raises(sb.ConfigError, match="precompute required"):
+        eng.sparse_forward(x)
+    with pytest.raises(sb.ConfigError, match="config: block sizes must be >= 1"):
+        eng.sparse_forward(x, config=sb.default_config(block3=0))

@@ -1,0 +1,296 @@
+"""GPU parity of the op-level C-ABI kernels against the oracle (bit-exact).
+
+Cases follow the reference's own unit tests (proj/tests/test_kernels.cpp,
+test_mask.cpp) and acceptance criterion 3 (acceptance.cpp:182-253): frozen
+windows, fringe clipping, batch OR, epilogue-on-copied-pixels-only, fused ==
+unfused, plus seeded random sweeps. Every comparison is np.array_equal on the
+raw float32 bits (NaN-free inputs), i.e. bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2211_02048_b200 as sb
+
+pytestmark = pytest.mark.gpu
+
+
+def cu(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def rand_epi_np(rng, c, n=1, silu=True, per_sample=False):
+    k = n * c if per_sample else c
+    sc = rng.uniform(0.5, 1.5, k).astype(np.float32)
+    sh = rng.uniform(-0.4, 0.4, k).astype(np.float32)
+    steps = [("ss", sc, sh)]
+    if silu:
+        steps.append(("act", sb.ACT_SILU))
+    return steps
+
+
+def to_dev_epi(steps):
+    e = sb.Epilogue()
+    for st in steps:
+        if st[0] == "ss":
+            e.add_scale_shift(torch.from_numpy(st[1]), torch.from_numpy(st[2]))
+        else:
+            e.add_activation(st[1])
+    return e
+
+
+# ----------------------------------------------------------- masks -------
+
+def test_difference_mask_threshold_strict_and_batch_or(orc):
+    # test_mask.cpp:33-51
+    o = np.zeros((1, 2, 3, 3), np.float32)
+    e = o.copy()
+    e[0, 1, 2, 2] = 0.5
+    e[0, 0, 0, 0] = 1e-3
+    m = host(sb.compute_difference_mask(cu(o), cu(e), 1e-3))
+    assert m.sum() == 1 and m[2, 2] == 1 and m[0, 0] == 0
+    o = np.zeros((2, 1, 2, 2), np.float32)
+    e = o.copy()
+    e[0, 0, 0, 0] = 1
+    e[1, 0, 1, 1] = 1
+    m = host(sb.compute_difference_mask(cu(o), cu(e), 0.1))
+    assert m[0, 0] == 1 and m[1, 1] == 1 and m.sum() == 2
+
+
+@pytest.mark.parametrize("kind,n,c,h,w,seed", [("rect1", 1, 64, 256, 256, 7), ("blob5", 2, 3, 64, 48, 3),
+                                                ("multi15", 1, 5, 37, 53, 9), ("rect35", 3, 2, 31, 17, 4)])
+def test_difference_mask_matches_oracle(orc, kind, n, c, h, w, seed):
+    o, e = orc.make_edit_fixture(kind, n, c, h, w, seed)
+    want = orc.difference_mask(o, e, 1e-3)
+    got = host(sb.compute_difference_mask(cu(o), cu(e), 1e-3))
+    assert np.array_equal(got, want)
+
+
+def test_difference_mask_golden_hash(orc):
+    o, e = orc.make_edit_fixture("rect1", 1, 64, 256, 256, 7)
+    m = host(sb.compute_difference_mask(cu(o), cu(e), 1e-3))
+    assert orc.fnv1a64(m) == 0x938A3A322907C793
+    assert int(m.sum()) == 784
+
+
+def test_dilate_and_downsample_match_oracle(orc):
+    rng = np.random.default_rng(11)
+    for rep in range(30):
+        h, w = rng.integers(4, 40, 2)
+        m = (rng.random((h, w)) < 0.1).astype(np.uint8)
+        r = int(rng.integers(0, 4))
+        assert np.array_equal(host(sb.dilate_mask(cu(m), r)), orc.dilate_mask(m, r))
+    m = (rng.random((48, 64)) < 0.05).astype(np.uint8)
+    for oh, ow in [(24, 32), (12, 16), (48, 8), (1, 1)]:
+        assert np.array_equal(host(sb.downsample_mask(cu(m), oh, ow)), orc.downsample_mask(m, oh, ow))
+    with pytest.raises(sb.ConfigError, match="non-integer scale factor"):
+        sb.downsample_mask(cu(m), 7, 7)
+
+
+def test_block_indices_match_oracle_and_golden(orc):
+    rng = np.random.default_rng(41)
+    for rep in range(40):
+        h, w = rng.integers(5, 70, 2)
+        b = int(rng.integers(1, 9))
+        batch = int(rng.integers(1, 4))
+        m = (rng.random((h, w)) < rng.uniform(0.0, 0.2)).astype(np.uint8)
+        want, _ = orc.mask_to_block_indices(m, b, batch)
+        got = host(sb.mask_to_block_indices(cu(m), b, batch))
+        assert np.array_equal(got, want), (h, w, b, batch)
+    # golden: 36 tiles at b=6 after two radius-1 dilations
+    o, e = orc.make_edit_fixture("rect1", 1, 64, 256, 256, 7)
+    m = sb.compute_difference_mask(cu(o), cu(e), 1e-3)
+    d = sb.dilate_mask(sb.dilate_mask(m, 1), 1)
+    idx = host(sb.mask_to_block_indices(d, 6, 1))
+    assert len(idx) == 36
+    assert orc.lib.orc_index_set_hash(idx.ctypes.data, 36, 6, 256, 256) == 0xCCBB614A2A613105
+
+
+# ---------------------------------------------------------- blocks -------
+
+def test_gather_frozen_windows():
+    # test_kernels.cpp:61-92
+    x = np.arange(16, dtype=np.float32).reshape(1, 1, 4, 4)
+    g = host(sb.gather(cu(x), cu(np.array([[0, 0, 0]], np.int32)), 2, 3, 1))
+    assert g.ravel().tolist() == [0, 0, 0, 0, 0, 0, 1, 2, 0, 4, 5, 6, 0, 8, 9, 10]
+    g = host(sb.gather(cu(x), cu(np.array([[0, 2, 2]], np.int32)), 2, 3, 1))
+    assert g.ravel().tolist() == [5, 6, 7, 0, 9, 10, 11, 0, 13, 14, 15, 0, 0, 0, 0, 0]
+    g = host(sb.gather(cu(x), cu(np.array([[0, 2, 2]], np.int32)), 2, 1, 1))
+    assert g.ravel().tolist() == [10, 11, 14, 15]
+    x8 = np.arange(64, dtype=np.float32).reshape(1, 1, 8, 8)
+    g = host(sb.gather(cu(x8), cu(np.array([[0, 2, 2]], np.int32)), 2, 3, 2))
+    assert g.shape[-1] == 5 and g[0, 0, 0, 0] == x8[0, 0, 3, 3] and g[0, 0, 4, 4] == x8[0, 0, 7, 7]
+
+
+def test_gather_errors_like_reference():
+    x = cu(np.zeros((1, 1, 8, 8), np.float32))
+    i = cu(np.zeros((1, 3), np.int32))
+    with pytest.raises(sb.ConfigError, match="gather: kernel size must be 1 or 3"):
+        sb.gather(x, i, 2, 5, 1)
+    with pytest.raises(sb.ConfigError, match="gather: stride must be 1 or 2"):
+        sb.gather(x, i, 2, 3, 3)
+    with pytest.raises(sb.ConfigError, match="gather: index set lives at"):
+        sb.gather(x, i, 2, 3, 1, idx_hw=(4, 4))
+
+
+@pytest.mark.parametrize("k,s", [(3, 1), (1, 1), (3, 2)])
+def test_gather_with_epilogue_matches_oracle(orc, k, s):
+    rng = np.random.default_rng(71 + k + s)
+    for rep in range(6):
+        n, c = int(rng.integers(1, 3)), int(rng.integers(1, 9))
+        h, w = int(rng.integers(6, 40)), int(rng.integers(6, 40))
+        x = rng.uniform(-3, 3, (n, c, h, w)).astype(np.float32)
+        oh, ow = (h + 2 * ((k - 1) // 2) - k) // s + 1, (w + 2 * ((k - 1) // 2) - k) // s + 1
+        b = int(rng.integers(2, 8))
+        m = (rng.random((oh, ow)) < 0.15).astype(np.uint8)
+        idx, _ = orc.mask_to_block_indices(m, b, n)
+        epi = rand_epi_np(rng, c, n, silu=rep % 2 == 0, per_sample=rep % 3 == 0)
+        want = orc.gather(x, idx, b, oh, ow, k, s, epi)
+        got = host(sb.gather(cu(x), cu(idx), b, k, s, to_dev_epi(epi)))
+        assert bits_equal(got, want)
+
+
+def test_silu_relu_epilogue_zero_fill_untouched(orc):
+    # test_kernels.cpp:94-112
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (2, 3, 9, 9)).astype(np.float32)
+    idx = np.array([[0, 0, 0], [0, 3, 3], [1, 6, 6]], np.int32)
+    epi = rand_epi_np(rng, 3)
+    got = host(sb.gather(cu(x), cu(idx), 3, 3, 1, to_dev_epi(epi)))
+    assert got[0, 0, 0, 0] == 0.0
+    assert bits_equal(got, orc.gather(x, idx, 3, 9, 9, 3, 1, epi))
+    epi = [("act", sb.ACT_RELU)]
+    x[0, 0, 1, 1] = -0.0
+    assert bits_equal(host(sb.gather(cu(x), cu(idx), 3, 3, 1, to_dev_epi(epi))), orc.gather(x, idx, 3, 9, 9, 3, 1, epi))
+
+
+def test_scatter_family_matches_oracle(orc):
+    rng = np.random.default_rng(81)
+    for rep in range(12):
+        n, c, h, w = int(rng.integers(1, 3)), int(rng.integers(1, 6)), int(rng.integers(5, 30)), int(rng.integers(5, 30))
+        b = int(rng.integers(1, 7))
+        m = (rng.random((h, w)) < 0.1).astype(np.uint8)
+        idx, _ = orc.mask_to_block_indices(m, b, n)
+        blocks = rng.uniform(-1, 1, (len(idx), c, b, b)).astype(np.float32)
+        base = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+        assert bits_equal(host(sb.scatter(cu(blocks), cu(idx), cu(base))), orc.scatter(blocks, idx, base))
+        tb = cu(base)
+        sb.scatter_add_inplace(cu(blocks), cu(idx), tb)
+        assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
+
+
+def test_scatter_clips_fringe_tiles():
+    # test_kernels.cpp:136-145
+    base = cu(np.zeros((1, 1, 5, 5), np.float32))
+    sb.scatter_inplace(cu(np.full((1, 1, 4, 4), 3.0, np.float32)), cu(np.array([[0, 4, 4]], np.int32)), base)
+    out = host(base)
+    assert out[0, 0, 4, 4] == 3.0 and (out != 0).sum() == 1
+
+
+def test_scatter_map_and_scatter_gather_match_oracle(orc):
+    rng = np.random.default_rng(93)
+    for rep in range(10):
+        h, c, n = 12 + rep, 3, 2
+        pm = np.zeros((h, h), np.uint8)
+        for _ in range(3):
+            pm[rng.integers(0, h), rng.integers(0, h)] = 1
+        prod, _ = orc.mask_to_block_indices(pm, 4, n)
+        blocks = rng.uniform(-1, 1, (len(prod), c, 4, 4)).astype(np.float32)
+        base = rng.uniform(-1, 1, (n, c, h, h)).astype(np.float32)
+        cm = np.zeros((h, h), np.uint8)
+        cm[0, 0] = 1
+        cm[rng.integers(0, h), rng.integers(0, h)] = 1
+        cons, _ = orc.mask_to_block_indices(cm, 4, n)
+        want_map, want_bps = orc.build_scatter_map(prod, 4, h, h)
+        got_map, got_bps = sb.build_scatter_map(cu(prod), 4, h, h)
+        assert got_bps == want_bps
+        assert np.array_equal(host(got_map).view(np.uint8).ravel(), want_map.view(np.uint8).ravel())
+        epi = rand_epi_np(rng, c) if rep % 2 == 0 else []
+        k = 1 if rep % 3 == 0 else 3
+        want = orc.scatter_gather(blocks, prod, base, cons, 4, h, h, k, 1, epi)
+        got = host(sb.scatter_gather(cu(blocks), cu(base), (got_map, got_bps), cu(cons), 4, k, 1, to_dev_epi(epi)))
+        assert bits_equal(got, want)
+
+
+def test_scatter_map_rejects_batch_pattern_mismatch():
+    idx = cu(np.array([[0, 0, 0], [1, 4, 4]], np.int32))
+    with pytest.raises(sb.ConfigError, match="tile pattern differs across batch"):
+        sb.build_scatter_map(idx, 4, 8, 8)
+
+
+def test_block_residual_fused_equals_unfused_and_oracle(orc):
+    # test_kernels.cpp:250-286
+    rng = np.random.default_rng(103)
+    for rep in range(8):
+        h, c, n = 16, 4, 1 + rep % 2
+        s_ = rng.uniform(-1, 1, (n, c, h, h)).astype(np.float32)
+        osc = rng.uniform(-1, 1, (n, c, h, h)).astype(np.float32)
+        mm = np.zeros((h, h), np.uint8)
+        smk = np.zeros((h, h), np.uint8)
+        for _ in range(3):
+            mm[rng.integers(0, h), rng.integers(0, h)] = 1
+            smk[rng.integers(0, h), rng.integers(0, h)] = 1
+        mi, _ = orc.mask_to_block_indices(orc.dilate_mask(mm, 1), 6, n)
+        si, _ = orc.mask_to_block_indices(smk, 4, n)
+        mb = rng.uniform(-1, 1, (len(mi), c, 6, 6)).astype(np.float32)
+        pb = rng.uniform(-1, 1, (len(si), c, 4, 4)).astype(np.float32)
+        want = orc.scatter_with_block_residual(mb, mi, pb, si, s_, osc, True)
+        assert bits_equal(want, orc.scatter_with_block_residual(mb, mi, pb, si, s_, osc, False))
+        f = host(sb.scatter_with_block_residual(cu(mb), cu(mi), cu(pb), cu(si), cu(s_), cu(osc)))
+        u = host(sb.scatter_with_block_residual_unfused(cu(mb), cu(mi), cu(pb), cu(si), cu(s_), cu(osc)))
+        assert bits_equal(f, want) and bits_equal(u, want)
+
+
+def test_block_arithmetic_and_epilogue_on_blocks(orc):
+    rng = np.random.default_rng(139)
+    a = np.arange(8, dtype=np.float32).reshape(2, 1, 2, 2)
+    b = np.full_like(a, 10.0)
+    assert host(sb.add_blocks(cu(a), cu(b))).ravel()[3] == 13.0
+    assert host(sb.subtract_blocks(cu(a), cu(b))).ravel()[3] == -7.0
+    idx = np.array([[0, 0, 0], [1, 4, 4]], np.int32)
+    s = rng.uniform(-1, 1, (2, 3, 4, 4)).astype(np.float32)
+    epi = rand_epi_np(rng, 3, n=2, per_sample=True)
+    t = cu(s)
+    sb.apply_epilogue_on_blocks(t, cu(idx), to_dev_epi(epi))
+    assert bits_equal(host(t), orc.apply_epilogue_on_blocks(s, idx, 8, 8, epi))
+
+
+@pytest.mark.parametrize("math", [sb.MATH_EXACT, sb.MATH_FP32_FMA])
+def test_conv_on_blocks_and_conv2d(orc, math):
+    # test_kernels.cpp:288-351: conv_on_blocks over a whole-canvas tile == conv2d
+    rng = np.random.default_rng(113)
+    for k in (1, 3):
+        for s in (1, 2):
+            x = rng.uniform(-1, 1, (2, 3, 8, 8)).astype(np.float32)
+            wt = rng.uniform(-0.5, 0.5, (5, 3, k, k)).astype(np.float32)
+            bias = rng.uniform(-0.2, 0.2, 5).astype(np.float32)
+            oh = (8 + 2 * ((k - 1) // 2) - k) // s + 1
+            idx = np.array([[0, 0, 0], [1, 0, 0]], np.int32)
+            g = orc.gather(x, idx, oh, oh, oh, k, s)
+            want_blocks = orc.conv_on_blocks(g, wt, bias, k, s, oh)
+            want_dense = orc.conv2d(x, wt, bias, k, s)
+            got_blocks = host(sb.conv_on_blocks(cu(g), cu(wt), cu(bias), s, oh, math=math))
+            got_dense = host(sb.conv2d(cu(x), cu(wt), cu(bias), s, math=math))
+            if math == sb.MATH_EXACT:
+                assert bits_equal(got_blocks, want_blocks) and bits_equal(got_dense, want_dense)
+                assert bits_equal(want_blocks.transpose(1, 0, 2, 3).reshape(5, 2, oh, oh), want_dense.transpose(1, 0, 2, 3))
+            else:
+                assert np.abs(got_dense - want_dense).max() <= 1e-4 * np.abs(want_dense).max()
+
+
+def test_conv_on_blocks_geometry_error():
+    with pytest.raises(sb.ConfigError, match="conv_on_blocks: window 8 with k=3 s=1 yields 6, expected block 5"):
+        sb.conv_on_blocks(cu(np.zeros((1, 2, 8, 8), np.float32)), cu(np.zeros((2, 2, 3, 3), np.float32)), None, 1, 5)
