@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the SIGE sparse-update path on B200 (BASELINE.json metric).
+
+Workload (N=1 line): BASELINE config 2 — the DDIM-UNet-shaped residual stack
+(ddim_stack: 3x256x256 input, 128-512 channels, 51 layers / 80 conv sites,
+random init from Rng seed 2211) with the reference's rect1 edit (1.196 % of
+pixels, seed 7), dilate_full 5, dilate_scale 1, min_sparse_res 64 (the paper's
+policy), block 6 (3x3) / 4 (1x1). One step = one sparse edit:
+difference mask -> on-device IndexPlan -> all 80 fused gather/conv/scatter
+launches -> final output, on inputs resident in HBM. L2 (126 MB) is flushed
+between timed steps (a 512 MB write outside the per-step CUDA events).
+
+`value` is the mean per-edit latency in ms (lower is better); `e2e` is the
+same edit through the C-ABI host-buffer entry point (H2D of the edited image,
+D2H of the output inside the timed region). The dense B200 pass (the same
+kernels over every tile) gives `speedup_vs_dense`. `--impl reference` times
+the unmodified reference (oracle/_ref, compiled from /root/reference) on the
+host cores instead. With torchrun (N>1) every rank runs its own edit per step
+(request i -> GPU i mod N, BASELINE config 5 sharding; no collective on the
+data path); the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-edit latency ms & speedup vs dense at 1.2% edit; gather/scatter GB/s"
+WORKLOAD = dict(model="ddim_stack", fixture="rect1", seed=7, dilate_full=5, dilate_scale=1,
+                min_sparse_res=64, block3=6, block1=4)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--math", default="tf32", choices=["tf32", "exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-edits", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------ reference --
+
+def reference_setup(model_name, fx, seed, n_threads, cache_from=None):
+    """Reference model + cache + inputs through oracle/_ref (the unmodified
+    reference compiled from /root/reference). cache_from: an engine whose
+    device cache seeds the reference cache (skips the untimed CPU precompute)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle
+
+    R = oracle.ref()
+    os.environ["SIGE_THREADS"] = str(n_threads)
+    rm = R.model(model_name)
+    c, h, w = (3, 256, 256) if model_name == "ddim_stack" else (64, 256, 256)
+    orig, edited = R.make_edit_fixture(fx, 1, c, h, w, seed)
+    mask = R.difference_mask(orig, edited)
+    if cache_from is None:
+        cache = rm.precompute(orig)
+    else:
+        L = R.lib
+        L.ref_cache_create_for.restype = C.c_void_p
+        L.ref_cache_create_for.argtypes = [C.c_void_p]
+        L.ref_cache_put_tensor.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_void_p] + [C.c_int] * 4
+        L.ref_cache_put_norm.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_void_p, C.c_void_p, C.c_int]
+        h_cache = L.ref_cache_create_for(rm.h)
+        for kind, key, shp in cache_from.cache_entries(0):
+            if kind == "T":
+                t = cache_from.get_tensor(key, shp).numpy()
+                assert L.ref_cache_put_tensor(h_cache, 0, key.encode(), t.ctypes.data, *shp) == 0
+            else:
+                sc, sh = (np.ascontiguousarray(a.numpy(), np.float32) for a in cache_from.get_norm(key, shp))
+                assert L.ref_cache_put_norm(h_cache, 0, key.encode(), sc.ctypes.data, sh.ctypes.data, shp) == 0
+        cache = oracle.Cache(R, h_cache)
+    return R, rm, cache, orig, edited, mask
+
+
+def time_reference_edits(rm, cache, edited, mask, cfg, edits):
+    ts = []
+    for _ in range(edits):
+        t0 = time.perf_counter()
+        rm.sparse_forward(cache, edited, mask, cfg)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return ts
+
+
+def main_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2211_02048_b200 as sb
+
+    nthreads = os.cpu_count() or 1
+    cfg = sb.default_config(**{k: WORKLOAD[k] for k in ("dilate_full", "dilate_scale", "min_sparse_res", "block3", "block1")})
+    try:
+        R, rm, cache, orig, edited, mask = reference_setup(WORKLOAD["model"], WORKLOAD["fixture"], WORKLOAD["seed"], nthreads)
+    except Exception as e:  # reference library missing on this box
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
+        return
+    time_reference_edits(rm, cache, edited, mask, cfg, max(1, min(args.warmup, 1)))
+    ts = time_reference_edits(rm, cache, edited, mask, cfg, args.steps)
+    v = sum(ts) / len(ts)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference Rng fixtures, seed 7)",
+        "config": {"workload": "config2 ddim_stack 3x256x256 rect1 1.2% edit, dilate_full 5, min_sparse_res 64",
+                   **WORKLOAD},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": nthreads, "kind": "reference",
+                         "sample": f"{args.steps} sparse_forward edits of config 2 at SIGE_THREADS={nthreads}"},
+        "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# -------------------------------------------------------------- ours -----
+
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_02048_b200 as sb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    math = sb.MATH_TF32 if args.math == "tf32" else sb.MATH_EXACT
+    cfg = sb.default_config(**{k: WORKLOAD[k] for k in ("dilate_full", "dilate_scale", "min_sparse_res", "block3", "block1")})
+
+    model = sb.Model(WORKLOAD["model"])
+    c, h, w = model.in_shape
+    # request i -> GPU i mod N: rank r serves seeds 7 + r, 7 + r + N, ...
+    seed = WORKLOAD["seed"] + rank
+    orig, edited = sb.make_edit_fixture(WORKLOAD["fixture"], 1, c, h, w, seed)
+    eng = sb.Engine(model, batch=1, math=math)
+    orig_d, edited_d = orig.to(dev), edited.to(dev)
+    eng.precompute(orig_d)
+    out = torch.empty(eng.output_shape(), device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        eng.sparse_forward(edited_d, config=cfg, out=out)
+    torch.cuda.synchronize()
+    launches_per_step = eng.last_launch_count()
+
+    # ---- timed region: K steps, per-step events, L2 flushed in between
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(dev.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    l0 = sb.kernel_launch_count()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        eng.sparse_forward(edited_d, config=cfg, out=out)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = sb.kernel_launch_count() - l0
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    per = [a.elapsed_time(b) for a, b in ev]
+    total = torch.tensor([sum(per)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = total.item() / args.steps
+
+    # ---- trace-derived traffic (gathered/scattered elements, MACs)
+    tr = eng.trace().numpy()
+    gathered, scattered = int(tr[:, 1].sum()), int(tr[:, 2].sum())
+    macs, dense_macs = int(tr[:, 3].sum()), int(tr[:, 4].sum())
+    active_blocks = int(tr[tr[:, 5] == 1, 0].sum())
+
+    # ---- dense B200 pass (same kernels over every tile, fresh statistics)
+    for _ in range(2):
+        eng.dense_forward(edited_d)
+    torch.cuda.synchronize()
+    dts = []
+    for _ in range(max(3, min(10, args.steps))):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.dense_forward(edited_d)
+        b.record(stream)
+        torch.cuda.synchronize()
+        dts.append(a.elapsed_time(b))
+    dense_ms = sum(dts) / len(dts)
+
+    # ---- e2e through the C-ABI host-buffer entry point (pinned buffers)
+    edited_h = edited.pin_memory()
+    out_h = torch.empty(eng.output_shape(), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        eng.sparse_forward_host(edited_h, config=cfg, out_host=out_h)
+    e2e = []
+    for _ in range(max(3, min(10, args.steps))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.sparse_forward_host(edited_h, config=cfg, out_host=out_h)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    e2e_t = torch.tensor([sum(e2e) / len(e2e)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = e2e_t.item()
+
+    # ---- roofline of the dominant kernel (k_conv_tc), CUDA events per launch
+    eng.set_profiling(True)
+    for _ in range(3):
+        flush.zero_()
+        eng.sparse_forward(edited_d, config=cfg, out=out)
+    eng.set_profiling(False)
+    prof = eng.profile_read().numpy()
+    conv_ms = float(prof[:, 0].sum()) / 3.0
+    conv_flops = float(prof[:, 1].sum()) / 3.0
+    n_conv = len(prof) // 3
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    # TF32 runs at half the bf16 tensor rate on Blackwell; the measured bf16
+    # cuBLAS number is the denominator the driver asks for.
+    achieved_tf = conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
+
+    if rank != 0:
+        dist.barrier() if world > 1 else None
+        return
+    gs_bytes = (gathered + scattered) * 4 * 2
+    line = {
+        "metric": METRIC,
+        "value": round(ms_per_step, 4),
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "tf32" if math == sb.MATH_TF32 else "f32",
+        "data": "synthetic (reference Rng fixtures + random-init weights, seed 2211)",
+        "config": {"workload": "config2 ddim_stack 3x256x256 rect1 1.2% edit (784 px), one edit per GPU per step",
+                   **WORKLOAD, "batch": 1, "l2": "flushed between steps (512 MB write)",
+                   "parallelism": f"request-sharded x{world} (no data-path collective)"},
+        "speedup_vs_dense": round(dense_ms / ms_per_step, 3),
+        "dense_ms": round(dense_ms, 4),
+        "edits_per_s": round(world * 1e3 / ms_per_step, 2),
+        "gather_scatter_gbs": round(gs_bytes / (ms_per_step * 1e-3) / 1e9, 2),
+        "trace": {"active_blocks": active_blocks, "gathered_elems": gathered, "scattered_elems": scattered,
+                  "macs": macs, "dense_macs": dense_macs, "mac_reduction": round(dense_macs / max(macs, 1), 3)},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms",
+                "h2d_bytes_per_step": int(edited.numel() * 4), "d2h_bytes_per_step": int(out.numel() * 4)},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches_per_step,
+        "wall_s_timed": round(wall, 3),
+        "roofline": {"bound": "tensor", "kernel": "k_conv_tc (fused gather->tcgen05 tf32 GEMM->scatter)",
+                     "achieved": round(achieved_tf, 3), "peak": bf16_peak, "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / bf16_peak, 5), "peak_source": f"bf16 {peak_src}",
+                     "tf32_note": "kind::tf32 issues at half the bf16 rate",
+                     "launches_per_step": n_conv, "conv_ms_per_step": round(conv_ms, 4),
+                     "algorithmic_flops_per_step": conv_flops, "traffic": None},
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            nthreads = os.cpu_count() or 1
+            R, rm, cache, o2, e2, m2 = reference_setup(WORKLOAD["model"], WORKLOAD["fixture"], WORKLOAD["seed"],
+                                                       nthreads, cache_from=eng)
+            ts = time_reference_edits(rm, cache, e2, m2, cfg, args.cpu_sample_edits)
+            line["cpu_baseline"] = {"value": round(sum(ts) / len(ts), 3), "unit": "ms", "cores": nthreads,
+                                    "kind": "reference",
+                                    "sample": f"{len(ts)} sparse_forward edits of config 2 (oracle/_ref, "
+                                              f"SIGE_THREADS={nthreads}, cache seeded from the device precompute)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -258,6 +258,9 @@ int sige_engine_put_norm(sige_engine* eng, int step, const char* key, const floa
 /* Download a cache entry (host NCHW) — for tests. */
 int sige_engine_get_tensor(sige_engine* eng, int step, const char* key, float* host_nchw,
                            size_t numel);
+/* Download a folded norm entry (scale, shift: `numel` values each). */
+int sige_engine_get_norm(sige_engine* eng, int step, const char* key, float* host_scale,
+                         float* host_shift, size_t numel);
 /* sparse_forward (graph.hpp:224-226, graph.cpp:619-901). edited is device NCHW;
  * mask (device u8 H*W) may be NULL, in which case the engine computes it
  * against the cached original input with cfg->mask_threshold (mask.cpp:14-32).
@@ -284,6 +287,19 @@ int sige_engine_last_launch_count(const sige_engine* eng);
  * Synchronises the stream. */
 int sige_engine_trace(sige_engine* eng, uint64_t* rows, int cap, int* nrows,
                       sige_stream_t stream);
+/* Per-conv-launch profiling (CUDA events around each fused conv launch of
+ * subsequent engine calls; off by default). sige_engine_profile_read
+ * synchronises the stream and returns up to `cap` rows of {ms, algorithmic
+ * flops (2*MACs over the tiles actually processed), tensor-core flag}, then
+ * clears the record. */
+int sige_engine_set_profiling(sige_engine* eng, int enable);
+int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows,
+                             sige_stream_t stream);
+/* Newline-separated cache listing for `step`: "T <key> <n> <c> <h> <w>" for
+ * tensors (reference NCHW shape) and "N <key> <count>" for folded norms.
+ * Returns the needed buffer size in *needed. */
+int sige_engine_cache_entries(const sige_engine* eng, int step, char* buf, size_t cap,
+                              size_t* needed);
 /* Bytes of device memory held by the cache (ActivationCache::element_breakdown
  * * 4, graph.cpp:287-302). */
 size_t sige_engine_cache_bytes(const sige_engine* eng);

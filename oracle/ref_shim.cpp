@@ -611,3 +611,35 @@ int ref_output_coverage(void* model, const uint8_t* mask, int h, int w, int batc
 }
 
 }  // extern "C"
+
+// Cache construction through the reference's public ActivationCache API
+// (graph.hpp:116-156) — lets bench.py's CPU baseline skip the (untimed)
+// dense precompute by seeding the reference cache with already computed
+// entries.
+extern "C" {
+
+void* ref_cache_create_for(void* model) {
+  auto* c = new ActivationCache();
+  c->set_model_hash(static_cast<ModelSpec*>(model)->structure_hash());
+  return c;
+}
+
+int ref_cache_put_tensor(void* cache, int step, const char* key, const float* data, int n, int c,
+                         int h, int w) {
+  return guarded([&] {
+    static_cast<ActivationCache*>(cache)->put_tensor(step, key, to_tensor(data, n, c, h, w),
+                                                     CacheCategory::ConvOutput);
+  });
+}
+
+int ref_cache_put_norm(void* cache, int step, const char* key, const float* scale,
+                       const float* shift, int count) {
+  return guarded([&] {
+    FoldedNorm f;
+    f.scale.assign(scale, scale + count);
+    f.shift.assign(shift, shift + count);
+    static_cast<ActivationCache*>(cache)->put_norm(step, key, std::move(f));
+  });
+}
+
+}  // extern "C"

@@ -387,6 +387,12 @@ class Engine:
         _check(_lib().sige_engine_get_tensor(self.h, step, key.encode(), out.data_ptr(), out.numel()))
         return out
 
+    def get_norm(self, key: str, count: int, step: int = 0):
+        sc = torch.empty(count, dtype=torch.float32)
+        sh = torch.empty(count, dtype=torch.float32)
+        _check(_lib().sige_engine_get_norm(self.h, step, key.encode(), sc.data_ptr(), sh.data_ptr(), count))
+        return sc, sh
+
     def sparse_forward(self, edited: torch.Tensor, mask: torch.Tensor | None = None,
                        config: RunConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
         e = _dev(edited, torch.float32, "sparse_forward")
@@ -422,6 +428,31 @@ class Engine:
         n = C.c_int(0)
         _check(_lib().sige_engine_trace(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
         return rows[: n.value].clone()
+
+    def set_profiling(self, on: bool) -> None:
+        _check(_lib().sige_engine_set_profiling(self.h, int(on)))
+
+    def profile_read(self, cap: int = 4096):
+        """[(ms, flops, tensor_core)] of the fused conv launches since the last read."""
+        rows = torch.zeros((cap, 3), dtype=torch.float64)
+        n = C.c_int(0)
+        _check(_lib().sige_engine_profile_read(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
+        return rows[: n.value].clone()
+
+    def cache_entries(self, step: int = 0):
+        """[("T", key, (n, c, h, w)) | ("N", key, count)] of the device cache."""
+        need = C.c_size_t(0)
+        _check(_lib().sige_engine_cache_entries(self.h, step, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(_lib().sige_engine_cache_entries(self.h, step, buf, need.value, C.byref(need)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            f = line.split()
+            if f[0] == "T":
+                out.append(("T", f[1], tuple(int(v) for v in f[2:6])))
+            else:
+                out.append(("N", f[1], int(f[2])))
+        return out
 
     def cache_bytes(self) -> int:
         return int(_lib().sige_engine_cache_bytes(self.h))

@@ -177,6 +177,7 @@ SYMBOLS = {
     "sige_engine_put_tensor": (_i, [_vp, _i, C.c_char_p, _vp, _sz]),
     "sige_engine_put_norm": (_i, [_vp, _i, C.c_char_p, _vp, _vp, _sz]),
     "sige_engine_get_tensor": (_i, [_vp, _i, C.c_char_p, _vp, _sz]),
+    "sige_engine_get_norm": (_i, [_vp, _i, C.c_char_p, _vp, _vp, _sz]),
     "sige_engine_sparse_forward": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, _vp]),
     "sige_engine_sparse_forward_host": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, _vp]),
     "sige_engine_dense_forward": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
@@ -184,6 +185,9 @@ SYMBOLS = {
     "sige_engine_last_launch_count": (_i, [_vp]),
     "sige_engine_trace": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_bytes": (_sz, [_vp]),
+    "sige_engine_set_profiling": (_i, [_vp, _i]),
+    "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
+    "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),
     "sige_model_build": (_i, [C.c_char_p, C.POINTER(C.POINTER(ModelDesc))]),
     "sige_model_free": (None, [C.POINTER(ModelDesc)]),

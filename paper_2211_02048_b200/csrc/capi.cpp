@@ -308,6 +308,11 @@ int sige_engine_get_tensor(sige_engine* eng, int step, const char* key, float* h
   return guarded([&] { eng->impl->get_tensor(step, key, host, numel); });
 }
 
+int sige_engine_get_norm(sige_engine* eng, int step, const char* key, float* sc, float* sh,
+                         size_t numel) {
+  return guarded([&] { eng->impl->get_norm(step, key, sc, sh, numel); });
+}
+
 int sige_engine_sparse_forward(sige_engine* eng, const float* edited, const uint8_t* mask,
                                const sige_run_config* cfg, float* out, sige_stream_t s) {
   return guarded([&] {
@@ -393,6 +398,22 @@ int sige_engine_last_launch_count(const sige_engine* eng) { return eng ? eng->im
 
 int sige_engine_trace(sige_engine* eng, uint64_t* rows, int cap, int* nrows, sige_stream_t s) {
   return guarded([&] { *nrows = eng->impl->trace(rows, cap, as_stream(s)); });
+}
+
+int sige_engine_set_profiling(sige_engine* eng, int enable) {
+  return guarded([&] { eng->impl->set_profiling(enable != 0); });
+}
+
+int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows, sige_stream_t s) {
+  return guarded([&] { *nrows = eng->impl->profile_read(rows, cap, as_stream(s)); });
+}
+
+int sige_engine_cache_entries(const sige_engine* eng, int step, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    std::string s = eng->impl->cache_entries(step);
+    *needed = s.size() + 1;
+    if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
 }
 
 size_t sige_engine_cache_bytes(const sige_engine* eng) { return eng ? eng->impl->cache_bytes() : 0; }

@@ -281,10 +281,69 @@ Tiles Engine::dense_tiles(int oh, int ow) {
 
 void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& dst,
                   cudaStream_t st) const {
+  ProfRec rec{};
+  if (profiling_) {
+    for (cudaEvent_t* e : {&rec.a, &rec.b}) {
+      if (ev_pool_.empty()) {
+        SIGE_CUDA(cudaEventCreate(e));
+      } else {
+        *e = ev_pool_.back();
+        ev_pool_.pop_back();
+      }
+    }
+    SIGE_CUDA(cudaEventRecord(rec.a, st));
+  }
   if (math_ == SIGE_MATH_TF32)
     launch_conv_tc(src, t, cw, dst, st);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
+  if (profiling_) {
+    SIGE_CUDA(cudaEventRecord(rec.b, st));
+    rec.count_dev = t.count_dev;
+    rec.count = t.count;
+    // algorithmic FLOPs per tile: 2 * C_out * C_in * k^2 * (pixels of the
+    // tile inside the canvas ~ bh*bw; fringe clipping ignored)
+    rec.flops_per_tile = 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * t.bh * t.bw;
+    rec.tc = math_ == SIGE_MATH_TF32;
+    prof_.push_back(rec);
+  }
+}
+
+void Engine::set_profiling(bool on) { profiling_ = on; }
+
+int Engine::profile_read(double* rows, int cap, cudaStream_t st) {
+  SIGE_CUDA(cudaStreamSynchronize(st));
+  int n = 0;
+  for (const ProfRec& r : prof_) {
+    if (n < cap && rows) {
+      float ms = 0.0f;
+      SIGE_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      int32_t cnt = r.count;
+      if (r.count_dev) SIGE_CUDA(cudaMemcpy(&cnt, r.count_dev, sizeof cnt, cudaMemcpyDeviceToHost));
+      rows[3 * n] = ms;
+      rows[3 * n + 1] = r.flops_per_tile * cnt;
+      rows[3 * n + 2] = r.tc;
+    }
+    ev_pool_.push_back(r.a);
+    ev_pool_.push_back(r.b);
+    ++n;
+  }
+  prof_.clear();
+  return n;
+}
+
+std::string Engine::cache_entries(int step) const {
+  std::ostringstream o;
+  for (auto& kv : cache_) {
+    if (kv.first.first != step || kv.first.second == "input") continue;
+    const DevTensor& t = kv.second;
+    o << "T " << kv.first.second << ' ' << t.n << ' ' << t.c << ' ' << t.h << ' ' << t.w << '\n';
+  }
+  for (auto& kv : norms_) {
+    if (kv.first.first != step) continue;
+    o << "N " << kv.first.second << ' ' << kv.second.np << '\n';
+  }
+  return o.str();
 }
 
 // fold_norm_layer (graph.cpp:310-322).
@@ -465,6 +524,14 @@ void Engine::put_norm(int step, const std::string& key, const float* sc, const f
   DevNorm& n = norm_slot(step, key, static_cast<int>(np));
   SIGE_CUDA(cudaMemcpy(n.scale, sc, np * sizeof(float), cudaMemcpyHostToDevice));
   SIGE_CUDA(cudaMemcpy(n.shift, sh, np * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void Engine::get_norm(int step, const std::string& key, float* sc, float* sh, size_t np) {
+  const DevNorm& n = cache_norm(step, key);
+  if (np != static_cast<size_t>(n.np)) throw ConfigError("cache norm " + key + ": size mismatch");
+  SIGE_CUDA(cudaDeviceSynchronize());
+  SIGE_CUDA(cudaMemcpy(sc, n.scale, np * sizeof(float), cudaMemcpyDeviceToHost));
+  SIGE_CUDA(cudaMemcpy(sh, n.shift, np * sizeof(float), cudaMemcpyDeviceToHost));
 }
 
 void Engine::get_tensor(int step, const std::string& key, float* host, size_t numel) {

@@ -67,6 +67,7 @@ class Engine {
   void put_tensor(int step, const std::string& key, const float* host_nchw, size_t numel);
   void put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np);
   void get_tensor(int step, const std::string& key, float* host_nchw, size_t numel);
+  void get_norm(int step, const std::string& key, float* sc, float* sh, size_t np);
   void sparse_forward(const float* edited, const uint8_t* mask, const sige_run_config& cfg,
                       float* out, cudaStream_t st);
   void dense_forward(const float* in, bool reused_stats, int step, float* out, cudaStream_t st);
@@ -75,6 +76,9 @@ class Engine {
   int last_launch_count() const { return last_launches_; }
   int trace(uint64_t* rows, int cap, cudaStream_t st);
   size_t cache_bytes() const;
+  void set_profiling(bool on);
+  int profile_read(double* rows, int cap, cudaStream_t st);
+  std::string cache_entries(int step) const;
   int in_channels() const { return in_c_; }
   int in_h() const { return in_h_; }
   int in_w() const { return in_w_; }
@@ -113,6 +117,16 @@ class Engine {
   std::map<std::string, std::unique_ptr<Program>> programs_;
   Program* last_program_ = nullptr;
   int last_launches_ = 0;
+  struct ProfRec {
+    cudaEvent_t a, b;
+    const int32_t* count_dev;
+    int count;
+    double flops_per_tile;
+    int tc;
+  };
+  bool profiling_ = false;
+  mutable std::vector<ProfRec> prof_;
+  mutable std::vector<cudaEvent_t> ev_pool_;
   // per-call bindings read by program steps
   const float* cur_in_ = nullptr;
   float* cur_out_ = nullptr;
