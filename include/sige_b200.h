@@ -148,7 +148,8 @@ typedef struct sige_scatter_entry {
 enum {
   SIGE_MATH_EXACT = 0, /* fp32 CUDA cores, reference accumulation order, no FMA: bit-exact */
   SIGE_MATH_TF32 = 1,  /* tcgen05.mma kind::tf32, fp32 accumulators in TMEM */
-  SIGE_MATH_FP32_FMA = 2 /* fp32 CUDA cores with FMA (1e-4 check mode) */
+  SIGE_MATH_FP32_FMA = 2, /* fp32 CUDA cores with FMA (1e-4 check mode) */
+  SIGE_MATH_F16 = 3 /* tcgen05.mma kind::f16 with fp16 operands, fp32 accumulators in TMEM */
 };
 
 /* ---- mask reduction (proj/include/sige/mask.hpp) -------------------------- */
@@ -293,6 +294,10 @@ int sige_engine_trace(sige_engine* eng, uint64_t* rows, int cap, int* nrows,
  * flops (2*MACs over the tiles actually processed), tensor-core flag}, then
  * clears the record. */
 int sige_engine_set_profiling(sige_engine* eng, int enable);
+/* CUDA-graph replay of sparse_forward (on by default): after one direct run,
+ * each (edited, mask, out) pointer binding is captured once and replayed with a
+ * single graph launch. Results are identical either way. */
+int sige_engine_set_graphs(sige_engine* eng, int enable);
 int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows,
                              sige_stream_t stream);
 /* Newline-separated cache listing for `step`: "T <key> <n> <c> <h> <w>" for

@@ -22,6 +22,7 @@ from ._capi import (  # noqa: F401  (re-exported constants)
     ACT_RELU,
     ACT_SILU,
     MATH_EXACT,
+    MATH_F16,
     MATH_FP32_FMA,
     MATH_TF32,
     RunConfig,
@@ -428,6 +429,9 @@ class Engine:
         n = C.c_int(0)
         _check(_lib().sige_engine_trace(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
         return rows[: n.value].clone()
+
+    def set_graphs(self, on: bool) -> None:
+        _check(_lib().sige_engine_set_graphs(self.h, int(on)))
 
     def set_profiling(self, on: bool) -> None:
         _check(_lib().sige_engine_set_profiling(self.h, int(on)))

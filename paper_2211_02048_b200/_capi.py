@@ -24,7 +24,7 @@ EPI_SCALE_SHIFT, EPI_ACTIVATION = 0, 1
 MAX_EPI_STEPS = 4
 NORM_GROUP, NORM_INSTANCE, NORM_BATCH = 0, 1, 2
 LAYER_CONV, LAYER_NORM, LAYER_ACTIVATION, LAYER_RESBLOCK, LAYER_DOWNSAMPLE, LAYER_UPSAMPLE = range(6)
-MATH_EXACT, MATH_TF32, MATH_FP32_FMA = 0, 1, 2
+MATH_EXACT, MATH_TF32, MATH_FP32_FMA, MATH_F16 = 0, 1, 2, 3
 
 FloatP = C.POINTER(C.c_float)
 
@@ -186,6 +186,7 @@ SYMBOLS = {
     "sige_engine_trace": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_bytes": (_sz, [_vp]),
     "sige_engine_set_profiling": (_i, [_vp, _i]),
+    "sige_engine_set_graphs": (_i, [_vp, _i]),
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),

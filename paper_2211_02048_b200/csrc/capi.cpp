@@ -404,6 +404,10 @@ int sige_engine_set_profiling(sige_engine* eng, int enable) {
   return guarded([&] { eng->impl->set_profiling(enable != 0); });
 }
 
+int sige_engine_set_graphs(sige_engine* eng, int enable) {
+  return guarded([&] { eng->impl->set_graphs(enable != 0); });
+}
+
 int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows, sige_stream_t s) {
   return guarded([&] { *nrows = eng->impl->profile_read(rows, cap, as_stream(s)); });
 }

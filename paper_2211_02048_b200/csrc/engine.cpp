@@ -51,6 +51,7 @@ Src plain(const DevTensor& t) {
   s.c = t.c;
   s.h = t.h;
   s.w = t.w;
+  s.half = t.half;
   s.epi.fma_expf = host_expf_is_fma() ? 1 : 0;
   return s;
 }
@@ -82,13 +83,19 @@ struct Program {
   int32_t* any = nullptr;
   int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
   int launches = 0;
+  bool ran = false;
+  std::map<std::tuple<const void*, const void*, const void*>, std::pair<cudaGraphExec_t, int>> graphs;
+  ~Program() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+  }
 };
 
 // ----------------------------------------------------------- basics -----
 
 Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), math_(math) {
   if (batch < 1) throw ConfigError("engine: batch must be >= 1");
-  if (math != SIGE_MATH_EXACT && math != SIGE_MATH_TF32 && math != SIGE_MATH_FP32_FMA)
+  if (math != SIGE_MATH_EXACT && math != SIGE_MATH_TF32 && math != SIGE_MATH_FP32_FMA &&
+      math != SIGE_MATH_F16)
     throw ConfigError("engine: unknown math mode " + std::to_string(math));
   shapes_ = walk_shapes(m);
   name_ = m->name ? m->name : "";
@@ -112,9 +119,9 @@ Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), m
     w.stride = c.stride;
     w.w = upload(c.weight, static_cast<size_t>(c.c_out) * c.c_in * c.k * c.k);
     w.bias = upload(c.bias, c.c_out);
-    if (math_ == SIGE_MATH_TF32) {
-      w.w_tc = pack_weights_tc(w.w, c.c_out, c.c_in, c.k, &w.n_pad, &w.k_pad, nullptr);
-      allocations_.push_back(const_cast<float*>(w.w_tc));
+    if (tensor_cores()) {
+      pack_weights_tc(w.w, c.c_out, c.c_in, c.k, math_ == SIGE_MATH_F16 ? 1 : 0, &w, nullptr);
+      allocations_.push_back(const_cast<void*>(w.w_tc));
     }
     return w;
   };
@@ -150,9 +157,14 @@ Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), m
 }
 
 Engine::~Engine() {
-  for (auto& kv : programs_) {
-    (void)kv;
+  cudaDeviceSynchronize();
+  programs_.clear();  // destroys captured graphs
+  for (auto& r : prof_) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
   }
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (cap_stream_) cudaStreamDestroy(cap_stream_);
   for (void* p : allocations_) cudaFree(p);
 }
 
@@ -194,17 +206,35 @@ const DevNorm& Engine::cache_norm(int step, const std::string& key) const {
   return it->second;
 }
 
-DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, int w, int layout) {
+DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, int w, int layout, int half) {
   DevTensor& t = cache_[{step, key}];
-  if (!t.p || t.c != c || t.h != h || t.w != w || t.n != batch_ || t.layout != layout) {
-    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * sizeof(float)));
+  if (!t.p || t.c != c || t.h != h || t.w != w || t.n != batch_ || t.layout != layout || t.half != half) {
+    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * (half ? 2 : 4)));
     t.n = batch_;
     t.c = c;
     t.h = h;
     t.w = w;
     t.layout = layout;
+    t.half = half;
   }
   return t;
+}
+
+// act1 of ResBlock `layer` for `step`: computed by precompute, or derived here
+// from conv1.out + norm1 when the cache was uploaded from a CPU precompute.
+const DevTensor& Engine::ensure_act(int step, const std::string& key, int layer, cudaStream_t st) {
+  auto it = cache_.find({step, key + ".act1"});
+  if (it != cache_.end()) return it->second;
+  const LayerDev& L = layers_[layer];
+  const DevTensor& m1 = cache_tensor(step, key + ".conv1.out");
+  const DevNorm& f = cache_norm(step, key + ".norm1");
+  Src s = plain(m1);
+  epi_push_ss(s.epi, f.scale, f.shift, f.np, m1.c);
+  epi_push_act(s.epi, L.act);
+  DevTensor& a = cache_slot(step, key + ".act1", m1.c, m1.h, m1.w, kNHWC, act_half());
+  launch_materialize_act(s, a.p, a.half, st);
+  SIGE_CUDA(cudaStreamSynchronize(st));
+  return a;
 }
 
 DevNorm& Engine::norm_slot(int step, const std::string& key, int np) {
@@ -217,15 +247,16 @@ DevNorm& Engine::norm_slot(int step, const std::string& key, int np) {
   return n;
 }
 
-DevTensor& Engine::scratch(const std::string& key, int c, int h, int w, int layout) {
+DevTensor& Engine::scratch(const std::string& key, int c, int h, int w, int layout, int half) {
   DevTensor& t = scratch_[key];
-  if (!t.p || t.c != c || t.h != h || t.w != w || t.layout != layout) {
-    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * sizeof(float)));
+  if (!t.p || t.c != c || t.h != h || t.w != w || t.layout != layout || t.half != half) {
+    t.p = static_cast<float*>(alloc(static_cast<size_t>(batch_) * c * h * w * (half ? 2 : 4)));
     t.n = batch_;
     t.c = c;
     t.h = h;
     t.w = w;
     t.layout = layout;
+    t.half = half;
   }
   return t;
 }
@@ -247,22 +278,33 @@ DevTensor& Engine::work_buffer(int step, const std::string& key) {
   if (it != work_.end()) return it->second;
   const DevTensor& src = cache_tensor(step, key);
   DevTensor w = src;
-  w.p = static_cast<float*>(alloc(src.numel() * sizeof(float)));
-  SIGE_CUDA(cudaMemcpy(w.p, src.p, src.numel() * sizeof(float), cudaMemcpyDeviceToDevice));
+  w.p = static_cast<float*>(alloc(src.bytes()));
+  SIGE_CUDA(cudaMemcpy(w.p, src.p, src.bytes(), cudaMemcpyDeviceToDevice));
   return work_[{step, key}] = w;
 }
 
 // All tiles of an (oh, ow) grid, 8x8, n-major: the dense path runs the same
 // fused kernels over every tile (equal to conv2d, test_kernels.cpp:288-351).
-Tiles Engine::dense_tiles(int oh, int ow) {
-  constexpr int kB = 8;
-  auto key = std::make_pair(oh, ow);
+// Tile shape for the dense path. CUDA-core kernel: 8x8. Tensor cores: the
+// widest tile (<= 16 columns) whose GEMM rows (bh-1)*P + bw fit one M=128 MMA.
+std::pair<int, int> Engine::dense_shape(int oh, int ow, int k, int s) const {
+  if (!tensor_cores()) return {8, 8};
+  const int bw = std::min(ow, 16);
+  const int P = s == 1 ? bw + k - 1 : bw + 1;
+  const int bh = std::max(1, std::min(oh, (128 - bw) / P + 1));
+  return {bh, bw};
+}
+
+Tiles Engine::dense_tiles(int oh, int ow, int k, int s) {
+  const auto shape = dense_shape(oh, ow, k, s);
+  const int bh = shape.first, bw = shape.second;
+  auto key = std::make_tuple(oh, ow, bh, bw);
   auto it = dense_tiles_.find(key);
   if (it == dense_tiles_.end()) {
     std::vector<int32_t> idx;
     for (int n = 0; n < batch_; ++n)
-      for (int r = 0; r < oh; r += kB)
-        for (int c = 0; c < ow; c += kB) {
+      for (int r = 0; r < oh; r += bh)
+        for (int c = 0; c < ow; c += bw) {
           idx.push_back(n);
           idx.push_back(r);
           idx.push_back(c);
@@ -275,7 +317,8 @@ Tiles Engine::dense_tiles(int oh, int ow) {
   t.idx = it->second.first;
   t.count = it->second.second;
   t.capacity = t.count;
-  t.bh = t.bw = kB;
+  t.bh = bh;
+  t.bw = bw;
   return t;
 }
 
@@ -293,8 +336,8 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     }
     SIGE_CUDA(cudaEventRecord(rec.a, st));
   }
-  if (math_ == SIGE_MATH_TF32)
-    launch_conv_tc(src, t, cw, dst, st);
+  if (tensor_cores())
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
   if (profiling_) {
@@ -304,7 +347,7 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     // algorithmic FLOPs per tile: 2 * C_out * C_in * k^2 * (pixels of the
     // tile inside the canvas ~ bh*bw; fringe clipping ignored)
     rec.flops_per_tile = 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * t.bh * t.bw;
-    rec.tc = math_ == SIGE_MATH_TF32;
+    rec.tc = tensor_cores() ? 1 : 0;
     prof_.push_back(rec);
   }
 }
@@ -335,8 +378,10 @@ int Engine::profile_read(double* rows, int cap, cudaStream_t st) {
 std::string Engine::cache_entries(int step) const {
   std::ostringstream o;
   for (auto& kv : cache_) {
-    if (kv.first.first != step || kv.first.second == "input") continue;
+    if (kv.first.first != step || kv.first.second == "input" || kv.second.half) continue;
     const DevTensor& t = kv.second;
+    if (kv.first.second.size() > 5 && kv.first.second.compare(kv.first.second.size() - 5, 5, ".act1") == 0)
+      continue;  // engine-internal activation buffer, not a reference cache entry
     o << "T " << kv.first.second << ' ' << t.n << ' ' << t.c << ' ' << t.h << ' ' << t.w << '\n';
   }
   for (auto& kv : norms_) {
@@ -351,14 +396,27 @@ void Engine::fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream
   if (L.norm_kind == SIGE_NORM_BATCH) {
     launch_bn_fold(L.channels, L.eps, L.gamma, L.beta, L.rmean, L.rvar, out.scale, out.shift, st);
   } else {
-    launch_gn_fold(x, L.groups, L.eps, L.gamma, L.beta, out.scale, out.shift, nullptr,
-                   math_ == SIGE_MATH_TF32 ? 0 : 1, st);
+    if (!gn_scratch_) gn_scratch_ = static_cast<double*>(alloc(kGnScratch * sizeof(double)));
+    launch_gn_fold(x, L.groups, L.eps, L.gamma, L.beta, out.scale, out.shift, gn_scratch_, kGnScratch,
+                   tensor_cores() ? 0 : 1, st);
+  }
+}
+
+// Derived activation buffers go stale when their inputs are replaced.
+void Engine::drop_act(int step) {
+  for (auto it = cache_.begin(); it != cache_.end();) {
+    const std::string& k = it->first.second;
+    if (it->first.first == step && k.size() > 5 && k.compare(k.size() - 5, 5, ".act1") == 0)
+      it = cache_.erase(it);
+    else
+      ++it;
   }
 }
 
 void Engine::invalidate_programs() {
   // Working buffers mirror cache contents; any cache write drops them. The
   // memory stays in allocations_ until the engine dies (cache writes are rare).
+  SIGE_CUDA(cudaDeviceSynchronize());  // captured graphs may still be running
   work_.clear();
   programs_.clear();
   last_program_ = nullptr;
@@ -379,7 +437,7 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
       case SIGE_LAYER_DOWNSAMPLE: {
         DevTensor& o = capture ? cache_slot(step, key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC)
                                : scratch("dense." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
-        conv(x, dense_tiles(sh.h_out, sh.w_out), L.conv, to_dst(o), st);
+        conv(x, dense_tiles(sh.h_out, sh.w_out, L.conv.k, L.conv.stride), L.conv, to_dst(o), st);
         x = plain(o);
         break;
       }
@@ -407,7 +465,7 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         const int c1 = L.conv.c_out, co = L.conv2.c_out, h = sh.h_in, w = sh.w_in;
         DevTensor& m1 = capture ? cache_slot(step, key + ".conv1.out", c1, h, w, kNHWC)
                                 : scratch("dense." + key + ".conv1.out", c1, h, w, kNHWC);
-        conv(x, dense_tiles(h, w), L.conv, to_dst(m1), st);
+        conv(x, dense_tiles(h, w, 3, 1), L.conv, to_dst(m1), st);
         const int np = L.norm_kind == SIGE_NORM_BATCH ? L.channels : batch_ * L.channels;
         DevNorm* f;
         if (reused) {
@@ -419,22 +477,28 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         Src mid = plain(m1);
         epi_push_ss(mid.epi, f->scale, f->shift, f->np, c1);
         epi_push_act(mid.epi, L.act);
+        if (use_act()) {  // conv2 stages act1 = act(norm1(m1)) evaluated once per pixel
+          DevTensor& a1 = capture ? cache_slot(step, key + ".act1", c1, h, w, kNHWC, act_half())
+                                  : scratch("dense." + key + ".act1", c1, h, w, kNHWC, act_half());
+          launch_materialize_act(mid, a1.p, a1.half, st);
+          mid = plain(a1);
+        }
         DevTensor& sc = capture ? cache_slot(step, key + ".shortcut.out", co, h, w, kNHWC)
                                 : scratch("dense." + key + ".shortcut.out", co, h, w, kNHWC);
         if (L.has_shortcut)
-          conv(x, dense_tiles(h, w), L.shortcut, to_dst(sc), st);
+          conv(x, dense_tiles(h, w, 1, 1), L.shortcut, to_dst(sc), st);
         else
           launch_materialize(x, sc.p, kNHWC, st);
         DevTensor& sum = capture ? cache_slot(step, key + ".sum", co, h, w, kNHWC)
                                  : scratch("dense." + key + ".sum", co, h, w, kNHWC);
         if (capture) {
           DevTensor& m2 = cache_slot(step, key + ".conv2.out", co, h, w, kNHWC);
-          conv(mid, dense_tiles(h, w), L.conv2, to_dst(m2), st);
+          conv(mid, dense_tiles(h, w, 3, 1), L.conv2, to_dst(m2), st);
           launch_add(m2.p, sc.p, sum.p, sum.numel(), st);  // add(m, sc), graph.cpp:404
         } else {
           Dst d = to_dst(sum, kAddSrc);
           d.addend = plain(sc);
-          conv(mid, dense_tiles(h, w), L.conv2, d, st);
+          conv(mid, dense_tiles(h, w, 3, 1), L.conv2, d, st);
         }
         x = plain(sum);
         break;
@@ -503,6 +567,7 @@ void Engine::put_tensor(int step, const std::string& key, const float* host, siz
     throw ConfigError("cache entry " + key + ": expected " +
                       std::to_string(static_cast<size_t>(batch_) * c * h * w) + " values");
   invalidate_programs();
+  drop_act(step);
   const int layout = is_nchw_key(key) ? kNCHW : kNHWC;
   DevTensor& t = cache_slot(step, key, c, h, w, layout);
   std::vector<float> buf(numel);
@@ -521,6 +586,7 @@ void Engine::put_tensor(int step, const std::string& key, const float* host, siz
 
 void Engine::put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np) {
   invalidate_programs();
+  drop_act(step);
   DevNorm& n = norm_slot(step, key, static_cast<int>(np));
   SIGE_CUDA(cudaMemcpy(n.scale, sc, np * sizeof(float), cudaMemcpyHostToDevice));
   SIGE_CUDA(cudaMemcpy(n.shift, sh, np * sizeof(float), cudaMemcpyHostToDevice));
@@ -537,6 +603,7 @@ void Engine::get_norm(int step, const std::string& key, float* sc, float* sh, si
 void Engine::get_tensor(int step, const std::string& key, float* host, size_t numel) {
   const DevTensor& t = cache_tensor(step, key);
   if (numel != t.numel()) throw ConfigError("cache entry " + key + ": size mismatch");
+  if (t.half) throw ConfigError("cache entry " + key + ": fp16 activation buffer (engine-internal)");
   std::vector<float> buf(numel);
   SIGE_CUDA(cudaDeviceSynchronize());
   SIGE_CUDA(cudaMemcpy(buf.data(), t.p, numel * sizeof(float), cudaMemcpyDeviceToHost));
@@ -617,6 +684,7 @@ struct ProgramBuilder {
     j.w = wbuf.w;
     j.b = e.b;
     j.layout = wbuf.layout;
+    j.half = wbuf.half;
     P.restores.push_back(j);
     P.restore_max = std::max<long long>(P.restore_max, static_cast<long long>(e.capacity) * e.b * e.b * wbuf.c);
   }
@@ -665,7 +733,7 @@ struct ProgramBuilder {
           Src s = flow;
           if (!runs_sparse(L, flow.h, flow.w, cfg)) {
             DevTensor& o = E.scratch("sparse." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
-            Tiles t = E.dense_tiles(sh.h_out, sh.w_out);
+            Tiles t = E.dense_tiles(sh.h_out, sh.w_out, cw.k, cw.stride);
             Dst d = to_dst(o);
             add([eng, s, t, cw, d, fin, bind](cudaStream_t st) { eng->conv(bind(s, fin), t, cw, d, st); });
             flow = plain(o);
@@ -729,7 +797,7 @@ struct ProgramBuilder {
             DevTensor& o = E.scratch("sparse." + key + ".sum", co, h, w, kNHWC);
             const int np = L.norm_kind == SIGE_NORM_BATCH ? L.channels : N * L.channels;
             DevNorm& f = E.scratch_norm("sparse." + key + ".norm1", np);
-            Tiles t = E.dense_tiles(h, w);
+            Tiles t = E.dense_tiles(h, w, 3, 1), t1 = E.dense_tiles(h, w, 1, 1);
             ConvW c1w = L.conv, c2w = L.conv2, scw = L.shortcut;
             LayerDev Lc = L;
             DevTensor m1c = m1;
@@ -737,18 +805,24 @@ struct ProgramBuilder {
             Src mid = plain(m1);
             epi_push_ss(mid.epi, f.scale, f.shift, np, c1);
             epi_push_act(mid.epi, L.act);
+            DevTensor a1c{};
+            if (E.use_act()) a1c = E.scratch("sparse." + key + ".act1", c1, h, w, kNHWC, E.act_half());
             Dst d = to_dst(o, kAddSrc);
             DevTensor* scd = nullptr;
             if (L.has_shortcut) scd = &E.scratch("sparse." + key + ".shortcut", co, h, w, kNHWC);
             DevTensor scc = scd ? *scd : DevTensor{};
             const bool has_sc = L.has_shortcut != 0;
-            add([eng, x0, t, c1w, c2w, scw, Lc, m1c, fc, mid, d, scc, has_sc, fin, bind](cudaStream_t st) mutable {
+            add([eng, x0, t, t1, c1w, c2w, scw, Lc, m1c, fc, mid, a1c, d, scc, has_sc, fin, bind](cudaStream_t st) mutable {
               Src xin = bind(x0, fin);
               eng->conv(xin, t, c1w, to_dst(m1c), st);
               eng->fold_norm(Lc, plain(m1c), fc, st);
+              if (a1c.p) {  // act1 once per pixel, conv2 stages plain copies
+                launch_materialize_act(mid, a1c.p, a1c.half, st);
+                mid = plain(a1c);
+              }
               Dst dd = d;
               if (has_sc) {
-                eng->conv(xin, t, scw, to_dst(scc), st);
+                eng->conv(xin, t1, scw, to_dst(scc), st);
                 dd.addend = plain(scc);
               } else {
                 dd.addend = xin;
@@ -770,11 +844,28 @@ struct ProgramBuilder {
             ConvW c1w = L.conv, c2w = L.conv2, scw = L.shortcut;
             // 1. conv1 over main tiles -> W(conv1.out)
             Dst d1 = to_dst(w1);
-            add([eng, x0, tm, c1w, d1, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), tm, c1w, d1, st); });
-            restore(w1, c1c, em);
             // 2. conv2 on scatter_gather(m1) with norm1 + act (graph.cpp:821-846)
             Src mid = plain(w1);
-            if (L.norm_kind == SIGE_NORM_BATCH || cfg.norm_precompute) {
+            const bool reuse = L.norm_kind == SIGE_NORM_BATCH || cfg.norm_precompute;
+            if (reuse && E.use_act()) {
+              // conv1's epilogue also writes act1 = act(norm1(value)) for its
+              // tiles into W(act1); conv2 stages plain copies of W(act1).
+              const DevNorm& f = E.cache_norm(step, key + ".norm1");
+              const DevTensor& ca = E.ensure_act(step, key, static_cast<int>(i), nullptr);
+              DevTensor& wa = E.work_buffer(step, key + ".act1");
+              d1.act = wa.p;
+              d1.act_half = wa.half;
+              d1.act_epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+              epi_push_ss(d1.act_epi, f.scale, f.shift, f.np, c1);
+              epi_push_act(d1.act_epi, L.act);
+              restore(wa, ca, em);
+              mid = plain(wa);
+            }
+            add([eng, x0, tm, c1w, d1, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), tm, c1w, d1, st); });
+            restore(w1, c1c, em);
+            if (reuse && E.use_act()) {
+              // mid already reads W(act1)
+            } else if (reuse) {
               const DevNorm& f = E.cache_norm(step, key + ".norm1");
               epi_push_ss(mid.epi, f.scale, f.shift, f.np, c1);
             } else {
@@ -786,7 +877,7 @@ struct ProgramBuilder {
               add([eng, Lc, fc, w1s](cudaStream_t st) mutable { eng->fold_norm(Lc, w1s, fc, st); });
               epi_push_ss(mid.epi, f.scale, f.shift, np, c1);
             }
-            epi_push_act(mid.epi, L.act);
+            if (!(reuse && E.use_act())) epi_push_act(mid.epi, L.act);
             Dst d2 = to_dst(ws, kResMain);
             d2.aux = osc.p;
             conv_step(mid, tm, c2w, d2);
@@ -877,14 +968,51 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
     return;
   }
   Program& P = program(cfg);
-  // Lazy restore of the tiles the previous call dirtied.
-  if (last_program_ && !last_program_->restores.empty())
-    launch_restore(last_program_->restores_dev, static_cast<int>(last_program_->restores.size()),
-                   static_cast<int>(std::min<long long>(last_program_->restore_max, 1LL << 30)), st);
   cur_in_ = edited;
   cur_out_ = out;
-  // Mask -> bits (compute_difference_mask against the cached original input
-  // when no mask is given), then the IndexPlan.
+  last_program_ = &P;
+  // Replay: after one direct run the whole call (mask, plan, every fused conv,
+  // final copy, restore) is captured once per (input, mask, output) binding
+  // into a CUDA graph on an internal stream and replayed with one launch.
+  if (use_graphs_ && !profiling_ && P.ran) {
+    auto key = std::make_tuple(static_cast<const void*>(edited), static_cast<const void*>(mask),
+                               static_cast<const void*>(out));
+    auto it = P.graphs.find(key);
+    if (it == P.graphs.end()) {
+      if (!cap_stream_) SIGE_CUDA(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking));
+      cudaGraph_t g = nullptr;
+      const uint64_t b0 = g_launches.load();
+      SIGE_CUDA(cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeThreadLocal));
+      try {
+        run_program(P, edited, mask, cfg, cap_stream_);
+      } catch (...) {
+        cudaStreamEndCapture(cap_stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      SIGE_CUDA(cudaStreamEndCapture(cap_stream_, &g));
+      const int kernels = static_cast<int>(g_launches.load() - b0);
+      g_launches.fetch_sub(static_cast<uint64_t>(kernels));  // counted when the graph runs
+      cudaGraphExec_t ex = nullptr;
+      SIGE_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      it = P.graphs.emplace(key, std::make_pair(ex, kernels)).first;
+    }
+    SIGE_CUDA(cudaGraphLaunch(it->second.first, st));
+    g_launches.fetch_add(static_cast<uint64_t>(it->second.second));
+    last_launches_ = it->second.second;
+    return;
+  }
+  run_program(P, edited, mask, cfg, st);
+  P.ran = true;
+  last_launches_ = static_cast<int>(g_launches.load() - before);
+}
+
+// One sparse_forward call on `st`: mask -> bits (compute_difference_mask
+// against the cached original input when no mask is given), the IndexPlan,
+// every compiled step, then the restore of the tiles this call dirtied.
+void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
+                         const sige_run_config& cfg, cudaStream_t st) {
   SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
   if (mask) {
     launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st);
@@ -896,9 +1024,12 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
   launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
               static_cast<int>(P.entries.size()), st);
   for (auto& f : P.steps) f(st);
-  last_program_ = &P;
-  last_launches_ = static_cast<int>(g_launches.load() - before);
+  if (!P.restores.empty())
+    launch_restore(P.restores_dev, static_cast<int>(P.restores.size()),
+                   static_cast<int>(std::min<long long>(P.restore_max, 1LL << 30)), st);
 }
+
+void Engine::set_graphs(bool on) { use_graphs_ = on; }
 
 int Engine::trace(uint64_t* rows, int cap, cudaStream_t st) {
   if (!last_program_) return 0;

@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -29,10 +30,12 @@
 namespace sige_b200 {
 
 struct DevTensor {
-  float* p = nullptr;
+  float* p = nullptr;  // fp32 storage, or fp16 when `half` (activation buffers)
   int n = 0, c = 0, h = 0, w = 0;
   int layout = kNHWC;
+  int half = 0;
   size_t numel() const { return static_cast<size_t>(n) * c * h * w; }
+  size_t bytes() const { return numel() * (half ? 2 : 4); }
 };
 
 struct DevNorm {
@@ -77,6 +80,7 @@ class Engine {
   int trace(uint64_t* rows, int cap, cudaStream_t st);
   size_t cache_bytes() const;
   void set_profiling(bool on);
+  void set_graphs(bool on);
   int profile_read(double* rows, int cap, cudaStream_t st);
   std::string cache_entries(int step) const;
   int in_channels() const { return in_c_; }
@@ -90,16 +94,30 @@ class Engine {
   void conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& dst, cudaStream_t st) const;
   const DevTensor& cache_tensor(int step, const std::string& key) const;
   const DevNorm& cache_norm(int step, const std::string& key) const;
-  DevTensor& cache_slot(int step, const std::string& key, int c, int h, int w, int layout);
+  DevTensor& cache_slot(int step, const std::string& key, int c, int h, int w, int layout, int half = 0);
   DevNorm& norm_slot(int step, const std::string& key, int np);
   DevTensor& work_buffer(int step, const std::string& key);
-  DevTensor& scratch(const std::string& key, int c, int h, int w, int layout);
+  DevTensor& scratch(const std::string& key, int c, int h, int w, int layout, int half = 0);
+  // Activation buffers (tensor-core modes): conv2 of a ResBlock stages
+  // act1 = act(norm1(conv1.out)) instead of re-applying the chain.
+  bool use_act() const { return tensor_cores(); }
+  int act_half() const { return math_ == SIGE_MATH_F16 ? 1 : 0; }
+  const DevTensor& ensure_act(int step, const std::string& key, int layer, cudaStream_t st);
   DevNorm& scratch_norm(const std::string& key, int np);
-  Tiles dense_tiles(int oh, int ow);
+  Tiles dense_tiles(int oh, int ow, int k, int s);
+  std::pair<int, int> dense_shape(int oh, int ow, int k, int s) const;
+  bool tensor_cores() const { return math_ == SIGE_MATH_TF32 || math_ == SIGE_MATH_F16; }
+  static constexpr int kGnScratch = 1 << 16;
+  double* gn_scratch_ = nullptr;
   void invalidate_programs();
+  void drop_act(int step);
   void dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
                   cudaStream_t st);
   Program& program(const sige_run_config& cfg);
+  void run_program(Program& P, const float* edited, const uint8_t* mask, const sige_run_config& cfg,
+                   cudaStream_t st);
+  bool use_graphs_ = true;
+  cudaStream_t cap_stream_ = nullptr;
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
 
   std::string name_;
@@ -113,7 +131,7 @@ class Engine {
   std::map<std::pair<int, std::string>, DevTensor> work_;
   std::map<std::string, DevTensor> scratch_;
   std::map<std::string, DevNorm> scratch_norms_;
-  std::map<std::pair<int, int>, std::pair<int32_t*, int>> dense_tiles_;
+  std::map<std::tuple<int, int, int, int>, std::pair<int32_t*, int>> dense_tiles_;
   std::map<std::string, std::unique_ptr<Program>> programs_;
   Program* last_program_ = nullptr;
   int last_launches_ = 0;

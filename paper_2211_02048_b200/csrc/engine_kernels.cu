@@ -271,6 +271,62 @@ __global__ void k_gn_fast(Src x, int groups, float eps, const float* __restrict_
   }
 }
 
+// Multi-CTA statistics for the tensor-core mode: CTA (n, s) owns pixel range s
+// of sample n, one thread per channel (NHWC rows are read coalesced),
+// per-thread double sum / sum of squares in pixel order, then a fixed-order
+// reduction over the group's channels -> partial[(n*groups + g)*S + s].
+// Deterministic (fixed partition and order) but not the reference's rounding.
+__global__ void k_gn_partial(Src x, int groups, int S, double* __restrict__ part) {
+  const int n = blockIdx.x / S, s = blockIdx.x % S;
+  const long long hw = static_cast<long long>(x.h) * x.w;
+  const long long p0 = hw * s / S, p1 = hw * (s + 1) / S;
+  extern __shared__ double red[];  // [2][C]
+  for (int c = threadIdx.x; c < x.c; c += blockDim.x) {
+    double a = 0.0, q = 0.0;
+    for (long long p = p0; p < p1; ++p) {
+      const double v = static_cast<double>(src_val(x, n, c, static_cast<int>(p / x.w), static_cast<int>(p % x.w)));
+      a += v;
+      q += v * v;
+    }
+    red[c] = a;
+    red[x.c + c] = q;
+  }
+  __syncthreads();
+  const int cpg = x.c / groups;
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    double a = 0.0, q = 0.0;
+    for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
+      a += red[c];
+      q += red[x.c + c];
+    }
+    part[(2 * (static_cast<long long>(n) * groups + g)) * S + s] = a;
+    part[(2 * (static_cast<long long>(n) * groups + g) + 1) * S + s] = q;
+  }
+}
+
+__global__ void k_gn_final(int n_groups_total, int groups, int S, int C, long long count_per_group,
+                           float eps, const double* __restrict__ part, const float* __restrict__ gamma,
+                           const float* __restrict__ beta, float* __restrict__ scale, float* __restrict__ shift) {
+  const int cpg = C / groups;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_groups_total * cpg; q += gridDim.x * blockDim.x) {
+    const int ng = q / cpg, ci = q % cpg;
+    const int n = ng / groups, g = ng % groups;
+    double a = 0.0, sq = 0.0;
+    for (int s = 0; s < S; ++s) {
+      a += part[(2LL * ng) * S + s];
+      sq += part[(2LL * ng + 1) * S + s];
+    }
+    const double cnt = static_cast<double>(count_per_group);
+    const double mean = a / cnt;
+    double var = sq / cnt - mean * mean;
+    if (var < 0.0) var = 0.0;
+    const int c = g * cpg + ci;
+    const float sc = __fdiv_rn(gamma[c], __fsqrt_rn(__fadd_rn(static_cast<float>(var), eps)));
+    scale[n * C + c] = sc;
+    shift[n * C + c] = __fsub_rn(beta[c], __fmul_rn(static_cast<float>(mean), sc));
+  }
+}
+
 __global__ void k_bn_fold(int c, float eps, const float* gamma, const float* beta, const float* rm,
                           const float* rv, float* scale, float* shift) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
@@ -368,7 +424,28 @@ __global__ void k_restore(const RestoreJob* __restrict__ jobs, int max_tiles) {
     if (y >= j.h || x >= j.w) continue;
     const size_t off = j.layout == kNHWC ? ((static_cast<size_t>(n) * j.h + y) * j.w + x) * j.c + ch
                                          : ((static_cast<size_t>(n) * j.c + ch) * j.h + y) * j.w + x;
-    j.dst[off] = j.src[off];
+    if (j.half)
+      reinterpret_cast<__half*>(j.dst)[off] = reinterpret_cast<const __half*>(j.src)[off];
+    else
+      j.dst[off] = j.src[off];
+  }
+}
+
+__global__ void k_materialize_act(Src s, void* __restrict__ dst, int half) {
+  const long long total = static_cast<long long>(s.n) * s.c * s.h * s.w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int ch = static_cast<int>(q % s.c);
+    long long p = q / s.c;
+    const int x = static_cast<int>(p % s.w);
+    p /= s.w;
+    const int y = static_cast<int>(p % s.h);
+    const int n = static_cast<int>(p / s.h);
+    const float v = src_val(s, n, ch, y, x);
+    if (half)
+      static_cast<__half*>(dst)[q] = __float2half_rn(v);
+    else
+      static_cast<float*>(dst)[q] = v;
   }
 }
 
@@ -465,7 +542,8 @@ void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate
 }
 
 void launch_gn_fold(const Src& x, int groups, float eps, const float* gamma, const float* beta,
-                    float* scale, float* shift, double* /*scratch*/, int exact, cudaStream_t st) {
+                    float* scale, float* shift, double* scratch, int scratch_len, int exact,
+                    cudaStream_t st) {
   if (groups < 1 || x.c % groups != 0)
     throw ConfigError("compute_norm_stats: groups " + std::to_string(groups) +
                       " must divide channels " + std::to_string(x.c));
@@ -473,6 +551,18 @@ void launch_gn_fold(const Src& x, int groups, float eps, const float* gamma, con
     const int items = x.n * groups;
     k_gn_exact<<<(items + 31) / 32, 32, 0, st>>>(x, groups, eps, gamma, beta, scale, shift);
     after_launch("k_gn_exact");
+  } else if (scratch && x.c <= 1024 && 2LL * x.n * groups * 2 <= scratch_len) {
+    const long long hw = static_cast<long long>(x.h) * x.w;
+    int S = static_cast<int>(std::max(1LL, std::min<long long>(hw / 16, (2LL * sm_count()) / x.n)));
+    S = static_cast<int>(std::min<long long>(S, scratch_len / (2LL * x.n * groups)));
+    const int threads = std::min(1024, std::max(32, (x.c + 31) / 32 * 32));
+    k_gn_partial<<<x.n * S, threads, 2 * x.c * sizeof(double), st>>>(x, groups, S, scratch);
+    after_launch("k_gn_partial");
+    const int items = x.n * x.c;
+    k_gn_final<<<(items + 255) / 256, 256, 0, st>>>(x.n * groups, groups, S, x.c,
+                                                   static_cast<long long>(x.c / groups) * hw, eps, scratch,
+                                                   gamma, beta, scale, shift);
+    after_launch("k_gn_final");
   } else {
     k_gn_fast<<<x.n * groups, 512, 0, st>>>(x, groups, eps, gamma, beta, scale, shift);
     after_launch("k_gn_fast");
@@ -483,6 +573,12 @@ void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, con
                     const float* rvar, float* scale, float* shift, cudaStream_t st) {
   k_bn_fold<<<(c + 255) / 256, 256, 0, st>>>(c, eps, gamma, beta, rmean, rvar, scale, shift);
   after_launch("k_bn_fold");
+}
+
+void launch_materialize_act(const Src& src, void* dst, int half, cudaStream_t st) {
+  const long long total = static_cast<long long>(src.n) * src.c * src.h * src.w;
+  k_materialize_act<<<grid_cap(total, 256), 256, 0, st>>>(src, dst, half);
+  after_launch("k_materialize_act");
 }
 
 void launch_materialize(const Src& src, float* dst, int dst_layout, cudaStream_t st) {

@@ -6,6 +6,8 @@
 // NCHW, the reference layout (proj/include/sige/tensor.hpp:12-39).
 #pragma once
 
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,6 +26,7 @@ struct Src {
   int layout = kNHWC;
   int n = 1, c = 0, h = 0, w = 0;  // logical dims
   int up = 0;                       // log2 upsample factor
+  int half = 0;                     // storage is fp16 (activation buffers), else fp32
   DevEpilogue epi;
 };
 
@@ -34,6 +37,7 @@ __device__ __forceinline__ float src_raw(const Src& s, int n, int ch, int y, int
   int py = y >> s.up, px = x >> s.up;
   size_t off = s.layout == kNHWC ? ((static_cast<size_t>(n) * ph + py) * pw + px) * s.c + ch
                                  : ((static_cast<size_t>(n) * s.c + ch) * ph + py) * pw + px;
+  if (s.half) return __half2float(reinterpret_cast<const __half*>(s.ptr)[off]);
   return __ldg(s.ptr + off);
 }
 __device__ __forceinline__ float src_val(const Src& s, int n, int ch, int y, int x) {
@@ -55,6 +59,12 @@ struct Dst {
   int mode = kStore;
   const float* aux = nullptr;  // NHWC, same shape (original shortcut)
   Src addend;                  // kAddSrc
+  // Optional activation output: act[p] = act_epi(value written at p) — the
+  // consumer's pending GroupNorm scale-shift + activation evaluated once per
+  // output pixel (NHWC, same shape; fp16 when act_half).
+  void* act = nullptr;
+  int act_half = 0;
+  DevEpilogue act_epi;
 };
 
 // The tile list a conv runs over: `count` triplets {n, r, c} (output-res
@@ -68,13 +78,21 @@ struct Tiles {
   int bh = 0, bw = 0;  // tile shape at output resolution (square for sparse)
 };
 
+// TMA descriptors of a packed weight tensor, one per N-slice width
+// (16, 32, 64, 128) with the taps batched per ring stage.
+struct TcMaps {
+  CUtensorMap m[4];
+  int tps[4];
+};
+
 struct ConvW {
   int c_in = 0, c_out = 0, k = 1, stride = 1;
   const float* w = nullptr;     // (c_out, c_in, k, k) reference layout
   const float* bias = nullptr;  // c_out or nullptr
-  const float* w_tc = nullptr;  // tcgen05 K-major packing (conv_tc.cu), may be nullptr
+  const void* w_tc = nullptr;   // tcgen05 packing [chunk][tap][group][n_pad][16 B] (conv_tc.cu)
   int n_pad = 0;                // c_out rounded up for the tensor-core N dimension
   int k_pad = 0;                // channels rounded up per tap for the K dimension
+  TcMaps maps{};
 };
 
 // Fused gather -> conv -> scatter over tiles (exact fp32 CUDA-core path:
@@ -83,11 +101,12 @@ void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, cons
                        int math, cudaStream_t st);
 // Same contract on tcgen05 tensor cores (kind::tf32, fp32 TMEM accumulators).
 // conv_tc.cu.
-void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst,
+void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
                     cudaStream_t st);
-// Packs reference-layout weights for launch_conv_tc; returns device buffer.
-float* pack_weights_tc(const float* w_dev_ref, int c_out, int c_in, int k, int* n_pad, int* k_pad,
-                       cudaStream_t st);
+// Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
+// k_pad and the TMA descriptors of `cw`).
+void pack_weights_tc(const float* w_dev_ref, int c_out, int c_in, int k, int f16, ConvW* cw,
+                     cudaStream_t st);
 
 // On-device IndexPlan (graph.cpp:506-528): for every entry e, tile (r, c) of
 // an (h_e, w_e, b_e) grid is active iff the full-resolution difference mask
@@ -112,7 +131,8 @@ void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate
 // writing scale/shift (n*C). exact=1 follows the reference's sequential
 // double accumulation order (bit-exact); 0 uses a parallel tree.
 void launch_gn_fold(const Src& x, int groups, float eps, const float* gamma, const float* beta,
-                    float* scale, float* shift, double* scratch, int exact, cudaStream_t st);
+                    float* scale, float* shift, double* scratch, int scratch_len, int exact,
+                    cudaStream_t st);
 // Batch-kind fold of running statistics (graph.cpp:313-320).
 void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, const float* rmean,
                     const float* rvar, float* scale, float* shift, cudaStream_t st);
@@ -133,7 +153,12 @@ struct RestoreJob {
   const int32_t* idx;
   const int32_t* count;
   int n, c, h, w, b, layout;
+  int half;  // 2-byte elements (fp16 activation buffers)
 };
+// dst (NHWC, fp16 when half else fp32) = value of `src` (pending chain applied)
+// at every pixel: the activation buffer a conv consumes instead of re-applying
+// GroupNorm scale-shift + SiLU per staged window element.
+void launch_materialize_act(const Src& src, void* dst, int half, cudaStream_t st);
 void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_tiles, cudaStream_t st);
 // out (NCHW, full) = *any ? value of `result` : cached_final — the empty-mask
 // short-circuit of sparse_forward (graph.cpp:665-668) folded into the final copy.

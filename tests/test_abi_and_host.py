@@ -32,7 +32,7 @@ def test_library_has_sm100a_code():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_capi.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(_capi.LIB_PATH)], capture_output=True, text=True).stdout
-    for mnemonic in ("UTCHMMA", "LDTM", "UBLKCP"):  # tcgen05.mma / tcgen05.ld / bulk copy
+    for mnemonic in ("UTCHMMA", "LDTM", "UTMALDG"):  # tcgen05.mma / tcgen05.ld / TMA load
         assert mnemonic in sass, mnemonic
 
 

@@ -124,3 +124,27 @@ def test_errors_like_reference(orc):
         eng.sparse_forward(x)
     with pytest.raises(sb.ConfigError, match="config: block sizes must be >= 1"):
         eng.sparse_forward(x, config=sb.default_config(block3=0))
+
+
+@pytest.mark.parametrize("math", [sb.MATH_EXACT, sb.MATH_F16])
+def test_graph_replay_identical(orc, math):
+    """CUDA-graph replay (default after the first call) gives the same bits as
+    direct launches, across repeated calls and a switch of edited input."""
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 31)
+    _, edited2 = orc.make_edit_fixture("blob5", 1, 3, 64, 64, 31)
+    cfg = sb.default_config(dilate_full=25)
+    outs = {}
+    for graphs in (False, True):
+        eng = sb.Engine(sb.Model("mini_unet_gn"), math=math)
+        eng.set_graphs(graphs)
+        eng.precompute(torch.from_numpy(orig).cuda())
+        e1, e2 = torch.from_numpy(edited).cuda(), torch.from_numpy(edited2).cuda()
+        out = torch.empty(eng.output_shape(), device="cuda")
+        res = []
+        for x in (e1, e1, e1, e2, e1):
+            eng.sparse_forward(x, config=cfg, out=out)
+            res.append(out.cpu().numpy().copy())
+        outs[graphs] = res
+    for a, b in zip(outs[False], outs[True]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(outs[True][0], outs[True][4])

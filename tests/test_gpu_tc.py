@@ -79,7 +79,8 @@ GEOMS = [  # n, c_in, c_out, k, s, h, w, block
 
 
 @pytest.mark.parametrize("g", GEOMS, ids=[f"n{g[0]}c{g[1]}-{g[2]}k{g[3]}s{g[4]}_{g[5]}x{g[6]}b{g[7]}" for g in GEOMS])
-def test_tc_conv_integer_bit_exact(orc, g):
+@pytest.mark.parametrize("math", [sb.MATH_TF32, sb.MATH_F16], ids=["tf32", "f16"])
+def test_tc_conv_integer_bit_exact(orc, g, math):
     n, c_in, c_out, k, s, h, w, b = g
     rng = np.random.default_rng(hash(g) % 2**32)
     orig, edited, wt, bias = int_case(rng, n, c_in, c_out, k, s, h, w)
@@ -91,7 +92,7 @@ def test_tc_conv_integer_bit_exact(orc, g):
     ocache = om.precompute(orig)
     want, _ = om.sparse_forward(ocache, edited, mask, cfg)
     for precompute_on_device in (False, True):
-        eng = sb.Engine(model, batch=n, math=sb.MATH_TF32)
+        eng = sb.Engine(model, batch=n, math=math)
         if precompute_on_device:
             eng.precompute(torch.from_numpy(orig).cuda())
             # the dense pass also runs on tensor cores: integer data keeps it exact
@@ -123,7 +124,8 @@ CASES = [
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-n{c[2]}" for c in CASES])
-def test_tc_engine_tolerance(orc, case):
+@pytest.mark.parametrize("math", [sb.MATH_TF32, sb.MATH_F16], ids=["tf32", "f16"])
+def test_tc_engine_tolerance(orc, case, math):
     name, fx, n, seed, over = case
     om = orc.model(name)
     c, h, w = sb.Model(name).in_shape
@@ -134,7 +136,7 @@ def test_tc_engine_tolerance(orc, case):
     cfg = sb.default_config(dilate_full=om.required_dilation() if df is None else df, **over)
     ocache = om.precompute(orig)
     want, _ = om.sparse_forward(ocache, edited, mask, cfg)
-    eng = sb.Engine(sb.Model(name), batch=n, math=sb.MATH_TF32)
+    eng = sb.Engine(sb.Model(name), batch=n, math=math)
     # cache from the CPU precompute isolates the sparse path's own error
     for kind, key, numel in ocache.entries():
         if kind == 0:
@@ -161,20 +163,21 @@ def test_tc_engine_tolerance(orc, case):
         outside = np.broadcast_to(cov[None, None] == 0, fin.shape)
         assert outside.any() and np.array_equal(got[outside], fin[outside])
     # and with the device precompute
-    eng2 = sb.Engine(sb.Model(name), batch=n, math=sb.MATH_TF32)
+    eng2 = sb.Engine(sb.Model(name), batch=n, math=math)
     eng2.precompute(torch.from_numpy(orig).cuda())
     got2 = eng2.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
     assert norm_err(got2, want) <= 1e-2
 
 
-def test_tc_config1_full_size(orc):
+@pytest.mark.parametrize("math", [sb.MATH_TF32, sb.MATH_F16], ids=["tf32", "f16"])
+def test_tc_config1_full_size(orc, math):
     om = orc.model("single_conv64")
     orig, edited = orc.make_edit_fixture("rect1", 1, 64, 256, 256, 7)
     mask = orc.difference_mask(orig, edited)
     cfg = sb.default_config(dilate_full=1)
     ocache = om.precompute(orig)
     want, _ = om.sparse_forward(ocache, edited, mask, cfg)
-    eng = sb.Engine(sb.Model("single_conv64"), math=sb.MATH_TF32)
+    eng = sb.Engine(sb.Model("single_conv64"), math=math)
     eng.precompute(torch.from_numpy(orig).cuda())
     got = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
     assert norm_err(got, want) <= 1e-2
