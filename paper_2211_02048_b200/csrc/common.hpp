@@ -65,6 +65,10 @@ int sm_count();
 struct DevEpilogue {
   int num_steps = 0;
   int fma_expf = 1;  // glibc expf variant to reproduce
+  // 1: SiLU as x / (1 + __expf(-x)) with the fast divide (tensor-core modes,
+  // whose operands are rounded to 10-bit mantissas anyway); 0: bit-exact
+  // glibc expf + IEEE divide (the reference's arithmetic, exact mode).
+  int fast = 0;
   int kind[SIGE_MAX_EPI_STEPS] = {};
   int act[SIGE_MAX_EPI_STEPS] = {};
   int per_sample[SIGE_MAX_EPI_STEPS] = {};  // 1 if params are N*C (sample-major)
@@ -78,8 +82,9 @@ DevEpilogue make_dev_epilogue(const sige_epilogue* e, int channels, int batch);
 
 #ifdef __CUDACC__
 // Reference activation arithmetic (eltwise.cpp:23-36), no FMA contraction.
-__device__ __forceinline__ float dev_act(float v, int kind, int fma_expf) {
+__device__ __forceinline__ float dev_act(float v, int kind, int fma_expf, int fast = 0) {
   if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;  // NaN -> 0, -0 -> +0
+  if (kind == SIGE_ACT_SILU && fast) return __fdividef(v, 1.0f + __expf(-v));
   if (kind == SIGE_ACT_SILU) {
     float e = glibc_expf(-v, fma_expf != 0);
     return __fdiv_rn(v, __fadd_rn(1.0f, e));
@@ -95,13 +100,50 @@ __device__ __forceinline__ float dev_epi(const DevEpilogue& e, float v, int ch, 
   for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
     if (s >= e.num_steps) break;
     if (e.kind[s] == SIGE_EPI_ACTIVATION) {
-      v = dev_act(v, e.act[s], e.fma_expf);
+      v = dev_act(v, e.act[s], e.fma_expf, e.fast);
     } else {
       int off = e.per_sample[s] ? n * channels + ch : ch;
       v = __fadd_rn(__fmul_rn(__ldg(e.scale[s] + off), v), __ldg(e.shift[s] + off));
     }
   }
   return v;
+}
+
+// The chain over CNT consecutive channels ch0.. of one pixel, same arithmetic
+// as dev_epi per value; the per-channel params of each step are fetched with
+// 16-byte loads up front (one memory round trip per step instead of one per
+// value) when the offsets are 4-aligned.
+template <int CNT>
+__device__ __forceinline__ void dev_epi_vec(const DevEpilogue& e, float* v, int ch0, int channels, int n) {
+  static_assert(CNT % 4 == 0, "CNT must be a multiple of 4");
+#pragma unroll
+  for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
+    if (s >= e.num_steps) break;
+    if (e.kind[s] == SIGE_EPI_ACTIVATION) {
+#pragma unroll
+      for (int j = 0; j < CNT; ++j) v[j] = dev_act(v[j], e.act[s], e.fma_expf, e.fast);
+    } else {
+      const int off = e.per_sample[s] ? n * channels + ch0 : ch0;
+      float sc[CNT], sh[CNT];
+      if ((off & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < CNT; j += 4) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(e.scale[s] + off + j));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(e.shift[s] + off + j));
+          sc[j] = a.x, sc[j + 1] = a.y, sc[j + 2] = a.z, sc[j + 3] = a.w;
+          sh[j] = b.x, sh[j + 1] = b.y, sh[j + 2] = b.z, sh[j + 3] = b.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CNT; ++j) {
+          sc[j] = __ldg(e.scale[s] + off + j);
+          sh[j] = __ldg(e.shift[s] + off + j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CNT; ++j) v[j] = __fadd_rn(__fmul_rn(sc[j], v[j]), sh[j]);
+    }
+  }
 }
 #endif
 

@@ -25,21 +25,29 @@
 // act = chain(out) once per output pixel (Dst::act, fp16), and the consumer
 // stages plain copies of it.
 //
+// A operand: when the source already holds the MMA operand type (fp32 for
+// kind::tf32, fp16 for kind::f16), channels-last with no pending chain, every
+// 16-byte unit is one cp.async straight into the canonical layout (zero fill
+// by src-size 0) and the stage's mbarrier fires when the copies land
+// (cp.async.mbarrier.arrive), so the producers keep up to 4 K chunks in flight.
+// Other sources are staged synchronously (load, chain, convert, st.shared).
+//
 // Weights are packed [chunk][tap][group][n_pad][16 B] and streamed by TMA
 // (cp.async.bulk.tensor.3d, one copy per ring stage covering 1, 3 or 9 taps
-// of an N slice) through a 4-stage mbarrier ring. The N slice (16..128) is
-// chosen on the device from the live tile count so even a layer with a
-// handful of tiles fills the SMs. The epilogue reads TMEM with tcgen05.ld,
-// adds the bias and writes the conv output / residual join straight into the
-// destination with 16-byte stores (scatter fused, kernels.cpp:88-132, 291-337).
+// of an N slice) through an up-to-8-stage mbarrier ring. The N slice (16..128)
+// is chosen on the device from the live tile count so even a layer with a
+// handful of tiles fills the SMs. Two TMEM accumulators: the epilogue of item
+// i (tcgen05.ld, bias, conv output / residual join written straight into the
+// destination, scatter fused, kernels.cpp:88-132, 291-337) overlaps the MMAs
+// of item i+1.
 //
 // Launch: programmatic dependent launch — setup, TMEM allocation and the first
 // weight stages overlap the previous layer's tail (griddepcontrol.wait guards
 // every access to data the previous kernel produced).
 //
-// Warp roles (320 threads): warps 0-7 stage A and run the epilogue (warp w
-// reads TMEM lanes 32*(w%4), column half w/4); warp 8 allocates TMEM and
-// issues tcgen05.mma (one thread); warp 9 issues the weight TMA (one thread).
+// Warp roles (320 threads): warps 0-3 produce A, warps 4-7 run the epilogue
+// (warp w reads TMEM lanes 32*(w%4)), warp 8 allocates TMEM and issues
+// tcgen05.mma (one thread), warp 9 issues the weight TMA (one thread).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -58,11 +66,14 @@ namespace sige_b200 {
 
 namespace {
 
-constexpr int kMaxNB = 4;      // B (weight) ring stages (max)
-constexpr int kStageThreads = 256;
-constexpr int kThreads = kStageThreads + 64;
-constexpr int kMaxNTile = 128;  // TMEM columns allocated (fp32 accumulators)
-constexpr int kBatch = 8;       // 16-byte groups staged per thread per batch
+constexpr int kProdThreads = 128;  // warps 0-3: A producers
+constexpr int kEpiThreads = 128;   // warps 4-7: epilogue (TMEM lane quarter = warp % 4)
+constexpr int kThreads = kProdThreads + kEpiThreads + 64;  // + warp 8 (MMA), warp 9 (weight TMA)
+constexpr int kMaxNA = 4;          // A ring stages (max)
+constexpr int kMaxNB = 8;          // B (weight) ring stages (max)
+constexpr int kMaxNTile = 256;     // accumulator columns per TMEM buffer
+constexpr int kTmemCols = 2 * kMaxNTile;  // two accumulators: epilogue of item i overlaps MMA of item i+1
+constexpr int kBatch = 4;          // 16-byte groups staged per thread per batch (synchronous path)
 
 struct TcParams {
   Src src;
@@ -73,11 +84,13 @@ struct TcParams {
   int n_pad, nchunks, ntaps, phases;
   int P, Mt, T, win_h, win_w;
   int min_items;  // target number of work items (SM count)
-  int nb;         // ring stages in use
+  int na, nb;     // A / B ring stages in use
+  int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
   uint32_t lbo_a, idesc_base;
   int a_bytes, b_stage_bytes;
-  int tps[4];     // taps per weight stage for n_tile = 16, 32, 64, 128
+  int tps[5];     // taps per weight stage for n_tile = 16, 32, 64, 128, 256
   unsigned long long* tl;  // debug timeline (SIGE_TC_TIMELINE), nullptr normally
+  int dbg;                 // SIGE_TC_DEBUG bits (experiments only)
 };
 
 // ------------------------------------------------------------- PTX ------
@@ -85,7 +98,7 @@ __device__ __forceinline__ void tl_mark(const TcParams& p, int idx) {
   if (p.tl && blockIdx.x < 8) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.tl[blockIdx.x * 32 + idx] = t;
+    p.tl[blockIdx.x * 64 + idx] = t;
   }
 }
 __device__ __forceinline__ void tl_cta(const TcParams& p, int base) {
@@ -127,6 +140,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// 16-byte global -> shared copy; src_bytes = 0 zero-fills (gather's zero fill
+// of out-of-canvas window cells, kernels.cpp:60,72-75).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// The mbarrier receives one arrival when all prior cp.async of this thread landed.
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
                                        uint64_t* bar) {
   asm volatile(
@@ -147,6 +174,14 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// One lane of a converged warp (tcgen05.mma / commit are single-thread
+// instructions; the warp computes the descriptors uniformly).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .b32 r;\n .reg .pred p;\n elect.sync r|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(pred));
+  return pred != 0;
+}
 
 // UMMA shared-memory descriptor, SWIZZLE_NONE K-major (version 1 for sm_100):
 // start >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46), version bit 46.
@@ -179,15 +214,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                 "=r"(r[7])
-               : "r"(taddr));
+// 16 consecutive accumulator columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -199,6 +236,65 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ----------------------------------------------------- element-wise chain --
+// Chains evaluated inside this kernel (pending GroupNorm scale-shift + act on
+// staged values, act buffers written by the epilogue) run in the tensor-core
+// modes only, whose operands carry 10-bit mantissas: SiLU uses __expf and the
+// fast divide. Compile-time fast keeps the glibc-expf + IEEE-divide body (the
+// exact mode's arithmetic) out of this kernel — with it every inlined chain
+// multiplied the kernel to >1 MB of SASS and the warp roles thrashed the
+// instruction cache (an epilogue with a chain ran 5x slower than without).
+__device__ __forceinline__ float tc_act(float v, int kind) {
+  if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;
+  if (kind == SIGE_ACT_SILU) return __fdividef(v, 1.0f + __expf(-v));
+  return v;
+}
+
+__device__ __forceinline__ float tc_epi(const DevEpilogue& e, float v, int ch, int channels, int n) {
+#pragma unroll
+  for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
+    if (s >= e.num_steps) break;
+    if (e.kind[s] == SIGE_EPI_ACTIVATION) {
+      v = tc_act(v, e.act[s]);
+    } else {
+      const int off = e.per_sample[s] ? n * channels + ch : ch;
+      v = __fadd_rn(__fmul_rn(__ldg(e.scale[s] + off), v), __ldg(e.shift[s] + off));
+    }
+  }
+  return v;
+}
+
+// CNT consecutive channels ch0.. of one pixel; params fetched as 16-byte loads.
+template <int CNT>
+__device__ __forceinline__ void tc_epi_vec(const DevEpilogue& e, float* v, int ch0, int channels, int n) {
+#pragma unroll 1
+  for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
+    if (s >= e.num_steps) break;
+    if (e.kind[s] == SIGE_EPI_ACTIVATION) {
+      const int k = e.act[s];
+#pragma unroll
+      for (int j = 0; j < CNT; ++j) v[j] = tc_act(v[j], k);
+    } else {
+      const int off = e.per_sample[s] ? n * channels + ch0 : ch0;
+      if ((off & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < CNT; j += 4) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(e.scale[s] + off + j));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(e.shift[s] + off + j));
+          v[j] = __fadd_rn(__fmul_rn(a.x, v[j]), b.x);
+          v[j + 1] = __fadd_rn(__fmul_rn(a.y, v[j + 1]), b.y);
+          v[j + 2] = __fadd_rn(__fmul_rn(a.z, v[j + 2]), b.z);
+          v[j + 3] = __fadd_rn(__fmul_rn(a.w, v[j + 3]), b.w);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CNT; ++j)
+          v[j] = __fadd_rn(__fmul_rn(__ldg(e.scale[s] + off + j), v[j]), __ldg(e.shift[s] + off + j));
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------- staging --
@@ -218,35 +314,111 @@ __device__ __forceinline__ int32_t row_info(const TcParams& p, int q) {
                               static_cast<uint32_t>(wx));
 }
 
-// The pending element-wise chain over one unit's values, out of line so the
-// glibc-expf body exists once in the kernel (instruction-cache footprint).
-__device__ __noinline__ void epi_unit(const DevEpilogue& e, float* f, int cnt, int cc, int c, int n) {
-  for (int i = 0; i < cnt; ++i) f[i] = dev_epi(e, f[i], cc + i, c, n);
+// Asynchronous staging of K chunk `ch` into A stage `abuf` (shared address):
+// every 16-byte unit is one cp.async straight from the source (fp32 for
+// kind::tf32, whose MMA reads the top 19 bits; fp16 for kind::f16); window
+// cells outside the canvas, empty tile slots and padding rows are zero-filled
+// by the copy itself. No registers, no conversion: kProdThreads threads keep
+// several chunks in flight.
+template <bool F16>
+__device__ __forceinline__ void stage_a_async(const TcParams& p, uint32_t abuf, int ch, const int32_t* row_tab,
+                                              const int4* s_tile) {
+  constexpr int kG = F16 ? 8 : 4;  // channels per 16-byte group
+  constexpr int kEsz = F16 ? 2 : 4;
+  const int units = p.phases * p.T * p.Mt * 8;
+  const Src& s = p.src;
+  const int ph_h = s.h >> s.up, ph_w = s.w >> s.up;
+  const char* base = reinterpret_cast<const char*>(s.ptr);
+  for (int u = threadIdx.x; u < units; u += kProdThreads) {
+    const int32_t info = row_tab[u >> 3];
+    const char* src = base;
+    uint32_t bytes = 0;
+    if (info < 0) {
+      const int4 tl = s_tile[(info >> 24) & 0x7f];
+      const int y = tl.y + ((info >> 12) & 0xfff), x = tl.z + (info & 0xfff);
+      const int cc = ch * (8 * kG) + (u & 7) * kG;
+      if (tl.x >= 0 && y >= 0 && y < s.h && x >= 0 && x < s.w && cc < p.c_in) {
+        const size_t pix = (static_cast<size_t>(tl.x) * ph_h + (y >> s.up)) * ph_w + (x >> s.up);
+        src = base + (pix * s.c + cc) * kEsz;
+        bytes = 16;
+      }
+    }
+    cp_async16(abuf + (u & 7) * p.lbo_a + (u >> 3) * 16, src, bytes);
+  }
 }
 
-__device__ __noinline__ void raw_unit(const Src& s, float* f, int cnt, int cc, int n, int y, int x) {
+// Per-item precompute of the asynchronous staging: each producer thread owns
+// units u = tid + 128 k (k < 8 covers every stride-1 geometry, <= 1024 units);
+// the window pixel of a unit is fixed for the whole item, only the channel
+// chunk moves, so the per-chunk work is one add + one cp.async per unit.
+constexpr int kUnitRegs = 8;
+constexpr uint32_t kNoPix = 0xffffffffu;
+__device__ __forceinline__ void unit_pixels(const TcParams& p, const int32_t* row_tab, const int4* s_tile,
+                                            uint32_t (&pix_off)[kUnitRegs]) {
+  const Src& s = p.src;
+  const int units = p.phases * p.T * p.Mt * 8;
+  const int ph_h = s.h >> s.up, ph_w = s.w >> s.up;
+#pragma unroll
+  for (int k = 0; k < kUnitRegs; ++k) {
+    const int u = threadIdx.x + k * kProdThreads;
+    pix_off[k] = kNoPix;
+    if (u >= units) continue;
+    const int32_t info = row_tab[u >> 3];
+    if (info >= 0) continue;
+    const int4 tl = s_tile[(info >> 24) & 0x7f];
+    const int y = tl.y + ((info >> 12) & 0xfff), x = tl.z + (info & 0xfff);
+    if (tl.x < 0 || y < 0 || y >= s.h || x < 0 || x >= s.w) continue;
+    const size_t pix = (static_cast<size_t>(tl.x) * ph_h + (y >> s.up)) * ph_w + (x >> s.up);
+    pix_off[k] = static_cast<uint32_t>(pix * s.c + (u & 7) * 8);  // element offset of the unit at chunk 0
+  }
+}
+
+// K chunk `ch` (64 fp16 channels) of the item from the precomputed offsets.
+__device__ __forceinline__ void stage_a_async_fast(const TcParams& p, uint32_t abuf, int ch,
+                                                   const uint32_t (&pix_off)[kUnitRegs]) {
+  const int units = p.phases * p.T * p.Mt * 8;
+  const __half* base = reinterpret_cast<const __half*>(p.src.ptr);
+#pragma unroll
+  for (int k = 0; k < kUnitRegs; ++k) {
+    const int u = threadIdx.x + k * kProdThreads;
+    if (u >= units) break;
+    const int cc = ch * 64 + (u & 7) * 8;
+    const bool ok = pix_off[k] != kNoPix && cc < p.c_in;
+    cp_async16(abuf + (u & 7) * p.lbo_a + (u >> 3) * 16, ok ? base + pix_off[k] + ch * 64 : base, ok ? 16u : 0u);
+  }
+}
+
+// The pending element-wise chain over a partial unit's values. Inlined: the
+// chain descriptor lives in the __grid_constant__ parameters, and a reference
+// handed to an out-of-line function turns every field access into a generic
+// load from parameter space (a memory round trip per value).
+__device__ __forceinline__ void epi_unit(const DevEpilogue& e, float* f, int cnt, int cc, int c, int n) {
+  for (int i = 0; i < cnt; ++i) f[i] = tc_epi(e, f[i], cc + i, c, n);
+}
+
+__device__ __forceinline__ void raw_unit(const Src& s, float* f, int cnt, int cc, int n, int y, int x) {
   for (int i = 0; i < cnt; ++i) f[i] = src_raw(s, n, cc + i, y, x);
 }
 
-// Fills A buffer with K chunk `ch`. Phase 1 resolves kBatch units and issues
-// all their 16-byte loads (8-16 loads in flight per thread); phase 2 applies
-// the epilogue, converts (tf32 round / fp16) and stores to shared memory.
-// An fp16 source in F16 mode is a pure 16-byte copy.
+// Synchronous staging (sources that need a conversion or carry a pending
+// element-wise chain): phase 1 resolves kBatch units and issues all their
+// 16-byte loads; phase 2 applies the epilogue, converts (tf32 round / fp16)
+// and stores to shared memory. An fp16 source in F16 mode is a pure copy.
 template <bool F16>
-__device__ __forceinline__ void stage_a(const TcParams& p, uint8_t* abuf, int ch, const int32_t* row_tab,
-                                        const int4* s_tile) {
+__device__ __forceinline__ void stage_a_sync(const TcParams& p, uint8_t* abuf, int ch, const int32_t* row_tab,
+                                             const int4* s_tile) {
   constexpr int kG = F16 ? 8 : 4;  // channels per 16-byte group
   const int units = p.phases * p.T * p.Mt * 8;
   const Src& s = p.src;
   const bool half_src = F16 && s.half && s.layout == kNHWC && (s.c & 7) == 0 && s.epi.num_steps == 0;
   const bool vec = !s.half && s.layout == kNHWC && (s.c & 3) == 0;
   const int ph_h = s.h >> s.up, ph_w = s.w >> s.up;
-  for (int u0 = threadIdx.x; u0 < units; u0 += kStageThreads * kBatch) {
+  for (int u0 = threadIdx.x; u0 < units; u0 += kProdThreads * kBatch) {
     float4 raw[kBatch][kG / 4];
     int4 where[kBatch];  // (n, y, x, cc); n < 0 marks a zero unit
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-      const int u = u0 + b * kStageThreads;
+      const int u = u0 + b * kProdThreads;
       where[b] = make_int4(-1, 0, 0, 0);
 #pragma unroll
       for (int v = 0; v < kG / 4; ++v) raw[b][v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -270,7 +442,7 @@ __device__ __forceinline__ void stage_a(const TcParams& p, uint8_t* abuf, int ch
     }
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-      const int u = u0 + b * kStageThreads;
+      const int u = u0 + b * kProdThreads;
       if (u >= units) break;
       uint4 st;
       if (half_src) {
@@ -288,7 +460,12 @@ __device__ __forceinline__ void stage_a(const TcParams& p, uint8_t* abuf, int ch
         if (w4.x >= 0) {
           const int cnt = min(kG, p.c_in - w4.w);
           if (!vec) raw_unit(s, f, cnt, w4.w, w4.x, w4.y, w4.z);
-          if (s.epi.num_steps) epi_unit(s.epi, f, cnt, w4.w, s.c, w4.x);
+          if (s.epi.num_steps) {
+            if (cnt == kG)
+              tc_epi_vec<kG>(s.epi, f, w4.w, s.c, w4.x);
+            else
+              epi_unit(s.epi, f, cnt, w4.w, s.c, w4.x);
+          }
         }
         if constexpr (F16) {
           st = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
@@ -303,108 +480,163 @@ __device__ __forceinline__ void stage_a(const TcParams& p, uint8_t* abuf, int ch
 }
 
 // ------------------------------------------------------------ epilogue --
-__device__ __noinline__ float addend_val(const Src& a, int n, int oc, int y, int x) {
-  return src_val(a, n, oc, y, x);
-}
-
-__device__ __noinline__ void act_store(const Dst& d, size_t p, int n, int oc0, const float* v, int cnt) {
-  float a[8];
-  for (int j = 0; j < cnt; ++j) a[j] = dev_epi(d.act_epi, v[j], oc0 + j, d.c, n);
-  if (d.act_half) {
-    __half* h = static_cast<__half*>(d.act) + p;
-    if (cnt == 8 && (p & 7) == 0) {
-      *reinterpret_cast<uint4*>(h) = make_uint4(pack_h2(a[0], a[1]), pack_h2(a[2], a[3]), pack_h2(a[4], a[5]),
-                                                pack_h2(a[6], a[7]));
-    } else {
-      for (int j = 0; j < cnt; ++j) h[j] = __float2half_rn(a[j]);
+// Out-of-line path for output groups the vector path cannot take (channel
+// counts that are not multiples of 4, the last partial group, kAddSrc with an
+// addend that is not a plain channels-last fp32 tensor). The destination is
+// passed by value: a reference into the __grid_constant__ parameters would
+// make every field access a generic load from parameter space.
+__device__ __noinline__ void out_slow(const Dst d, const float* bias, int c_out, size_t pix, int n, int y, int x,
+                                      int oc0, const float* vin, int cnt) {
+  const size_t at = pix + oc0;
+  float* o = d.ptr + at;
+  for (int j = 0; j < cnt; ++j) {
+    float v = vin[j];
+    if (bias) v = __fadd_rn(v, __ldg(bias + oc0 + j));
+    float w;
+    switch (d.mode) {
+      case kStore:
+        w = v;
+        break;
+      case kResMain:
+        w = __fadd_rn(v, __ldg(d.aux + at + j));
+        break;
+      case kResShortcut:
+        w = __fadd_rn(o[j], __fsub_rn(v, __ldg(d.aux + at + j)));
+        break;
+      default:
+        w = __fadd_rn(v, tc_epi(d.addend.epi, src_raw(d.addend, n, oc0 + j, y, x), oc0 + j, d.addend.c, n));
+        break;
     }
-  } else {
-    float* f = static_cast<float*>(d.act) + p;
-    for (int j = 0; j < cnt; ++j) f[j] = a[j];
+    o[j] = w;
+    if (d.act) {
+      const float a = tc_epi(d.act_epi, w, oc0 + j, d.c, n);
+      if (d.act_half)
+        static_cast<__half*>(d.act)[at + j] = __float2half_rn(a);
+      else
+        static_cast<float*>(d.act)[at + j] = a;
+    }
   }
 }
 
-// 8 consecutive output channels of one pixel: bias, write mode, optional act.
-__device__ __forceinline__ void out8(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float (&v)[8]) {
+__device__ __forceinline__ void ld4(const float* p, float* v) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+}
+__device__ __forceinline__ void st4(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// 16 consecutive output channels oc0.. of one pixel: bias, the write mode
+// (scatter / residual join, kernels.cpp:88-132, 291-337) and, when the
+// destination carries an activation buffer, act = chain(written value) —
+// the consumer's pending GroupNorm scale-shift + activation evaluated once
+// per output pixel. One vector path; everything else goes out of line.
+__device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v) {
   const Dst& d = p.dst;
-  const int cnt = min(8, p.c_out - oc0);
+  const int cnt = min(16, p.c_out - oc0);
   if (cnt <= 0) return;
-  if (p.bias) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < cnt) v[j] = __fadd_rn(v[j], __ldg(p.bias + oc0 + j));
+  const bool addend_vec = d.mode != kAddSrc || (d.addend.layout == kNHWC && !d.addend.half && d.addend.up == 0 &&
+                                                d.addend.epi.num_steps == 0 && (d.addend.c & 3) == 0);
+  if (cnt < 16 || (d.c & 3) != 0 || !addend_vec) {
+    out_slow(d, p.bias, p.c_out, pix, n, y, x, oc0, v, cnt);
+    return;
   }
   const size_t at = pix + oc0;
-  const bool vec = cnt == 8 && (d.c & 3) == 0;
+  float t[16];
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) ld4(p.bias + oc0 + j, t + j);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+  }
   float* o = d.ptr + at;
-  if (d.mode == kStore && vec) {
-    reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  } else if ((d.mode == kResMain || d.mode == kResShortcut) && vec) {
-    const float4 a0 = __ldg(reinterpret_cast<const float4*>(d.aux + at));
-    const float4 a1 = __ldg(reinterpret_cast<const float4*>(d.aux + at) + 1);
-    const float aux[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    float r[8];
-    if (d.mode == kResMain) {
+  if (d.mode != kStore) {
+    const float* src = d.mode == kAddSrc
+                           ? d.addend.ptr + ((static_cast<size_t>(n) * d.addend.h + y) * d.addend.w + x) * d.addend.c + oc0
+                           : d.aux + at;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(v[j], aux[j]);
-    } else {
-      const float4 b0 = reinterpret_cast<const float4*>(o)[0], b1 = reinterpret_cast<const float4*>(o)[1];
-      const float cur[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int j = 0; j < 16; j += 4) ld4(src + j, t + j);
+    if (d.mode == kResShortcut) {
+      float cur[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(cur[j], __fsub_rn(v[j], aux[j]));
-    }
-    reinterpret_cast<float4*>(o)[0] = make_float4(r[0], r[1], r[2], r[3]);
-    reinterpret_cast<float4*>(o)[1] = make_float4(r[4], r[5], r[6], r[7]);
-  } else {
-    for (int j = 0; j < cnt; ++j) {
-      switch (d.mode) {
-        case kStore:
-          o[j] = v[j];
-          break;
-        case kResMain:
-          o[j] = __fadd_rn(v[j], __ldg(d.aux + at + j));
-          break;
-        case kResShortcut:
-          o[j] = __fadd_rn(o[j], __fsub_rn(v[j], __ldg(d.aux + at + j)));
-          break;
-        default:
-          o[j] = __fadd_rn(v[j], addend_val(d.addend, n, oc0 + j, y, x));
-          break;
+      for (int j = 0; j < 16; j += 4) {
+        const float4 c4 = *reinterpret_cast<const float4*>(o + j);
+        cur[j] = c4.x, cur[j + 1] = c4.y, cur[j + 2] = c4.z, cur[j + 3] = c4.w;
       }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(cur[j], __fsub_rn(v[j], t[j]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
     }
   }
-  if (d.act) act_store(d, at, n, oc0, v, cnt);
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) st4(o + j, v + j);
+  if (d.act) {
+    tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
+    if (d.act_half) {
+      uint4* h = reinterpret_cast<uint4*>(static_cast<__half*>(d.act) + at);
+      h[0] = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+      h[1] = make_uint4(pack_h2(v[8], v[9]), pack_h2(v[10], v[11]), pack_h2(v[12], v[13]), pack_h2(v[14], v[15]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) st4(static_cast<float*>(d.act) + at + j, v + j);
+    }
+  }
 }
 
-// Runtime N tile: the largest power-of-two slice of n_pad (<= 128, >= 16,
-// multiple of 16) that still yields >= min_items work items.
+// Runtime N tile. Candidates: 16, 32, 64, 128, 256 capped at n_pad (only
+// these widths have a tensor map whose box matches: pack_weights_tc builds
+// box n = min(size, n_pad)) and dividing n_pad. An MMA of width N costs about
+// max(47, 40 + N/4) cycles at this issue pattern (tools/mma_bench.cu on B200:
+// N=16: 47, 64: 65, 128: 76, 256: 130), every item runs the same number of
+// MMAs, so pick the width minimising rounds x cost-per-MMA over the SMs.
 __device__ __forceinline__ int pick_n_tile(const TcParams& p, int items_m) {
-  int nt = min(p.n_pad, kMaxNTile);
-  while (nt > 16 && (nt / 2) % 16 == 0 && p.n_pad % (nt / 2) == 0 &&
-         static_cast<long long>(items_m) * (p.n_pad / nt) < p.min_items)
-    nt /= 2;
-  return nt;
+  int best = min(p.n_pad, kMaxNTile);
+  long long best_cost = -1;
+  for (int c = 16; c <= kMaxNTile; c <<= 1) {
+    const int nt = min(c, p.n_pad);
+    if (p.n_pad % nt != 0) continue;
+    const long long items = static_cast<long long>(items_m) * (p.n_pad / nt);
+    const long long rounds = (items + p.min_items - 1) / p.min_items;
+    const long long cost = rounds * max(47, 40 + nt / 4) * 1024 + nt;  // ties -> narrower
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = nt;
+    }
+    if (nt == p.n_pad) break;
+  }
+  return best;
 }
 
-__device__ __forceinline__ int nt_index(int nt) { return nt <= 16 ? 0 : nt <= 32 ? 1 : nt <= 64 ? 2 : 3; }
+__device__ __forceinline__ int nt_index(int nt) {
+  return nt <= 16 ? 0 : nt <= 32 ? 1 : nt <= 64 ? 2 : nt <= 128 ? 3 : 4;
+}
 
-template <bool F16>
+// Warp roles (320 threads, one CTA per SM, persistent over work items =
+// (group of T tiles, N slice)):
+//   warps 0-3  A producers: K chunk c of item i into A stage c % na (cp.async
+//              ring, up to na-1 chunks in flight, or synchronous staging)
+//   warps 4-7  epilogue: TMEM accumulator (i & 1) -> bias / residual -> dst
+//   warp 8     TMEM allocation + the single MMA-issuing thread
+//   warp 9     weight producer: one TMA per ring stage (1, 3 or 9 taps)
+template <bool F16, int K, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[2], bar_afree[2];
-  __shared__ __align__(8) uint64_t bar_acc_full, bar_acc_empty;
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[kMaxNA], bar_afree[kMaxNA];
+  __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int4 s_tile[16];  // item tiles: (n, window origin y, x, -); n = -1 for empty slots
+  __shared__ int4 s_tile[16];  // producers' current item tiles: (n, window origin y, x, -); n = -1 empty slot
 
-  uint8_t* abuf[2] = {smem, smem + p.a_bytes};
-  uint8_t* bbuf = smem + 2 * p.a_bytes;
+  uint8_t* abuf0 = smem;
+  uint8_t* bbuf = smem + p.na * p.a_bytes;
   int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.nb * p.b_stage_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
-    tl_cta(p, 256);
+    tl_cta(p, 1024);
+    if (p.tl && blockIdx.x < 8) p.tl[blockIdx.x * 64 + 60] = clock64();
   }
   for (int q = threadIdx.x; q < p.phases * p.T * p.Mt; q += blockDim.x) row_tab[q] = row_info(p, q);
 
@@ -413,17 +645,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_bfull[i], 1);
       mbar_init(&bar_bempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_afull[i], kStageThreads);
+    for (int i = 0; i < p.na; ++i) {
+      mbar_init(&bar_afull[i], kProdThreads);
       mbar_init(&bar_afree[i], 1);
     }
-    mbar_init(&bar_acc_full, 1);
-    mbar_init(&bar_acc_empty, kStageThreads);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_acc_full[i], 1);
+      mbar_init(&bar_acc_empty[i], kEpiThreads);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(kMaxNTile)
+                 "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -447,100 +681,173 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t idesc = p.idesc_base | (static_cast<uint32_t>(n_tile >> 3) << 17);
   if (threadIdx.x == 0) pdl_trigger();  // the next layer may start its own setup
 
-  if (warp < 8) {
-    // ---------------- A staging + epilogue ----------------
-    pdl_wait();  // the source / destination were written by the previous kernel
+  if (warp < 4) {
+    // ---------------- A producers ----------------
+    pdl_wait();  // the source was written by the previous kernel
+    const uint32_t a0 = smem_u32(abuf0);
     uint32_t a_iter = 0, it = 0;
-    const int m = threadIdx.x & 127;  // TMEM lane = GEMM row
-    const int half = warp >> 2;       // column half of the accumulator
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int mi = item / n_slices, ni = item % n_slices;
+      const int mi = item / n_slices;
       const int g0 = mi * p.T, nt = min(p.T, count - g0);
-      asm volatile("bar.sync 1, %0;" ::"n"(kStageThreads));  // previous item's s_tile readers done
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));  // previous item's s_tile readers done
       if (threadIdx.x < p.T) {
         const int t = threadIdx.x, g = g0 + t;
         s_tile[t] = t < nt ? make_int4(p.tiles.idx[3 * g], p.tiles.idx[3 * g + 1] * p.s - p.pad,
                                        p.tiles.idx[3 * g + 2] * p.s - p.pad, 0)
                            : make_int4(-1, 0, 0, 0);
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kStageThreads));
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+      uint32_t pix_off[kUnitRegs];
+      const bool fast_units = F16 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
+      if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off);
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
       for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
-        const int b = a_iter & 1;
-        if (a_iter >= 2) mbar_wait(&bar_afree[b], ((a_iter >> 1) - 1) & 1);
-        stage_a<F16>(p, abuf[b], ch, row_tab, s_tile);
+        const int sidx = static_cast<int>(a_iter % p.na);
+        if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
+        if (p.async_a) {
+          // The arrival fires when this thread's copies have landed, so the
+          // producers run ahead to the next free stage without waiting.
+          if (fast_units)
+            stage_a_async_fast(p, a0 + sidx * p.a_bytes, ch, pix_off);
+          else
+            stage_a_async<F16>(p, a0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+          cp_async_arrive(&bar_afull[sidx]);
+        } else {
+          stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+          fence_proxy_async();
+          mbar_arrive(&bar_afull[sidx]);
+        }
         if (threadIdx.x == 0 && it == 0 && ch == 0) tl_mark(p, 3);
-        fence_proxy_async();
-        mbar_arrive(&bar_afull[b]);
+        if (threadIdx.x == 0 && it == 0 && ch < 8) tl_mark(p, 14 + ch);
       }
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 4);
-      mbar_wait(&bar_acc_full, it & 1);
-      tc_fence_after();
-      if (threadIdx.x == 0 && it == 0) tl_mark(p, 5);
-      const int t = m / p.Mt, rr = m - t * p.Mt;
-      const int oy = rr / p.P, ox = rr - oy * p.P;
-      bool valid = t < nt && oy < p.tiles.bh && ox < p.tiles.bw;
+    }
+    // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp < 8) {
+    // ---------------- epilogue ----------------
+    pdl_wait();  // the destination / residual inputs were written by earlier kernels
+    const int q = warp & 3;                       // TMEM lane quarter of this warp
+    const int m = q * 32 + lane;                  // TMEM lane = GEMM row
+    const int t = m / p.Mt, rr = m - t * p.Mt;
+    const int oy = rr / p.P, ox = rr - oy * p.P;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const int mi = item / n_slices, ni = item % n_slices;
+      const int g = mi * p.T + t;
+      bool valid = t < p.T && g < count && oy < p.tiles.bh && ox < p.tiles.bw;
       int n = 0, y = 0, x = 0;
       if (valid) {
-        const int4 tl = s_tile[t];
-        n = tl.x;
-        y = (tl.y + p.pad) / p.s + oy;
-        x = (tl.z + p.pad) / p.s + ox;
+        n = __ldg(p.tiles.idx + 3 * g);
+        y = __ldg(p.tiles.idx + 3 * g + 1) + oy;
+        x = __ldg(p.tiles.idx + 3 * g + 2) + ox;
         valid = y < p.dst.h && x < p.dst.w;
       }
       const size_t pix = ((static_cast<size_t>(n) * p.dst.h + y) * p.dst.w + x) * p.dst.c;
-      const int cols = n_tile / 2;
-      for (int cb = half * cols; cb < (half + 1) * cols; cb += 8) {
-        float v[8];
-        tmem_ld8(taddr + (static_cast<uint32_t>((warp & 3) * 32) << 16) + static_cast<uint32_t>(cb), v);
-        if (valid) out8(p, pix, n, y, x, ni * n_tile + cb, v);
+      // While the MMAs run: pull this item's per-channel params (bias, the act
+      // chain's scale/shift) and this row's residual operand into L1, so the
+      // epilogue's loads hit instead of paying an L2 round trip each.
+      {
+        const int oc0 = ni * n_tile, nb = n_tile * 4;  // bytes of one slice of per-channel floats
+        const int lines = (nb + 127) / 128;
+        int li = threadIdx.x - kProdThreads;
+        if (p.bias && li < lines) prefetch_l1(p.bias + oc0 + li * 32);
+        li -= lines;
+        const DevEpilogue& ae = p.dst.act_epi;
+        for (int sstep = 0; sstep < ae.num_steps && p.dst.act; ++sstep) {
+          if (ae.kind[sstep] != SIGE_EPI_SCALE_SHIFT) continue;
+          const int reps = ae.per_sample[sstep] ? p.dst.n : 1;
+          for (int r = 0; r < reps; ++r) {
+            const int off = (ae.per_sample[sstep] ? r * p.dst.c : 0) + oc0;
+            if (li >= 0 && li < lines) prefetch_l1(ae.scale[sstep] + off + li * 32);
+            if (li >= lines && li < 2 * lines) prefetch_l1(ae.shift[sstep] + off + (li - lines) * 32);
+            li -= 2 * lines;
+          }
+        }
+        if (valid && (p.dst.mode == kResMain || p.dst.mode == kResShortcut)) {
+          for (int b = 0; b < nb; b += 128) {
+            prefetch_l1(p.dst.aux + pix + oc0 + b / 4);
+            if (p.dst.mode == kResShortcut) prefetch_l1(p.dst.ptr + pix + oc0 + b / 4);
+          }
+        }
       }
-      if (threadIdx.x == 0 && it == 0) tl_mark(p, 6);
+      const uint32_t acc = it & 1;
+      mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
+      tc_fence_after();
+      if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 5);
+      const uint32_t tbase = taddr + (static_cast<uint32_t>(q * 32) << 16) + acc * kMaxNTile;
+      for (int cb = 0; cb < n_tile; cb += 16) {
+        float v[16];
+        tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
+        if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
+        if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v);
+      }
+      if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 47);
       tc_fence_before();
-      mbar_arrive(&bar_acc_empty);
+      mbar_arrive(&bar_acc_empty[acc]);
+      if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 6);
     }
   } else if (warp == 8) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      uint32_t a_iter = 0, b_iter = 0, it = 0;
-      const uint32_t a0 = smem_u32(abuf[0]), a1 = smem_u32(abuf[1]), b0 = smem_u32(bbuf);
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        if (it > 0) {
-          mbar_wait(&bar_acc_empty, (it - 1) & 1);
-          tc_fence_after();
-        }
-        for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
-          const int b = a_iter & 1;
-          mbar_wait(&bar_afull[b], (a_iter >> 1) & 1);
-          tc_fence_after();
-          if (it == 0 && ch == 0) tl_mark(p, 7);
-          const uint32_t abase = b ? a1 : a0;
-          for (int tg = 0; tg < tgroups; ++tg, ++b_iter) {
-            const int st = b_iter % p.nb;
-            mbar_wait(&bar_bfull[st], (b_iter / p.nb) & 1);
-            tc_fence_after();
-            if (b_iter == 0) tl_mark(p, 8);
-            for (int tt = 0; tt < tps; ++tt) {
-              const int tap = tg * tps + tt;
-              const int ky = tap / p.k, kx = tap - ky * p.k;
-              const int phase = p.s == 2 ? ((ky & 1) << 1) | (kx & 1) : 0;
-              const int shift = (ky / p.s) * p.P + (kx / p.s);
-              const uint32_t arow = abase + static_cast<uint32_t>((phase * p.T * p.Mt + shift) * 16);
-              const uint32_t brow = b0 + static_cast<uint32_t>(st * p.b_stage_bytes) + tt * tap_b;
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
-                const uint64_t ad = umma_desc(arow + kk * 2 * p.lbo_a, p.lbo_a, 128);
-                const uint64_t bd = umma_desc(brow + kk * 2 * lbo_b, lbo_b, 128);
-                umma<F16>(taddr, ad, bd, idesc, (ch | tap | kk) != 0 ? 1u : 0u);
-              }
-            }
-            umma_commit(&bar_bempty[st]);
-          }
-          umma_commit(&bar_afree[b]);
-        }
-        umma_commit(&bar_acc_full);
-        if (it == 0) tl_mark(p, 9);
+    // ---------------- MMA issuer (whole warp, converged) ----------------
+    // Descriptors are uniform: base descriptor with a zero start field plus
+    // the (stage, tap, k-step) offset in 16-byte units; the taps are unrolled
+    // at compile time (K, S), one elected lane issues each tcgen05.mma.
+    uint32_t a_iter = 0, b_iter = 0, it = 0;
+    const uint32_t a0 = smem_u32(abuf0) >> 4, b0 = smem_u32(bbuf) >> 4;
+    const uint64_t adesc0 = umma_desc(0, p.lbo_a, 128), bdesc0 = umma_desc(0, lbo_b, 128);
+    const uint32_t lbo_a16 = p.lbo_a >> 4, lbo_b16 = lbo_b >> 4, tap_b16 = tap_b >> 4;
+    const uint32_t plane16 = static_cast<uint32_t>(p.T * p.Mt), astage16 = static_cast<uint32_t>(p.a_bytes >> 4);
+    const uint32_t bstage16 = static_cast<uint32_t>(p.b_stage_bytes >> 4), P = static_cast<uint32_t>(p.P);
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const uint32_t acc = it & 1;
+      if (it >= 2) {
+        mbar_wait(&bar_acc_empty[acc], ((it >> 1) - 1) & 1);
+        __syncwarp();
+        tc_fence_after();
       }
+      const uint32_t tmem_d = taddr + acc * kMaxNTile;
+      for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
+        const uint32_t sidx = a_iter % static_cast<uint32_t>(p.na);
+        mbar_wait(&bar_afull[sidx], (a_iter / p.na) & 1);
+        __syncwarp();
+        fence_proxy_async();
+        tc_fence_after();
+        if (lane == 0 && it == 0 && ch == 0) tl_mark(p, 7);
+        if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 22 + ch);
+        const uint32_t abase = a0 + sidx * astage16;
+        uint32_t st = 0, bbase = 0;
+#pragma unroll
+        for (int tap = 0; tap < K * K; ++tap) {
+          const int tt = tap % tps;
+          if (tt == 0) {
+            st = b_iter % static_cast<uint32_t>(p.nb);
+            mbar_wait(&bar_bfull[st], (b_iter / p.nb) & 1);
+            __syncwarp();
+            tc_fence_after();
+            if (lane == 0 && b_iter == 0) tl_mark(p, 8);
+            bbase = b0 + st * bstage16;
+          }
+          const int ky = tap / K, kx = tap % K;
+          const uint32_t phase = S == 2 ? static_cast<uint32_t>(((ky & 1) << 1) | (kx & 1)) : 0u;
+          const uint32_t aoff =
+              abase + phase * plane16 + static_cast<uint32_t>(ky / S) * P + static_cast<uint32_t>(kx / S);
+          const uint32_t boff = bbase + static_cast<uint32_t>(tt) * tap_b16;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
+            const uint64_t ad = adesc0 | static_cast<uint64_t>((aoff + kk * 2 * lbo_a16) & 0x3FFFu);
+            const uint64_t bd = bdesc0 | static_cast<uint64_t>((boff + kk * 2 * lbo_b16) & 0x3FFFu);
+            if (elect_one()) umma<F16>(tmem_d, ad, bd, idesc, (ch | tap | kk) != 0 ? 1u : 0u);
+          }
+          if (tt == tps - 1) {
+            if (elect_one()) umma_commit(&bar_bempty[st]);
+            ++b_iter;
+          }
+        }
+        if (elect_one()) umma_commit(&bar_afree[sidx]);
+        if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 30 + ch);
+      }
+      if (elect_one()) umma_commit(&bar_acc_full[acc]);
+      if (lane == 0 && it == 0) tl_mark(p, 9);
     }
   } else {
     // ---------------- weight producer (TMA) ----------------
@@ -554,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ni = item % n_slices;
         for (int ch = 0; ch < p.nchunks; ++ch)
           for (int tg = 0; tg < tgroups; ++tg, ++b_iter) {
-            const int st = b_iter % p.nb;
+            const int st = static_cast<int>(b_iter % p.nb);
             if (b_iter >= static_cast<uint32_t>(p.nb)) mbar_wait(&bar_bempty[st], ((b_iter / p.nb) - 1) & 1);
             mbar_expect_tx(&bar_bfull[st], stage_bytes);
             tma_3d(b0 + st * p.b_stage_bytes, map, 0, ni * n_tile, (ch * p.ntaps + tg * tps) * 8, &bar_bfull[st]);
@@ -564,16 +871,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (threadIdx.x == 0) tl_mark(p, 12);
+  if (threadIdx.x == 0) {
+    tl_mark(p, 12);
+    if (p.tl && blockIdx.x < 8) p.tl[blockIdx.x * 64 + 61] = clock64();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 8) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kMaxNTile)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kTmemCols)
                  : "memory");
     if (lane == 0) {
       tl_mark(p, 13);
-      tl_cta(p, 512);
+      tl_cta(p, 2048);
     }
   }
 }
@@ -648,8 +958,8 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
   cw->w_tc = out;
   // One 3-D tensor map per N-slice width: dims (16-byte element group, n, (chunk, tap, group)),
   // box (group, n_tile, taps_per_stage * 8) — a ring stage is one TMA.
-  const int sizes[4] = {16, 32, 64, 128};
-  for (int i = 0; i < 4; ++i) {
+  const int sizes[5] = {16, 32, 64, 128, 256};
+  for (int i = 0; i < 5; ++i) {
     const int nt = std::min(sizes[i], cw->n_pad);
     const int tps = tps_for(nt, ntaps);
     cw->maps.tps[i] = tps;
@@ -673,6 +983,10 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   if (tiles.capacity == 0) return;
   TcParams p{};
   p.src = src;
+  if (f16 && src.twin && src.epi.num_steps == 0 && src.layout == kNHWC && !src.half) {
+    p.src.ptr = static_cast<const float*>(src.twin);  // stream the fp16 twin
+    p.src.half = 1;
+  }
   p.tiles = tiles;
   p.dst = dst;
   p.bias = cw.bias;
@@ -684,7 +998,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.n_pad = cw.n_pad;
   p.nchunks = cw.k_pad / (f16 ? 64 : 32);
   p.ntaps = cw.k * cw.k;
-  for (int i = 0; i < 4; ++i) p.tps[i] = cw.maps.tps[i];
+  for (int i = 0; i < 5; ++i) p.tps[i] = cw.maps.tps[i];
   const int bh = tiles.bh, bw = tiles.bw;
   int rows_ph;
   if (cw.stride == 1) {
@@ -720,30 +1034,58 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.lbo_a = static_cast<uint32_t>(r_total * 16);
   p.a_bytes = (r_total * 16 * 8 + 1023) / 1024 * 1024;
   int max_stage = 0;
-  const int sizes[4] = {16, 32, 64, 128};
-  for (int i = 0; i < 4; ++i) max_stage = std::max(max_stage, p.tps[i] * std::min(sizes[i], p.n_pad) * 128);
+  const int sizes[5] = {16, 32, 64, 128, 256};
+  for (int i = 0; i < 5; ++i) max_stage = std::max(max_stage, p.tps[i] * std::min(sizes[i], p.n_pad) * 128);
   p.b_stage_bytes = (max_stage + 1023) / 1024 * 1024;
   p.min_items = sm_count();
   const uint32_t fmt = f16 ? 0u : 2u;
   p.idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(128 >> 4) << 24);
-  const size_t fixed = 2 * static_cast<size_t>(p.a_bytes) + sizeof(int32_t) * p.phases * p.T * p.Mt;
+  // A staged by cp.async when the source already holds the MMA operand —
+  // fp16 channels-last with no pending chain, in F16 mode. kind::tf32 would
+  // read fp32 sources as-is but truncates them to 10-bit mantissas (2x the
+  // round-to-nearest error: 1.15e-2 normalised on ddim_stack_64x32 vs the
+  // 1e-2 bar), so TF32 stages synchronously with cvt.rna like every
+  // converting / chained source.
+  const int unit_ch = f16 ? 8 : 4;
+  p.async_a = f16 && p.src.layout == kNHWC && p.src.epi.num_steps == 0 && p.src.c == cw.c_in &&
+                      p.src.c % unit_ch == 0 && p.src.half != 0
+                  ? 1
+                  : 0;
+  // Ring depths: as many A stages (<= 4) and weight stages (<= 8) as fit.
+  constexpr size_t kSmemBudget = 225 * 1024;
+  const size_t fixed = sizeof(int32_t) * p.phases * p.T * p.Mt;
+  p.na = kMaxNA;
   p.nb = kMaxNB;
-  while (p.nb > 2 && fixed + static_cast<size_t>(p.nb) * p.b_stage_bytes > 220 * 1024) --p.nb;
-  const size_t smem = fixed + static_cast<size_t>(p.nb) * p.b_stage_bytes;
-  if (smem > 220 * 1024)
+  auto need = [&] { return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.nb) * p.b_stage_bytes; };
+  while (need() > kSmemBudget && (p.nb > 4 || (p.na == 2 && p.nb > 2))) --p.nb;
+  while (need() > kSmemBudget && p.na > 2) --p.na;
+  while (need() > kSmemBudget && p.nb > 2) --p.nb;
+  const size_t smem = need();
+  if (smem > kSmemBudget)
     throw ConfigError("conv (tensor core): staging needs " + std::to_string(smem) + " B of shared memory");
+  using KernelFn = void (*)(TcParams, TcMaps);
+  KernelFn fn = nullptr;
+  if (cw.k == 1)
+    fn = f16 ? k_conv_tc<true, 1, 1> : k_conv_tc<false, 1, 1>;
+  else if (cw.stride == 1)
+    fn = f16 ? k_conv_tc<true, 3, 1> : k_conv_tc<false, 3, 1>;
+  else
+    fn = f16 ? k_conv_tc<true, 3, 2> : k_conv_tc<false, 3, 2>;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    SIGE_CUDA(cudaFuncSetAttribute(k_conv_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    SIGE_CUDA(cudaFuncSetAttribute(k_conv_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (KernelFn f : {k_conv_tc<true, 1, 1>, k_conv_tc<false, 1, 1>, k_conv_tc<true, 3, 1>, k_conv_tc<false, 3, 1>,
+                       k_conv_tc<true, 3, 2>, k_conv_tc<false, 3, 2>})
+      SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
   });
   static unsigned long long* tl_buf = nullptr;
   static const bool timeline = std::getenv("SIGE_TC_TIMELINE") != nullptr;
   if (timeline) {
-    if (!tl_buf) SIGE_CUDA(cudaMalloc(&tl_buf, 1024 * sizeof(unsigned long long)));
-    SIGE_CUDA(cudaMemsetAsync(tl_buf, 0, 1024 * sizeof(unsigned long long), st));
+    if (!tl_buf) SIGE_CUDA(cudaMalloc(&tl_buf, 4096 * sizeof(unsigned long long)));
+    SIGE_CUDA(cudaMemsetAsync(tl_buf, 0, 4096 * sizeof(unsigned long long), st));
     p.tl = tl_buf;
   }
+  static const int dbg = std::getenv("SIGE_TC_DEBUG") ? std::atoi(std::getenv("SIGE_TC_DEBUG")) : 0;
+  p.dbg = dbg;
   const long long max_items = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
   const int grid = static_cast<int>(std::max(1LL, std::min<long long>(max_items, sm_count())));
   cudaLaunchConfig_t cfg{};
@@ -756,30 +1098,31 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (f16)
-    SIGE_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<true>, p, cw.maps));
-  else
-    SIGE_CUDA(cudaLaunchKernelEx(&cfg, k_conv_tc<false>, p, cw.maps));
+  SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
   after_launch("k_conv_tc");
   if (timeline) {
-    unsigned long long h[1024];
+    static unsigned long long h[4096];
     SIGE_CUDA(cudaMemcpyAsync(h, tl_buf, sizeof h, cudaMemcpyDeviceToHost, st));
     SIGE_CUDA(cudaStreamSynchronize(st));
     unsigned long long t0 = ~0ull, tend = 0, last = 0;
     for (int i = 0; i < grid; ++i)
-      if (h[256 + i]) {
-        t0 = std::min(t0, h[256 + i]);
-        tend = std::max(tend, h[512 + i]);
+      if (h[1024 + i]) {
+        t0 = std::min(t0, h[1024 + i]);
+        tend = std::max(tend, h[2048 + i]);
       }
     for (int i = 0; i < grid; ++i)
-      if (h[256 + i]) last = std::max(last, h[256 + i] - t0);
-    std::fprintf(stderr, "[tc] %dx%d c%d->%d k%d s%d T%d Mt%d grid %d nb %d: span %.2f us, last entry %.2f us\n",
-                 tiles.bh, tiles.bw, cw.c_in, cw.c_out, cw.k, cw.stride, p.T, p.Mt, grid, p.nb, (tend - t0) * 1e-3,
-                 last * 1e-3);
+      if (h[1024 + i]) last = std::max(last, h[1024 + i] - t0);
+    std::fprintf(stderr,
+                 "[tc] %dx%d c%d->%d k%d s%d T%d Mt%d grid %d na %d nb %d async %d: span %.2f us, last entry %.2f us\n",
+                 tiles.bh, tiles.bw, cw.c_in, cw.c_out, cw.k, cw.stride, p.T, p.Mt, grid, p.na, p.nb, p.async_a,
+                 (tend - t0) * 1e-3, last * 1e-3);
     for (int c = 0; c < 2; ++c) {
+      if (h[c * 64 + 12] > h[c * 64 + 0])
+        std::fprintf(stderr, "  cta%d clock: %.0f MHz\n", c,
+                     double(h[c * 64 + 61] - h[c * 64 + 60]) / double(h[c * 64 + 12] - h[c * 64 + 0]) * 1e3);
       std::fprintf(stderr, "  cta%d:", c);
-      for (int e = 0; e < 14; ++e)
-        std::fprintf(stderr, " %d:%.2f", e, h[c * 32 + e] ? (h[c * 32 + e] - t0) * 1e-3 : -1.0);
+      for (int e = 0; e < 48; ++e)
+        if (h[c * 64 + e]) std::fprintf(stderr, " %d:%.2f", e, (static_cast<long long>(h[c * 64 + e]) - static_cast<long long>(t0)) * 1e-3);
       std::fprintf(stderr, "\n");
     }
   }

@@ -53,6 +53,7 @@ Src plain(const DevTensor& t) {
   s.w = t.w;
   s.half = t.half;
   s.epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+  s.twin = t.h16;
   return s;
 }
 
@@ -64,7 +65,16 @@ Dst to_dst(const DevTensor& t, int mode = kStore) {
   d.h = t.h;
   d.w = t.w;
   d.mode = mode;
+  if (t.h16) {  // the epilogue also writes the fp16 twin (identity chain)
+    d.act = t.h16;
+    d.act_half = 1;
+  }
   return d;
+}
+
+bool ends_with(const std::string& s, const char* suf) {
+  const size_t n = std::strlen(suf);
+  return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
 }
 
 }  // namespace
@@ -206,6 +216,17 @@ const DevNorm& Engine::cache_norm(int step, const std::string& key) const {
   return it->second;
 }
 
+bool Engine::wants_twin(const std::string& key, int layout, int half) const {
+  if (math_ != SIGE_MATH_F16 || layout != kNHWC || half) return false;
+  if (ends_with(key, ".sum")) return true;
+  return ends_with(key, ".out") && !ends_with(key, "conv1.out") && !ends_with(key, "conv2.out") &&
+         !ends_with(key, "shortcut.out");
+}
+
+void Engine::attach_twin(DevTensor& t, const std::string& key) {
+  if (wants_twin(key, t.layout, t.half) && !t.h16) t.h16 = alloc(t.numel() * 2);
+}
+
 DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, int w, int layout, int half) {
   DevTensor& t = cache_[{step, key}];
   if (!t.p || t.c != c || t.h != h || t.w != w || t.n != batch_ || t.layout != layout || t.half != half) {
@@ -216,7 +237,9 @@ DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, in
     t.w = w;
     t.layout = layout;
     t.half = half;
+    t.h16 = nullptr;
   }
+  attach_twin(t, key);
   return t;
 }
 
@@ -257,7 +280,9 @@ DevTensor& Engine::scratch(const std::string& key, int c, int h, int w, int layo
     t.w = w;
     t.layout = layout;
     t.half = half;
+    t.h16 = nullptr;
   }
+  attach_twin(t, key);
   return t;
 }
 
@@ -280,6 +305,10 @@ DevTensor& Engine::work_buffer(int step, const std::string& key) {
   DevTensor w = src;
   w.p = static_cast<float*>(alloc(src.bytes()));
   SIGE_CUDA(cudaMemcpy(w.p, src.p, src.bytes(), cudaMemcpyDeviceToDevice));
+  if (src.h16) {
+    w.h16 = alloc(src.numel() * 2);
+    SIGE_CUDA(cudaMemcpy(w.h16, src.h16, src.numel() * 2, cudaMemcpyDeviceToDevice));
+  }
   return work_[{step, key}] = w;
 }
 
@@ -494,7 +523,7 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         if (capture) {
           DevTensor& m2 = cache_slot(step, key + ".conv2.out", co, h, w, kNHWC);
           conv(mid, dense_tiles(h, w, 3, 1), L.conv2, to_dst(m2), st);
-          launch_add(m2.p, sc.p, sum.p, sum.numel(), st);  // add(m, sc), graph.cpp:404
+          launch_add_h(m2.p, sc.p, sum.p, sum.h16, sum.numel(), st);  // add(m, sc), graph.cpp:404
         } else {
           Dst d = to_dst(sum, kAddSrc);
           d.addend = plain(sc);
@@ -582,6 +611,10 @@ void Engine::put_tensor(int step, const std::string& key, const float* host, siz
     std::memcpy(buf.data(), host, numel * sizeof(float));
   }
   SIGE_CUDA(cudaMemcpy(t.p, buf.data(), numel * sizeof(float), cudaMemcpyHostToDevice));
+  if (t.h16) {
+    launch_to_half(t.p, t.h16, numel, nullptr);
+    SIGE_CUDA(cudaStreamSynchronize(nullptr));
+  }
 }
 
 void Engine::put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np) {
@@ -686,6 +719,12 @@ struct ProgramBuilder {
     j.layout = wbuf.layout;
     j.half = wbuf.half;
     P.restores.push_back(j);
+    if (wbuf.h16 && cache.h16) {  // the fp16 twin's dirtied tiles too
+      j.dst = static_cast<float*>(wbuf.h16);
+      j.src = static_cast<const float*>(cache.h16);
+      j.half = 1;
+      P.restores.push_back(j);
+    }
     P.restore_max = std::max<long long>(P.restore_max, static_cast<long long>(e.capacity) * e.b * e.b * wbuf.c);
   }
 

@@ -34,6 +34,7 @@ struct DevTensor {
   int n = 0, c = 0, h = 0, w = 0;
   int layout = kNHWC;
   int half = 0;
+  void* h16 = nullptr;  // fp16 twin (F16 mode, tensors that feed convolutions)
   size_t numel() const { return static_cast<size_t>(n) * c * h * w; }
   size_t bytes() const { return numel() * (half ? 2 : 4); }
 };
@@ -95,6 +96,11 @@ class Engine {
   const DevTensor& cache_tensor(int step, const std::string& key) const;
   const DevNorm& cache_norm(int step, const std::string& key) const;
   DevTensor& cache_slot(int step, const std::string& key, int c, int h, int w, int layout, int half = 0);
+  // F16 mode: layer outputs that later convolutions read (".out" of Conv /
+  // Downsample layers, ".sum" of ResBlocks) carry an fp16 twin written by the
+  // producing kernel's epilogue.
+  bool wants_twin(const std::string& key, int layout, int half) const;
+  void attach_twin(DevTensor& t, const std::string& key);
   DevNorm& norm_slot(int step, const std::string& key, int np);
   DevTensor& work_buffer(int step, const std::string& key);
   DevTensor& scratch(const std::string& key, int c, int h, int w, int layout, int half = 0);

@@ -399,7 +399,9 @@ __global__ void k_identity_join(Src s, Tiles t, Dst d) {
     int n, y, x, ch;
     if (!tile_elem(t, count, d.c, d.h, d.w, q, n, y, x, ch)) continue;
     const size_t p = ((static_cast<size_t>(n) * d.h + y) * d.w + x) * d.c + ch;
-    d.ptr[p] = __fadd_rn(d.ptr[p], __fsub_rn(src_val(s, n, ch, y, x), d.aux[p]));
+    const float v = __fadd_rn(d.ptr[p], __fsub_rn(src_val(s, n, ch, y, x), d.aux[p]));
+    d.ptr[p] = v;
+    if (d.act && d.act_half) static_cast<__half*>(d.act)[p] = __float2half_rn(v);  // fp16 twin
   }
 }
 
@@ -468,10 +470,19 @@ __global__ void k_finalize(Src r, const float* __restrict__ cached, const int32_
 }
 
 __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ o,
-                      long long n) {
+                      __half* __restrict__ oh, long long n) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const float v = __fadd_rn(a[q], b[q]);
+    o[q] = v;
+    if (oh) oh[q] = __float2half_rn(v);
+  }
+}
+
+__global__ void k_to_half(const float* __restrict__ a, __half* __restrict__ o, long long n) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x)
-    o[q] = __fadd_rn(a[q], b[q]);
+    o[q] = __float2half_rn(a[q]);
 }
 
 __global__ void k_nchw_to_nhwc(const float* __restrict__ in, float* __restrict__ out, int n, int c,
@@ -577,7 +588,9 @@ void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, con
 
 void launch_materialize_act(const Src& src, void* dst, int half, cudaStream_t st) {
   const long long total = static_cast<long long>(src.n) * src.c * src.h * src.w;
-  k_materialize_act<<<grid_cap(total, 256), 256, 0, st>>>(src, dst, half);
+  Src s = src;
+  s.epi.fast = 1;  // activation buffers exist in the tensor-core modes only
+  k_materialize_act<<<grid_cap(total, 256), 256, 0, st>>>(s, dst, half);
   after_launch("k_materialize_act");
 }
 
@@ -618,8 +631,19 @@ void launch_finalize(const Src& result, const float* cached_final, const int32_t
 }
 
 void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st) {
-  k_add<<<grid_cap(static_cast<long long>(n), 256), 256, 0, st>>>(a, b, out, static_cast<long long>(n));
+  launch_add_h(a, b, out, nullptr, n, st);
+}
+
+void launch_add_h(const float* a, const float* b, float* out, void* out_h16, size_t n, cudaStream_t st) {
+  k_add<<<grid_cap(static_cast<long long>(n), 256), 256, 0, st>>>(a, b, out, static_cast<__half*>(out_h16),
+                                                                  static_cast<long long>(n));
   after_launch("k_add");
+}
+
+void launch_to_half(const float* src, void* dst_h16, size_t n, cudaStream_t st) {
+  k_to_half<<<grid_cap(static_cast<long long>(n), 256), 256, 0, st>>>(src, static_cast<__half*>(dst_h16),
+                                                                      static_cast<long long>(n));
+  after_launch("k_to_half");
 }
 
 void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st) {

@@ -28,6 +28,9 @@ struct Src {
   int up = 0;                       // log2 upsample factor
   int half = 0;                     // storage is fp16 (activation buffers), else fp32
   DevEpilogue epi;
+  // fp16 channels-last copy of the same values (F16 mode): the tensor-core
+  // conv streams it with cp.async when no element-wise chain is pending.
+  const void* twin = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -79,10 +82,10 @@ struct Tiles {
 };
 
 // TMA descriptors of a packed weight tensor, one per N-slice width
-// (16, 32, 64, 128) with the taps batched per ring stage.
+// (16, 32, 64, 128, 256) with the taps batched per ring stage.
 struct TcMaps {
-  CUtensorMap m[4];
-  int tps[4];
+  CUtensorMap m[5];
+  int tps[5];
 };
 
 struct ConvW {
@@ -166,6 +169,10 @@ void launch_finalize(const Src& result, const float* cached_final, const int32_t
                      cudaStream_t st);
 // Elementwise a + b over n values (dense ResBlock sum in precompute).
 void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st);
+// Same, also writing out_h16 = fp16(out) when out_h16 != nullptr.
+void launch_add_h(const float* a, const float* b, float* out, void* out_h16, size_t n, cudaStream_t st);
+// dst_h16 = fp16(src) elementwise (same layout).
+void launch_to_half(const float* src, void* dst_h16, size_t n, cudaStream_t st);
 // Layout conversions.
 void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);
 void launch_nhwc_to_nchw(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);

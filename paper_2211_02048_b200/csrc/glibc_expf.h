@@ -40,7 +40,10 @@ namespace sige_b200 {
 }
 static const uint64_t kExp2fTabHost[32] = SIGE_EXP2F_TAB;
 #ifdef __CUDACC__
-__device__ __constant__ uint64_t kExp2fTabDev[32] = SIGE_EXP2F_TAB;
+// Global (not __constant__): the index k & 31 differs per lane, and the
+// constant cache serialises divergent indices (up to 32 ways per warp load);
+// through L1 the whole 256-byte table is two cache lines.
+__device__ const uint64_t kExp2fTabDev[32] = SIGE_EXP2F_TAB;
 #endif
 
 
@@ -125,7 +128,7 @@ SIGE_HD double dfma(double a, double b, double c) {
 }
 SIGE_HD uint64_t tab(uint32_t i) {
 #ifdef __CUDA_ARCH__
-  return kExp2fTabDev[i];
+  return __ldg(kExp2fTabDev + i);
 #else
   return kExp2fTabHost[i];
 #endif
