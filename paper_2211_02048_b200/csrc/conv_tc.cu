@@ -70,7 +70,7 @@ constexpr int kProdThreads = 128;  // warps 0-3: A producers
 constexpr int kEpiThreads = 128;   // warps 4-7: epilogue (TMEM lane quarter = warp % 4)
 constexpr int kThreads = kProdThreads + kEpiThreads + 64;  // + warp 8 (MMA), warp 9 (weight TMA)
 constexpr int kMaxNA = 4;          // A ring stages (max)
-constexpr int kMaxNB = 8;          // B (weight) ring stages (max)
+constexpr int kMaxNB = 16;         // B (weight) ring slots (max)
 constexpr int kMaxNTile = 256;     // accumulator columns per TMEM buffer
 constexpr int kTmemCols = 2 * kMaxNTile;  // two accumulators: epilogue of item i overlaps MMA of item i+1
 constexpr int kBatch = 4;          // 16-byte groups staged per thread per batch (synchronous path)
@@ -87,7 +87,7 @@ struct TcParams {
   int na, nb;     // A / B ring stages in use
   int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
   uint32_t lbo_a, idesc_base;
-  int a_bytes, b_stage_bytes;
+  int a_bytes, b_ring_bytes;  // A stage bytes; B ring bytes (slots sized per launch from the N tile)
   int tps[5];     // taps per weight stage for n_tile = 16, 32, 64, 128, 256
   unsigned long long* tl;  // debug timeline (SIGE_TC_TIMELINE), nullptr normally
   int dbg;                 // SIGE_TC_DEBUG bits (experiments only)
@@ -613,6 +613,48 @@ __device__ __forceinline__ int nt_index(int nt) {
   return nt <= 16 ? 0 : nt <= 32 ? 1 : nt <= 64 ? 2 : nt <= 128 ? 3 : 4;
 }
 
+// MMA-issue state shared by the unrolled chunk bodies (uniform across the warp).
+struct MmaCtx {
+  uint32_t a0, b0, lbo_a16, lbo_b16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
+  uint64_t adesc0, bdesc0;
+  uint64_t* bar_bfull;
+  uint64_t* bar_bempty;
+  uint32_t bslot = 0, bphase = 0;
+};
+
+// All MMAs of one K chunk: K*K taps x 4 k-steps, one weight stage per TPS taps.
+template <bool F16, int K, int S, int TPS>
+__device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_chunk) {
+  static_assert((K * K) % TPS == 0, "taps per stage must divide the tap count");
+#pragma unroll
+  for (int tg = 0; tg < K * K / TPS; ++tg) {
+    mbar_wait(&c.bar_bfull[c.bslot], c.bphase);
+    __syncwarp();
+    tc_fence_after();
+    const uint32_t bbase = c.b0 + c.bslot * c.bstage16;
+#pragma unroll
+    for (int tt = 0; tt < TPS; ++tt) {
+      const int tap = tg * TPS + tt;
+      const int ky = tap / K, kx = tap % K;
+      const uint32_t phase = S == 2 ? static_cast<uint32_t>(((ky & 1) << 1) | (kx & 1)) : 0u;
+      const uint32_t aoff = abase + phase * c.plane16 + static_cast<uint32_t>(ky / S) * c.P + static_cast<uint32_t>(kx / S);
+      const uint32_t boff = bbase + static_cast<uint32_t>(tt) * c.tap_b16;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
+        const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * 2 * c.lbo_a16) & 0x3FFFu);
+        const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2 * c.lbo_b16) & 0x3FFFu);
+        const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
+        if (elect_one()) umma<F16>(c.tmem_d, ad, bd, c.idesc, accum);
+      }
+    }
+    if (elect_one()) umma_commit(&c.bar_bempty[c.bslot]);
+    if (++c.bslot == c.nb) {
+      c.bslot = 0;
+      c.bphase ^= 1;
+    }
+  }
+}
+
 // Warp roles (320 threads, one CTA per SM, persistent over work items =
 // (group of T tiles, N slice)):
 //   warps 0-3  A producers: K chunk c of item i into A stage c % na (cp.async
@@ -631,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   uint8_t* abuf0 = smem;
   uint8_t* bbuf = smem + p.na * p.a_bytes;
-  int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.nb * p.b_stage_bytes);
+  int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.b_ring_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
@@ -640,8 +682,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int q = threadIdx.x; q < p.phases * p.T * p.Mt; q += blockDim.x) row_tab[q] = row_info(p, q);
 
+  // The live tile count (IndexPlan output, complete before the previous conv
+  // started) is the first dependent load: issue it before the setup work.
+  const int count = p.tiles.count_dev ? *p.tiles.count_dev : p.tiles.count;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < p.nb; ++i) {
+    for (int i = 0; i < kMaxNB; ++i) {
       mbar_init(&bar_bfull[i], 1);
       mbar_init(&bar_bempty[i], 1);
     }
@@ -668,8 +713,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) tl_mark(p, 1);
   // Tile lists / counts come from the IndexPlan, which finished before the
   // previous conv started; weights are static. Both are safe before the wait.
-  const int count = p.tiles.count_dev ? *p.tiles.count_dev : p.tiles.count;
   const int items_m = (count + p.T - 1) / p.T;
+  if (threadIdx.x == 0 && items_m >= 0) tl_mark(p, 48);
   const int n_tile = pick_n_tile(p, items_m);
   const int n_slices = p.n_pad / n_tile;
   const int n_items = items_m * n_slices;
@@ -679,11 +724,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lbo_b = static_cast<uint32_t>(n_tile * 16);
   const uint32_t tap_b = static_cast<uint32_t>(n_tile * 128);  // one tap of B in smem
   const uint32_t idesc = p.idesc_base | (static_cast<uint32_t>(n_tile >> 3) << 17);
+  // B ring: slots of one TMA stage (tps taps x n_tile rows x 128 B) each.
+  const uint32_t b_stage = static_cast<uint32_t>(tps) * tap_b;
+  const uint32_t nb = min(static_cast<uint32_t>(kMaxNB), static_cast<uint32_t>(p.b_ring_bytes) / b_stage);
   if (threadIdx.x == 0) pdl_trigger();  // the next layer may start its own setup
 
   if (warp < 4) {
     // ---------------- A producers ----------------
     pdl_wait();  // the source was written by the previous kernel
+    if (threadIdx.x == 0) tl_mark(p, 49);
     const uint32_t a0 = smem_u32(abuf0);
     uint32_t a_iter = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -697,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : make_int4(-1, 0, 0, 0);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+      if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
       const bool fast_units = F16 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off);
@@ -790,14 +840,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 8) {
     // ---------------- MMA issuer (whole warp, converged) ----------------
     // Descriptors are uniform: base descriptor with a zero start field plus
-    // the (stage, tap, k-step) offset in 16-byte units; the taps are unrolled
-    // at compile time (K, S), one elected lane issues each tcgen05.mma.
-    uint32_t a_iter = 0, b_iter = 0, it = 0;
-    const uint32_t a0 = smem_u32(abuf0) >> 4, b0 = smem_u32(bbuf) >> 4;
-    const uint64_t adesc0 = umma_desc(0, p.lbo_a, 128), bdesc0 = umma_desc(0, lbo_b, 128);
-    const uint32_t lbo_a16 = p.lbo_a >> 4, lbo_b16 = lbo_b >> 4, tap_b16 = tap_b >> 4;
-    const uint32_t plane16 = static_cast<uint32_t>(p.T * p.Mt), astage16 = static_cast<uint32_t>(p.a_bytes >> 4);
-    const uint32_t bstage16 = static_cast<uint32_t>(p.b_stage_bytes >> 4), P = static_cast<uint32_t>(p.P);
+    // the (stage, tap, k-step) offset in 16-byte units; taps are unrolled at
+    // compile time (K, S, taps per weight stage), ring slots advance by
+    // increments (no runtime divisions on the issue path), one elected lane
+    // issues each tcgen05.mma.
+    MmaCtx c;
+    c.a0 = smem_u32(abuf0) >> 4;
+    c.b0 = smem_u32(bbuf) >> 4;
+    c.adesc0 = umma_desc(0, p.lbo_a, 128);
+    c.bdesc0 = umma_desc(0, lbo_b, 128);
+    c.lbo_a16 = p.lbo_a >> 4;
+    c.lbo_b16 = lbo_b >> 4;
+    c.tap_b16 = tap_b >> 4;
+    c.plane16 = static_cast<uint32_t>(p.T * p.Mt);
+    c.bstage16 = b_stage >> 4;
+    c.P = static_cast<uint32_t>(p.P);
+    c.nb = nb;
+    c.idesc = idesc;
+    c.bar_bfull = bar_bfull;
+    c.bar_bempty = bar_bempty;
+    const uint32_t astage16 = static_cast<uint32_t>(p.a_bytes >> 4), na = static_cast<uint32_t>(p.na);
+    uint32_t aslot = 0, aphase = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       const uint32_t acc = it & 1;
       if (it >= 2) {
@@ -805,45 +868,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         tc_fence_after();
       }
-      const uint32_t tmem_d = taddr + acc * kMaxNTile;
-      for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
-        const uint32_t sidx = a_iter % static_cast<uint32_t>(p.na);
-        mbar_wait(&bar_afull[sidx], (a_iter / p.na) & 1);
+      c.tmem_d = taddr + acc * kMaxNTile;
+      for (int ch = 0; ch < p.nchunks; ++ch) {
+        mbar_wait(&bar_afull[aslot], aphase);
         __syncwarp();
         fence_proxy_async();
         tc_fence_after();
-        if (lane == 0 && it == 0 && ch == 0) tl_mark(p, 7);
         if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 22 + ch);
-        const uint32_t abase = a0 + sidx * astage16;
-        uint32_t st = 0, bbase = 0;
-#pragma unroll
-        for (int tap = 0; tap < K * K; ++tap) {
-          const int tt = tap % tps;
-          if (tt == 0) {
-            st = b_iter % static_cast<uint32_t>(p.nb);
-            mbar_wait(&bar_bfull[st], (b_iter / p.nb) & 1);
-            __syncwarp();
-            tc_fence_after();
-            if (lane == 0 && b_iter == 0) tl_mark(p, 8);
-            bbase = b0 + st * bstage16;
-          }
-          const int ky = tap / K, kx = tap % K;
-          const uint32_t phase = S == 2 ? static_cast<uint32_t>(((ky & 1) << 1) | (kx & 1)) : 0u;
-          const uint32_t aoff =
-              abase + phase * plane16 + static_cast<uint32_t>(ky / S) * P + static_cast<uint32_t>(kx / S);
-          const uint32_t boff = bbase + static_cast<uint32_t>(tt) * tap_b16;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
-            const uint64_t ad = adesc0 | static_cast<uint64_t>((aoff + kk * 2 * lbo_a16) & 0x3FFFu);
-            const uint64_t bd = bdesc0 | static_cast<uint64_t>((boff + kk * 2 * lbo_b16) & 0x3FFFu);
-            if (elect_one()) umma<F16>(tmem_d, ad, bd, idesc, (ch | tap | kk) != 0 ? 1u : 0u);
-          }
-          if (tt == tps - 1) {
-            if (elect_one()) umma_commit(&bar_bempty[st]);
-            ++b_iter;
-          }
+        const uint32_t abase = c.a0 + aslot * astage16;
+        if (tps == 9)
+          mma_chunk<F16, K, S, (K == 3 ? 9 : 1)>(c, abase, ch == 0);
+        else if (tps == 3)
+          mma_chunk<F16, K, S, (K == 3 ? 3 : 1)>(c, abase, ch == 0);
+        else
+          mma_chunk<F16, K, S, 1>(c, abase, ch == 0);
+        if (elect_one()) umma_commit(&bar_afree[aslot]);
+        if (++aslot == na) {
+          aslot = 0;
+          aphase ^= 1;
         }
-        if (elect_one()) umma_commit(&bar_afree[sidx]);
         if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 30 + ch);
       }
       if (elect_one()) umma_commit(&bar_acc_full[acc]);
@@ -854,17 +897,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const CUtensorMap* map = &maps.m[nti];
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-      uint32_t b_iter = 0;
+      uint32_t b_iter = 0, bslot = 0, bphase = 0;
       const uint32_t b0 = smem_u32(bbuf);
-      const uint32_t stage_bytes = static_cast<uint32_t>(tps) * tap_b;
+      const uint32_t stage_bytes = b_stage;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int ni = item % n_slices;
         for (int ch = 0; ch < p.nchunks; ++ch)
           for (int tg = 0; tg < tgroups; ++tg, ++b_iter) {
-            const int st = static_cast<int>(b_iter % p.nb);
-            if (b_iter >= static_cast<uint32_t>(p.nb)) mbar_wait(&bar_bempty[st], ((b_iter / p.nb) - 1) & 1);
+            const uint32_t st = bslot;
+            if (b_iter >= nb) mbar_wait(&bar_bempty[st], bphase ^ 1);
+            if (++bslot == nb) {
+              bslot = 0;
+              bphase ^= 1;
+            }
             mbar_expect_tx(&bar_bfull[st], stage_bytes);
-            tma_3d(b0 + st * p.b_stage_bytes, map, 0, ni * n_tile, (ch * p.ntaps + tg * tps) * 8, &bar_bfull[st]);
+            tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, (ch * p.ntaps + tg * tps) * 8, &bar_bfull[st]);
             if (b_iter == 0) tl_mark(p, 10);
           }
         if (item == static_cast<int>(blockIdx.x)) tl_mark(p, 11);
@@ -921,7 +968,7 @@ int n_pad_for(int c_out) { return c_out <= 128 ? (c_out + 15) / 16 * 16 : (c_out
 // Taps per weight stage for an N slice: small slices batch more taps per TMA.
 int tps_for(int n_tile, int ntaps) {
   if (ntaps == 1) return 1;
-  if (n_tile <= 16) return 9;
+  if (n_tile <= 32) return 9;  // a whole chunk (<= 36 KB) per TMA
   if (n_tile <= 64) return 3;
   return 1;
 }
@@ -1036,7 +1083,6 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   int max_stage = 0;
   const int sizes[5] = {16, 32, 64, 128, 256};
   for (int i = 0; i < 5; ++i) max_stage = std::max(max_stage, p.tps[i] * std::min(sizes[i], p.n_pad) * 128);
-  p.b_stage_bytes = (max_stage + 1023) / 1024 * 1024;
   p.min_items = sm_count();
   const uint32_t fmt = f16 ? 0u : 2u;
   p.idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(128 >> 4) << 24);
@@ -1051,18 +1097,20 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
                       p.src.c % unit_ch == 0 && p.src.half != 0
                   ? 1
                   : 0;
-  // Ring depths: as many A stages (<= 4) and weight stages (<= 8) as fit.
+  // Ring depths: up to 4 A stages, the rest of shared memory is the B ring
+  // (at least two of the largest weight stages).
   constexpr size_t kSmemBudget = 225 * 1024;
   const size_t fixed = sizeof(int32_t) * p.phases * p.T * p.Mt;
   p.na = kMaxNA;
-  p.nb = kMaxNB;
-  auto need = [&] { return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.nb) * p.b_stage_bytes; };
-  while (need() > kSmemBudget && (p.nb > 4 || (p.na == 2 && p.nb > 2))) --p.nb;
-  while (need() > kSmemBudget && p.na > 2) --p.na;
-  while (need() > kSmemBudget && p.nb > 2) --p.nb;
-  const size_t smem = need();
-  if (smem > kSmemBudget)
-    throw ConfigError("conv (tensor core): staging needs " + std::to_string(smem) + " B of shared memory");
+  auto b_room = [&] { return static_cast<long long>(kSmemBudget) - static_cast<long long>(fixed) -
+                             static_cast<long long>(p.na) * p.a_bytes; };
+  while (p.na > 2 && b_room() < 2LL * max_stage) --p.na;
+  if (b_room() < 2LL * max_stage)
+    throw ConfigError("conv (tensor core): staging needs " + std::to_string(fixed + p.na * p.a_bytes + 2 * max_stage) +
+                      " B of shared memory");
+  p.b_ring_bytes = static_cast<int>(std::min<long long>(b_room(), 16LL * max_stage) / 128 * 128);
+  p.nb = p.b_ring_bytes / max_stage;  // (report only; the device sizes slots per N tile)
+  const size_t smem = fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
   using KernelFn = void (*)(TcParams, TcMaps);
   KernelFn fn = nullptr;
   if (cw.k == 1)
@@ -1096,8 +1144,9 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
   after_launch("k_conv_tc");
   if (timeline) {
@@ -1121,7 +1170,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
         std::fprintf(stderr, "  cta%d clock: %.0f MHz\n", c,
                      double(h[c * 64 + 61] - h[c * 64 + 60]) / double(h[c * 64 + 12] - h[c * 64 + 0]) * 1e3);
       std::fprintf(stderr, "  cta%d:", c);
-      for (int e = 0; e < 48; ++e)
+      for (int e = 0; e < 56; ++e)
         if (h[c * 64 + e]) std::fprintf(stderr, " %d:%.2f", e, (static_cast<long long>(h[c * 64 + e]) - static_cast<long long>(t0)) * 1e-3);
       std::fprintf(stderr, "\n");
     }

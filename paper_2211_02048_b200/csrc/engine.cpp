@@ -376,6 +376,9 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     // algorithmic FLOPs per tile: 2 * C_out * C_in * k^2 * (pixels of the
     // tile inside the canvas ~ bh*bw; fringe clipping ignored)
     rec.flops_per_tile = 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * t.bh * t.bw;
+    if (!t.count_dev) {  // dense pass: the tiles clip at the canvas edge, count exact output pixels
+      rec.flops_per_tile = 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * dst.h * dst.w * dst.n / std::max(1, t.count);
+    }
     rec.tc = tensor_cores() ? 1 : 0;
     prof_.push_back(rec);
   }
