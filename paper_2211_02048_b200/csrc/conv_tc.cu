@@ -86,8 +86,11 @@ struct TcParams {
   int min_items;  // target number of work items (SM count)
   int na, nb;     // A / B ring stages in use
   int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
+  int xform;      // 1: async + in-shared-memory transform: [scale-shift (table), act] applied after landing
+  int xf_act;     // activation of the transform chain
+  int xf_table;   // floats per table (n * C) of the scale-shift table in shared memory
   uint32_t lbo_a, idesc_base;
-  int a_bytes, b_ring_bytes;  // A stage bytes; B ring bytes (slots sized per launch from the N tile)
+  int a_bytes, b_ring_bytes, xf_bytes;  // A stage bytes; B ring bytes (slots sized per launch from the N tile)
   int tps[5];     // taps per weight stage for n_tile = 16, 32, 64, 128, 256
   unsigned long long* tl;  // debug timeline (SIGE_TC_TIMELINE), nullptr normally
   int dbg;                 // SIGE_TC_DEBUG bits (experiments only)
@@ -348,13 +351,13 @@ __device__ __forceinline__ void stage_a_async(const TcParams& p, uint32_t abuf, 
 }
 
 // Per-item precompute of the asynchronous staging: each producer thread owns
-// units u = tid + 128 k (k < 8 covers every stride-1 geometry, <= 1024 units);
+// units u = tid + 128 k (k < 12 covers every stride-1 geometry, <= 1536 units);
 // the window pixel of a unit is fixed for the whole item, only the channel
 // chunk moves, so the per-chunk work is one add + one cp.async per unit.
-constexpr int kUnitRegs = 8;
+constexpr int kUnitRegs = 12;
 constexpr uint32_t kNoPix = 0xffffffffu;
 __device__ __forceinline__ void unit_pixels(const TcParams& p, const int32_t* row_tab, const int4* s_tile,
-                                            uint32_t (&pix_off)[kUnitRegs]) {
+                                            uint32_t (&pix_off)[kUnitRegs], int (&unit_n)[kUnitRegs]) {
   const Src& s = p.src;
   const int units = p.phases * p.T * p.Mt * 8;
   const int ph_h = s.h >> s.up, ph_w = s.w >> s.up;
@@ -370,6 +373,7 @@ __device__ __forceinline__ void unit_pixels(const TcParams& p, const int32_t* ro
     if (tl.x < 0 || y < 0 || y >= s.h || x < 0 || x >= s.w) continue;
     const size_t pix = (static_cast<size_t>(tl.x) * ph_h + (y >> s.up)) * ph_w + (x >> s.up);
     pix_off[k] = static_cast<uint32_t>(pix * s.c + (u & 7) * 8);  // element offset of the unit at chunk 0
+    unit_n[k] = tl.x;
   }
 }
 
@@ -385,6 +389,55 @@ __device__ __forceinline__ void stage_a_async_fast(const TcParams& p, uint32_t a
     const int cc = ch * 64 + (u & 7) * 8;
     const bool ok = pix_off[k] != kNoPix && cc < p.c_in;
     cp_async16(abuf + (u & 7) * p.lbo_a + (u >> 3) * 16, ok ? base + pix_off[k] + ch * 64 : base, ok ? 16u : 0u);
+  }
+}
+
+// In-shared-memory transform of the units of one landed chunk: the fp16
+// values of every unit that carries pixel data (never the zero fill, as
+// gather() leaves it, kernels.cpp:72-81) go through scale-shift (table of the
+// folded norm in shared memory, [n][C]) and the activation, back to fp16.
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Activation inside the transform: SiLU as x * (0.5 + 0.5 tanh(x / 2)) — one
+// MUFU op per value (the staged operand is fp16, far coarser than the
+// approximation).
+__device__ __forceinline__ float xf_act(float v, int kind) {
+  if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;
+  if (kind == SIGE_ACT_SILU) return v * fmaf(0.5f, tanh_approx(0.5f * v), 0.5f);
+  return v;
+}
+
+__device__ __forceinline__ void xform_chunk(const TcParams& p, uint8_t* abuf, int ch,
+                                            const uint32_t (&pix_off)[kUnitRegs], const int (&unit_n)[kUnitRegs],
+                                            const float* xf_scale, const float* xf_shift) {
+  const int units = p.phases * p.T * p.Mt * 8;
+  const int C = p.src.c;
+  const int act = p.xf_act;
+#pragma unroll
+  for (int k = 0; k < kUnitRegs; ++k) {
+    const int u = threadIdx.x + k * kProdThreads;
+    if (u >= units) break;
+    const int cc = ch * 64 + (u & 7) * 8;
+    if (pix_off[k] == kNoPix || cc >= p.c_in) continue;
+    uint4* at = reinterpret_cast<uint4*>(abuf + (u & 7) * p.lbo_a + (u >> 3) * 16);
+    uint4 raw = *at;
+    __half2* h = reinterpret_cast<__half2*>(&raw);
+    const float4* sc4 = reinterpret_cast<const float4*>(xf_scale + unit_n[k] * C + cc);
+    const float4* sh4 = reinterpret_cast<const float4*>(xf_shift + unit_n[k] * C + cc);
+    const float4 s0 = sc4[0], s1 = sc4[1], t0 = sh4[0], t1 = sh4[1];
+    const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    const float sh[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(h[j]);
+      h[j] = __floats2half2_rn(xf_act(fmaf(sc[2 * j], f.x, sh[2 * j]), act),
+                               xf_act(fmaf(sc[2 * j + 1], f.y, sh[2 * j + 1]), act));
+    }
+    *at = raw;
   }
 }
 
@@ -486,7 +539,7 @@ __device__ __forceinline__ void stage_a_sync(const TcParams& p, uint8_t* abuf, i
 // passed by value: a reference into the __grid_constant__ parameters would
 // make every field access a generic load from parameter space.
 __device__ __noinline__ void out_slow(const Dst d, const float* bias, int c_out, size_t pix, int n, int y, int x,
-                                      int oc0, const float* vin, int cnt) {
+                                      int oc0, float* vin, int cnt) {
   const size_t at = pix + oc0;
   float* o = d.ptr + at;
   for (int j = 0; j < cnt; ++j) {
@@ -508,6 +561,7 @@ __device__ __noinline__ void out_slow(const Dst d, const float* bias, int c_out,
         break;
     }
     o[j] = w;
+    vin[j] = w;  // the written value (GroupNorm statistics)
     if (d.act) {
       const float a = tc_epi(d.act_epi, w, oc0 + j, d.c, n);
       if (d.act_half)
@@ -531,7 +585,8 @@ __device__ __forceinline__ void st4(float* p, const float* v) {
 // destination carries an activation buffer, act = chain(written value) —
 // the consumer's pending GroupNorm scale-shift + activation evaluated once
 // per output pixel. One vector path; everything else goes out of line.
-__device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v) {
+__device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v,
+                                      float* written) {
   const Dst& d = p.dst;
   const int cnt = min(16, p.c_out - oc0);
   if (cnt <= 0) return;
@@ -539,6 +594,8 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
                                                 d.addend.epi.num_steps == 0 && (d.addend.c & 3) == 0);
   if (cnt < 16 || (d.c & 3) != 0 || !addend_vec) {
     out_slow(d, p.bias, p.c_out, pix, n, y, x, oc0, v, cnt);
+    if (d.gn_stats)
+      for (int j = 0; j < 16; ++j) written[j] = j < cnt ? v[j] : 0.0f;
     return;
   }
   const size_t at = pix + oc0;
@@ -572,6 +629,10 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
   }
 #pragma unroll
   for (int j = 0; j < 16; j += 4) st4(o + j, v + j);
+  if (d.gn_stats) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) written[j] = v[j];
+  }
   if (d.act) {
     tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
     if (d.act_half) {
@@ -582,6 +643,45 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
 #pragma unroll
       for (int j = 0; j < 16; j += 4) st4(static_cast<float*>(d.act) + at + j, v + j);
     }
+  }
+}
+
+// GroupNorm statistics of 16 written channels oc0.. of this lane's pixel
+// (w = 0 for rows without a pixel): per group, a warp reduction of (sum,
+// sum of squares) in doubles, then one atomicAdd per (n, group) per warp —
+// or per lane when the warp's rows belong to several samples.
+__device__ __forceinline__ void gn_accumulate(const Dst& d, int c_out, int oc0, int n, bool valid, const float* w) {
+  const int cpg = d.c / d.gn_groups;
+  const int lane = threadIdx.x & 31;
+  const int n0 = __shfl_sync(0xffffffffu, n, 0);
+  const bool uniform_n = __all_sync(0xffffffffu, !valid || n == n0);
+  if (!__any_sync(0xffffffffu, valid)) return;
+  for (int j0 = 0; j0 < 16 && oc0 + j0 < c_out;) {
+    const int g = (oc0 + j0) / cpg;
+    const int j1 = min(16, min(c_out - oc0, (g + 1) * cpg - oc0));  // channels j0..j1-1 are group g
+    // fp32 partials over <= 16 values x 32 rows; the arena accumulates in doubles.
+    float a = 0.0f, q = 0.0f;
+    if (valid)
+      for (int j = j0; j < j1; ++j) {
+        a += w[j];
+        q = fmaf(w[j], w[j], q);
+      }
+    double* slot = d.gn_stats + 2 * (static_cast<size_t>(valid ? n : n0) * d.gn_groups + g);
+    if (uniform_n) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        q += __shfl_xor_sync(0xffffffffu, q, o);
+      }
+      if (lane == 0) {
+        atomicAdd(slot, static_cast<double>(a));
+        atomicAdd(slot + 1, static_cast<double>(q));
+      }
+    } else if (valid) {
+      atomicAdd(slot, static_cast<double>(a));
+      atomicAdd(slot + 1, static_cast<double>(q));
+    }
+    j0 = j1;
   }
 }
 
@@ -673,7 +773,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   uint8_t* abuf0 = smem;
   uint8_t* bbuf = smem + p.na * p.a_bytes;
-  int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.b_ring_bytes);
+  float* xf_scale = reinterpret_cast<float*>(bbuf + p.b_ring_bytes);  // [n][C] (transform mode)
+  float* xf_shift = xf_scale + p.xf_table;
+  int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.b_ring_bytes + p.xf_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
@@ -734,6 +836,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();  // the source was written by the previous kernel
     if (threadIdx.x == 0) tl_mark(p, 49);
     const uint32_t a0 = smem_u32(abuf0);
+    if (p.xform) {
+      // Scale-shift table of the transform: folded from GroupNorm statistics
+      // (written by the previous conv's epilogue) or copied from the chain.
+      const Src& s = p.src;
+      for (int i = threadIdx.x; i < p.xf_table; i += kProdThreads) {
+        const int n = i / s.c, c = i - n * s.c;
+        float sc, sh;
+        if (s.gn_stats) {
+          const int g = c / (s.c / s.gn_groups);
+          const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + g);
+          const double mean = st[0] / s.gn_count;
+          double var = st[1] / s.gn_count - mean * mean;
+          if (var < 0.0) var = 0.0;
+          sc = __fdiv_rn(__ldg(s.gn_gamma + c), __fsqrt_rn(__fadd_rn(static_cast<float>(var), s.gn_eps)));
+          sh = __fsub_rn(__ldg(s.gn_beta + c), __fmul_rn(static_cast<float>(mean), sc));
+        } else {
+          const int off = s.epi.per_sample[0] ? i : c;
+          sc = __ldg(s.epi.scale[0] + off);
+          sh = __ldg(s.epi.shift[0] + off);
+        }
+        xf_scale[i] = sc;
+        xf_shift[i] = sh;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+    }
     uint32_t a_iter = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       const int mi = item / n_slices;
@@ -748,27 +875,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
+      int unit_n[kUnitRegs];
       const bool fast_units = F16 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
-      if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off);
+      if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
-      for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
-        const int sidx = static_cast<int>(a_iter % p.na);
-        if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
-        if (p.async_a) {
-          // The arrival fires when this thread's copies have landed, so the
-          // producers run ahead to the next free stage without waiting.
-          if (fast_units)
+      if (p.xform) {
+        // Async copy of chunk c, then transform of chunk c-1 (landed: this
+        // thread's copies are complete after wait_group 1, the other
+        // producers' after the named barrier), fence, arrive. Drained at the
+        // end of the item (the unit tables are per item).
+        int prev_sidx = -1;
+        for (int ch = 0; ch <= p.nchunks; ++ch) {
+          int sidx = -1;
+          if (ch < p.nchunks) {
+            sidx = static_cast<int>(a_iter % p.na);
+            if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
             stage_a_async_fast(p, a0 + sidx * p.a_bytes, ch, pix_off);
-          else
-            stage_a_async<F16>(p, a0 + sidx * p.a_bytes, ch, row_tab, s_tile);
-          cp_async_arrive(&bar_afull[sidx]);
-        } else {
-          stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
-          fence_proxy_async();
-          mbar_arrive(&bar_afull[sidx]);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            ++a_iter;
+          }
+          if (prev_sidx >= 0) {
+            if (ch < p.nchunks)
+              asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else
+              asm volatile("cp.async.wait_group 0;" ::: "memory");
+            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, pix_off, unit_n, xf_scale, xf_shift);
+            fence_proxy_async();
+            mbar_arrive(&bar_afull[prev_sidx]);
+          }
+          prev_sidx = sidx;
         }
-        if (threadIdx.x == 0 && it == 0 && ch == 0) tl_mark(p, 3);
-        if (threadIdx.x == 0 && it == 0 && ch < 8) tl_mark(p, 14 + ch);
+      } else {
+        for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
+          const int sidx = static_cast<int>(a_iter % p.na);
+          if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
+          if (p.async_a) {
+            // The arrival fires when this thread's copies have landed, so the
+            // producers run ahead to the next free stage without waiting.
+            if (fast_units)
+              stage_a_async_fast(p, a0 + sidx * p.a_bytes, ch, pix_off);
+            else
+              stage_a_async<F16>(p, a0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+            cp_async_arrive(&bar_afull[sidx]);
+          } else {
+            stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+            fence_proxy_async();
+            mbar_arrive(&bar_afull[sidx]);
+          }
+          if (threadIdx.x == 0 && it == 0 && ch < 8) tl_mark(p, 14 + ch);
+        }
       }
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 4);
     }
@@ -830,7 +985,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[16];
         tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
         if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
-        if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v);
+        float wv[16];
+        if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v, wv);
+        if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + cb, n, valid, wv);
       }
       if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 47);
       tc_fence_before();
@@ -1030,7 +1187,19 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   if (tiles.capacity == 0) return;
   TcParams p{};
   p.src = src;
-  if (f16 && src.twin && src.epi.num_steps == 0 && src.layout == kNHWC && !src.half) {
+  // Transform mode (F16): the fp16 twin streams by cp.async and the pending
+  // chain — [scale-shift, act] or GroupNorm-from-statistics then act — is
+  // applied in shared memory after the copy lands.
+  const DevEpilogue& e = src.epi;
+  const bool chain_ok =
+      src.gn_stats ? (e.num_steps == 0 || (e.num_steps == 1 && e.kind[0] == SIGE_EPI_ACTIVATION))
+                   : (e.num_steps >= 1 && e.num_steps <= 2 && e.kind[0] == SIGE_EPI_SCALE_SHIFT &&
+                      (e.num_steps == 1 || e.kind[1] == SIGE_EPI_ACTIVATION));
+  const bool twin_ok = f16 && src.twin && src.layout == kNHWC && !src.half && src.c == cw.c_in && src.c % 8 == 0;
+  bool xform = twin_ok && chain_ok && cw.stride == 1 && static_cast<long long>(src.n) * src.c <= 4096;
+  if (src.gn_stats && !xform)
+    throw ConfigError("conv (tensor core): GroupNorm-from-statistics source needs the F16 transform path");
+  if (twin_ok && (e.num_steps == 0 || xform)) {
     p.src.ptr = static_cast<const float*>(src.twin);  // stream the fp16 twin
     p.src.half = 1;
   }
@@ -1093,14 +1262,29 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   // 1e-2 bar), so TF32 stages synchronously with cvt.rna like every
   // converting / chained source.
   const int unit_ch = f16 ? 8 : 4;
-  p.async_a = f16 && p.src.layout == kNHWC && p.src.epi.num_steps == 0 && p.src.c == cw.c_in &&
+  p.async_a = f16 && p.src.layout == kNHWC && (p.src.epi.num_steps == 0 || xform) && p.src.c == cw.c_in &&
                       p.src.c % unit_ch == 0 && p.src.half != 0
                   ? 1
                   : 0;
+  if (xform && p.phases * p.T * p.Mt * 8 > kUnitRegs * kProdThreads) {
+    if (src.gn_stats)
+      throw ConfigError("conv (tensor core): tile too large for the GroupNorm-from-statistics transform");
+    xform = false;  // synchronous staging applies the chain instead
+    p.async_a = 0;
+    p.src = src;
+  }
+  p.xform = xform ? 1 : 0;
+  p.xf_act = SIGE_ACT_NONE;
+  if (xform) {
+    for (int i = 0; i < e.num_steps; ++i)
+      if (e.kind[i] == SIGE_EPI_ACTIVATION) p.xf_act = e.act[i];
+    p.xf_table = src.n * src.c;
+  }
+  p.xf_bytes = xform ? (2 * p.xf_table * 4 + 127) / 128 * 128 : 0;
   // Ring depths: up to 4 A stages, the rest of shared memory is the B ring
   // (at least two of the largest weight stages).
   constexpr size_t kSmemBudget = 225 * 1024;
-  const size_t fixed = sizeof(int32_t) * p.phases * p.T * p.Mt;
+  const size_t fixed = sizeof(int32_t) * p.phases * p.T * p.Mt + p.xf_bytes;
   p.na = kMaxNA;
   auto b_room = [&] { return static_cast<long long>(kSmemBudget) - static_cast<long long>(fixed) -
                              static_cast<long long>(p.na) * p.a_bytes; };

@@ -94,6 +94,8 @@ struct Program {
   int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
   int launches = 0;
   bool ran = false;
+  double* stats = nullptr;  // GroupNorm statistics arena (fused dense-fallback ResBlocks), zeroed per call
+  size_t stats_len = 0, stats_used = 0;
   std::map<std::tuple<const void*, const void*, const void*>, std::pair<cudaGraphExec_t, int>> graphs;
   ~Program() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
@@ -225,6 +227,31 @@ bool Engine::wants_twin(const std::string& key, int layout, int half) const {
 
 void Engine::attach_twin(DevTensor& t, const std::string& key) {
   if (wants_twin(key, t.layout, t.half) && !t.h16) t.h16 = alloc(t.numel() * 2);
+}
+
+void Engine::force_twin(DevTensor& t) {
+  if (math_ == SIGE_MATH_F16 && t.layout == kNHWC && !t.half && !t.h16) t.h16 = alloc(t.numel() * 2);
+}
+
+size_t Engine::stats_len() const {
+  size_t n = 0;
+  for (const LayerDev& L : layers_)
+    if (L.kind == SIGE_LAYER_RESBLOCK && L.norm_kind != SIGE_NORM_BATCH) n += 2 * static_cast<size_t>(batch_) * L.groups;
+  return n;
+}
+
+// Src / Dst wiring of a fused-statistics ResBlock: conv1 writes m1 (+ fp16
+// twin) and accumulates GroupNorm statistics of m1; conv2 stages the twin and
+// applies norm (folded from the statistics) + act in shared memory.
+static void wire_fused_gn(const LayerDev& L, const DevTensor& m1, double* stats, Dst& d1, Src& mid) {
+  d1.gn_stats = stats;
+  d1.gn_groups = L.groups;
+  mid.gn_stats = stats;
+  mid.gn_groups = L.groups;
+  mid.gn_eps = L.eps;
+  mid.gn_count = static_cast<double>(m1.c / L.groups) * m1.h * m1.w;
+  mid.gn_gamma = L.gamma;
+  mid.gn_beta = L.beta;
 }
 
 DevTensor& Engine::cache_slot(int step, const std::string& key, int c, int h, int w, int layout, int half) {
@@ -460,6 +487,14 @@ void Engine::invalidate_programs() {
 void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
                         cudaStream_t st) {
   Src x = input;
+  size_t dense_stats_used = 0;
+  if (!capture && !reused && math_ == SIGE_MATH_F16) {
+    if (!dense_stats_) {
+      dense_stats_len_ = std::max<size_t>(stats_len(), 1);
+      dense_stats_ = static_cast<double*>(alloc(dense_stats_len_ * sizeof(double)));
+    }
+    SIGE_CUDA(cudaMemsetAsync(dense_stats_, 0, dense_stats_len_ * sizeof(double), st));
+  }
   for (size_t i = 0; i < layers_.size(); ++i) {
     const LayerDev& L = layers_[i];
     const LayerShape& sh = shapes_[i];
@@ -495,6 +530,27 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         break;
       case SIGE_LAYER_RESBLOCK: {
         const int c1 = L.conv.c_out, co = L.conv2.c_out, h = sh.h_in, w = sh.w_in;
+        if (!capture && !reused && fused_gn(L)) {
+          // conv1 (+ statistics) -> [shortcut] -> conv2 (norm + act in smem) with the join add(m, sc).
+          DevTensor& m1 = scratch("dense." + key + ".conv1.out", c1, h, w, kNHWC);
+          force_twin(m1);
+          double* stats = dense_stats_ + dense_stats_used;
+          dense_stats_used += 2 * static_cast<size_t>(batch_) * L.groups;
+          Dst d1 = to_dst(m1);
+          Src mid = plain(m1);
+          wire_fused_gn(L, m1, stats, d1, mid);
+          epi_push_act(mid.epi, L.act);
+          conv(x, dense_tiles(h, w, 3, 1), L.conv, d1, st);
+          DevTensor& sc = scratch("dense." + key + ".shortcut.out", co, h, w, kNHWC);
+          if (L.has_shortcut)
+            conv(x, dense_tiles(h, w, 1, 1), L.shortcut, to_dst(sc), st);
+          DevTensor& sum = scratch("dense." + key + ".sum", co, h, w, kNHWC);
+          Dst d = to_dst(sum, kAddSrc);
+          d.addend = L.has_shortcut ? plain(sc) : x;
+          conv(mid, dense_tiles(h, w, 3, 1), L.conv2, d, st);
+          x = plain(sum);
+          break;
+        }
         DevTensor& m1 = capture ? cache_slot(step, key + ".conv1.out", c1, h, w, kNHWC)
                                 : scratch("dense." + key + ".conv1.out", c1, h, w, kNHWC);
         conv(x, dense_tiles(h, w, 3, 1), L.conv, to_dst(m1), st);
@@ -833,7 +889,41 @@ struct ProgramBuilder {
         case SIGE_LAYER_RESBLOCK: {
           const int h = flow.h, w = flow.w, c1 = L.conv.c_out, co = L.conv2.c_out;
           Src x0 = flow;
-          if (!runs_sparse(L, h, w, cfg)) {
+          if (!runs_sparse(L, h, w, cfg) && E.fused_gn(L)) {
+            // Dense fallback (graph.cpp:799-815), fresh statistics: conv1's
+            // epilogue accumulates them, conv2 folds + applies norm/act in smem.
+            DevTensor& m1 = E.scratch("sparse." + key + ".conv1", c1, h, w, kNHWC);
+            E.force_twin(m1);
+            DevTensor& o = E.scratch("sparse." + key + ".sum", co, h, w, kNHWC);
+            double* stats = P.stats + P.stats_used;
+            P.stats_used += 2 * static_cast<size_t>(N) * L.groups;
+            Dst d1 = to_dst(m1);
+            Src mid = plain(m1);
+            wire_fused_gn(L, m1, stats, d1, mid);
+            epi_push_act(mid.epi, L.act);
+            Tiles t = E.dense_tiles(h, w, 3, 1), t1 = E.dense_tiles(h, w, 1, 1);
+            ConvW c1w = L.conv, c2w = L.conv2, scw = L.shortcut;
+            DevTensor scc{};
+            if (L.has_shortcut) scc = E.scratch("sparse." + key + ".shortcut", co, h, w, kNHWC);
+            Dst d = to_dst(o, kAddSrc);
+            const bool has_sc = L.has_shortcut != 0;
+            add([eng, x0, t, t1, c1w, c2w, scw, d1, mid, d, scc, has_sc, fin, bind](cudaStream_t st) {
+              Src xin = bind(x0, fin);
+              eng->conv(xin, t, c1w, d1, st);
+              Dst dd = d;
+              if (has_sc) {
+                eng->conv(xin, t1, scw, to_dst(scc), st);
+                dd.addend = plain(scc);
+              } else {
+                dd.addend = xin;
+              }
+              eng->conv(mid, t, c2w, dd, st);
+            }, L.has_shortcut ? 3 : 2);
+            P.trace.push_back({-1, L.conv.c_in, c1, 3, 1, h, w, N});
+            P.trace.push_back({-1, c1, co, 3, 1, h, w, N});
+            if (L.has_shortcut) P.trace.push_back({-1, L.shortcut.c_in, co, 1, 1, h, w, N});
+            flow = plain(o);
+          } else if (!runs_sparse(L, h, w, cfg)) {
             // Dense fallback (graph.cpp:799-815): fresh statistics always.
             DevTensor& m1 = E.scratch("sparse." + key + ".conv1", c1, h, w, kNHWC);
             DevTensor& o = E.scratch("sparse." + key + ".sum", co, h, w, kNHWC);
@@ -979,6 +1069,8 @@ Program& Engine::program(const sige_run_config& cfg) {
   P->dilate_scale = cfg.dilate_scale;
   P->bits = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * in_h_ * ((in_w_ + 31) / 32)));
   P->any = static_cast<int32_t*>(alloc(sizeof(int32_t)));
+  P->stats_len = std::max<size_t>(stats_len(), 1);
+  P->stats = static_cast<double*>(alloc(P->stats_len * sizeof(double)));
   ProgramBuilder b{*this, *P, cfg, {}};
   b.build();
   if (!P->entries.empty()) {
@@ -1056,6 +1148,7 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
 void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
                          const sige_run_config& cfg, cudaStream_t st) {
   SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
+  if (P.stats_used) SIGE_CUDA(cudaMemsetAsync(P.stats, 0, P.stats_used * sizeof(double), st));
   if (mask) {
     launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st);
   } else {

@@ -101,6 +101,17 @@ class Engine {
   // producing kernel's epilogue.
   bool wants_twin(const std::string& key, int layout, int half) const;
   void attach_twin(DevTensor& t, const std::string& key);
+  void force_twin(DevTensor& t);
+  // F16 + GroupNorm/InstanceNorm ResBlocks with fresh statistics (dense
+  // fallback, dense_forward): conv1's epilogue accumulates the statistics,
+  // conv2 folds them and applies norm + act to its staged window in shared
+  // memory (no separate statistics / fold / activation kernels).
+  bool fused_gn(const LayerDev& L) const {
+    return math_ == SIGE_MATH_F16 && L.norm_kind != SIGE_NORM_BATCH;
+  }
+  double* dense_stats_ = nullptr;  // statistics arena of dense walks (zeroed per walk)
+  size_t dense_stats_len_ = 0;
+  size_t stats_len() const;        // doubles needed by all ResBlocks of the model
   DevNorm& norm_slot(int step, const std::string& key, int np);
   DevTensor& work_buffer(int step, const std::string& key);
   DevTensor& scratch(const std::string& key, int c, int h, int w, int layout, int half = 0);

@@ -31,6 +31,16 @@ struct Src {
   // fp16 channels-last copy of the same values (F16 mode): the tensor-core
   // conv streams it with cp.async when no element-wise chain is pending.
   const void* twin = nullptr;
+  // GroupNorm folded from raw statistics (F16 dense-fallback ResBlocks): when
+  // gn_stats != nullptr the chain is [scale-shift from (sum, sum of squares)
+  // per (n, group) in doubles, then `epi`]; scale = gamma / sqrt(var + eps),
+  // shift = beta - mean * scale (fold_stats, norm.cpp:66-90).
+  const double* gn_stats = nullptr;
+  int gn_groups = 0;
+  float gn_eps = 0.0f;
+  double gn_count = 0.0;  // values per (n, group)
+  const float* gn_gamma = nullptr;
+  const float* gn_beta = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -68,6 +78,11 @@ struct Dst {
   void* act = nullptr;
   int act_half = 0;
   DevEpilogue act_epi;
+  // Optional GroupNorm statistics of the written values: += (sum, sum of
+  // squares) per (n, group) into gn_stats[2 * (n * gn_groups + g)] (doubles,
+  // zeroed by the caller) — the next layer folds them (Src::gn_stats).
+  double* gn_stats = nullptr;
+  int gn_groups = 0;
 };
 
 // The tile list a conv runs over: `count` triplets {n, r, c} (output-res
