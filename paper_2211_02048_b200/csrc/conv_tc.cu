@@ -84,6 +84,9 @@ struct TcParams {
   int n_pad, nchunks, ntaps, phases;
   int P, Mt, T, win_h, win_w;
   int min_items;  // target number of work items (SM count)
+  int ks;         // split-K factor = cluster size (1: no cluster); K chunks split over the cluster's CTAs
+  int nt_fixed;   // N tile chosen on the host (static tile counts), 0: chosen on the device
+  int red_bytes;  // split-K reduction buffer: (ks-1) x 128 rows x (n_tile/ks) fp32
   int na, nb;     // A / B ring stages in use
   int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
   int xform;      // 1: async + in-shared-memory transform: [scale-shift (table), act] applied after landing
@@ -151,6 +154,49 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 // The mbarrier receives one arrival when all prior cp.async of this thread landed.
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t raddr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(raddr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_cluster_v4(uint32_t raddr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(raddr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  uint32_t done = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (!done && ++spins > (1u << 24)) __trap();
+  } while (!done);
 }
 
 __device__ __forceinline__ void prefetch_l1(const void* p) {
@@ -768,6 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[kMaxNA], bar_afree[kMaxNA];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
+  __shared__ __align__(8) uint64_t bar_red_full, bar_red_empty;  // split-K reduce-scatter (ks > 1)
   __shared__ uint32_t tmem_base;
   __shared__ int4 s_tile[16];  // producers' current item tiles: (n, window origin y, x, -); n = -1 empty slot
 
@@ -776,6 +823,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* xf_scale = reinterpret_cast<float*>(bbuf + p.b_ring_bytes);  // [n][C] (transform mode)
   float* xf_shift = xf_scale + p.xf_table;
   int32_t* row_tab = reinterpret_cast<int32_t*>(bbuf + p.b_ring_bytes + p.xf_bytes);
+  float* red_buf = reinterpret_cast<float*>(bbuf + p.b_ring_bytes + p.xf_bytes +
+                                            ((sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128) * 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
@@ -800,6 +849,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_acc_full[i], 1);
       mbar_init(&bar_acc_empty[i], kEpiThreads);
     }
+    mbar_init(&bar_red_full, (p.ks - 1) * (kEpiThreads / 32));   // one lane per epilogue warp of every sender
+    mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 8) {
@@ -810,6 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.ks > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t taddr = tmem_base;
   if (threadIdx.x == 0) tl_mark(p, 1);
@@ -817,7 +869,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // previous conv started; weights are static. Both are safe before the wait.
   const int items_m = (count + p.T - 1) / p.T;
   if (threadIdx.x == 0 && items_m >= 0) tl_mark(p, 48);
-  const int n_tile = pick_n_tile(p, items_m);
+  const int n_tile = p.nt_fixed ? p.nt_fixed : pick_n_tile(p, items_m);
+  // Split-K: the cluster's CTAs share each item, CTA `rank` runs K chunks
+  // [c_begin, c_end) and owns output columns [rank, rank + 1) * n_tile / ks.
+  const int rank = p.ks > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const int cid = blockIdx.x / p.ks, ncl = gridDim.x / p.ks;
+  const int c_begin = rank * p.nchunks / p.ks, c_end = (rank + 1) * p.nchunks / p.ks;
   const int n_slices = p.n_pad / n_tile;
   const int n_items = items_m * n_slices;
   const int nti = nt_index(n_tile);
@@ -862,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
     }
     uint32_t a_iter = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int item = cid; item < n_items; item += ncl, ++it) {
       const int mi = item / n_slices;
       const int g0 = mi * p.T, nt = min(p.T, count - g0);
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));  // previous item's s_tile readers done
@@ -885,9 +942,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // producers' after the named barrier), fence, arrive. Drained at the
         // end of the item (the unit tables are per item).
         int prev_sidx = -1;
-        for (int ch = 0; ch <= p.nchunks; ++ch) {
+        for (int ch = c_begin; ch <= c_end; ++ch) {
           int sidx = -1;
-          if (ch < p.nchunks) {
+          if (ch < c_end) {
             sidx = static_cast<int>(a_iter % p.na);
             if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
             stage_a_async_fast(p, a0 + sidx * p.a_bytes, ch, pix_off);
@@ -895,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++a_iter;
           }
           if (prev_sidx >= 0) {
-            if (ch < p.nchunks)
+            if (ch < c_end)
               asm volatile("cp.async.wait_group 1;" ::: "memory");
             else
               asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -906,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           prev_sidx = sidx;
         }
       } else {
-        for (int ch = 0; ch < p.nchunks; ++ch, ++a_iter) {
+        for (int ch = c_begin; ch < c_end; ++ch, ++a_iter) {
           const int sidx = static_cast<int>(a_iter % p.na);
           if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
           if (p.async_a) {
@@ -937,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t = m / p.Mt, rr = m - t * p.Mt;
     const int oy = rr / p.P, ox = rr - oy * p.P;
     uint32_t it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int item = cid; item < n_items; item += ncl, ++it) {
       const int mi = item / n_slices, ni = item % n_slices;
       const int g = mi * p.T + t;
       bool valid = t < p.T && g < count && oy < p.tiles.bh && ox < p.tiles.bw;
@@ -952,8 +1009,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // While the MMAs run: pull this item's per-channel params (bias, the act
       // chain's scale/shift) and this row's residual operand into L1, so the
       // epilogue's loads hit instead of paying an L2 round trip each.
+      const int slice = n_tile / p.ks, own0 = rank * slice;  // this CTA's output columns within the item
       {
-        const int oc0 = ni * n_tile, nb = n_tile * 4;  // bytes of one slice of per-channel floats
+        const int oc0 = ni * n_tile + own0, nb = slice * 4;  // bytes of one slice of per-channel floats
         const int lines = (nb + 127) / 128;
         int li = threadIdx.x - kProdThreads;
         if (p.bias && li < lines) prefetch_l1(p.bias + oc0 + li * 32);
@@ -981,13 +1039,76 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 5);
       const uint32_t tbase = taddr + (static_cast<uint32_t>(q * 32) << 16) + acc * kMaxNTile;
-      for (int cb = 0; cb < n_tile; cb += 16) {
-        float v[16];
-        tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
-        if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
-        float wv[16];
-        if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v, wv);
-        if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + cb, n, valid, wv);
+      if (p.ks == 1) {
+        for (int cb = 0; cb < n_tile; cb += 16) {
+          float v[16];
+          tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
+          if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
+          float wv[16];
+          if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v, wv);
+          if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + cb, n, valid, wv);
+        }
+      } else {
+        // Split-K reduce-scatter over DSMEM: every CTA parks the partial
+        // columns each peer owns in its own shared memory (slot d-1 for the
+        // owner at distance d; layout [slot][16-col block][float4 j][row], so
+        // a warp's accesses are contiguous), signals the owners, then sums
+        // the partials of its own columns in rank order (deterministic),
+        // reading the peers' slots remotely, and runs the epilogue on them.
+        if (it > 0) mbar_wait_cluster(&bar_red_empty, (it - 1) & 1);  // owners read the previous item
+        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 53);
+        const int blocks = slice / 16;
+        for (int d = 1; d < p.ks; ++d) {
+          const int owner = (rank + d) % p.ks;
+          float4* slot = reinterpret_cast<float4*>(red_buf) + static_cast<size_t>(d - 1) * blocks * 4 * 128;
+          for (int b = 0; b < blocks; ++b) {
+            float v[16];
+            tmem_ld16(tbase + static_cast<uint32_t>(owner * slice + b * 16), v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              slot[(b * 4 + j) * 128 + m] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+        // __syncwarp orders the warp's stores before lane 0's cluster-scope release.
+        __syncwarp();
+        if (lane == 0)
+          for (int d = 1; d < p.ks; ++d)
+            mbar_arrive_remote(mapa(smem_u32(&bar_red_full), static_cast<uint32_t>((rank + d) % p.ks)));
+        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 51);
+        mbar_wait_cluster(&bar_red_full, it & 1);
+        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 52);
+        const uint32_t red0 = smem_u32(red_buf);
+        for (int b = 0; b < blocks; ++b) {
+          float tot[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) tot[j] = 0.0f;
+          for (int r2 = 0; r2 < p.ks; ++r2) {  // rank order
+            if (r2 == rank) {
+              float v[16];
+              tmem_ld16(tbase + static_cast<uint32_t>(own0 + b * 16), v);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) tot[j] += v[j];
+            } else {
+              const int d = (rank - r2 + p.ks) % p.ks;  // distance from peer r2 to this owner
+              const uint32_t base = mapa(red0, static_cast<uint32_t>(r2)) +
+                                    static_cast<uint32_t>((((d - 1) * blocks + b) * 4 * 128 + m) * 16);
+              float4 f[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) f[j] = ld_cluster_v4(base + j * 128 * 16);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                tot[4 * j] += f[j].x, tot[4 * j + 1] += f[j].y, tot[4 * j + 2] += f[j].z, tot[4 * j + 3] += f[j].w;
+              }
+            }
+          }
+          float wv[16];
+          if (valid) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv);
+          if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + own0 + b * 16, n, valid, wv);
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int d = 1; d < p.ks; ++d)  // this owner is done with the peers' slots
+            mbar_arrive_remote(mapa(smem_u32(&bar_red_empty), static_cast<uint32_t>((rank - d + p.ks) % p.ks)));
       }
       if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 47);
       tc_fence_before();
@@ -1018,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.bar_bempty = bar_bempty;
     const uint32_t astage16 = static_cast<uint32_t>(p.a_bytes >> 4), na = static_cast<uint32_t>(p.na);
     uint32_t aslot = 0, aphase = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int item = cid; item < n_items; item += ncl, ++it) {
       const uint32_t acc = it & 1;
       if (it >= 2) {
         mbar_wait(&bar_acc_empty[acc], ((it >> 1) - 1) & 1);
@@ -1026,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
       }
       c.tmem_d = taddr + acc * kMaxNTile;
-      for (int ch = 0; ch < p.nchunks; ++ch) {
+      for (int ch = c_begin; ch < c_end; ++ch) {
         mbar_wait(&bar_afull[aslot], aphase);
         __syncwarp();
         fence_proxy_async();
@@ -1034,11 +1155,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 22 + ch);
         const uint32_t abase = c.a0 + aslot * astage16;
         if (tps == 9)
-          mma_chunk<F16, K, S, (K == 3 ? 9 : 1)>(c, abase, ch == 0);
+          mma_chunk<F16, K, S, (K == 3 ? 9 : 1)>(c, abase, ch == c_begin);
         else if (tps == 3)
-          mma_chunk<F16, K, S, (K == 3 ? 3 : 1)>(c, abase, ch == 0);
+          mma_chunk<F16, K, S, (K == 3 ? 3 : 1)>(c, abase, ch == c_begin);
         else
-          mma_chunk<F16, K, S, 1>(c, abase, ch == 0);
+          mma_chunk<F16, K, S, 1>(c, abase, ch == c_begin);
         if (elect_one()) umma_commit(&bar_afree[aslot]);
         if (++aslot == na) {
           aslot = 0;
@@ -1057,9 +1178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t b_iter = 0, bslot = 0, bphase = 0;
       const uint32_t b0 = smem_u32(bbuf);
       const uint32_t stage_bytes = b_stage;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      for (int item = cid; item < n_items; item += ncl) {
         const int ni = item % n_slices;
-        for (int ch = 0; ch < p.nchunks; ++ch)
+        for (int ch = c_begin; ch < c_end; ++ch)
           for (int tg = 0; tg < tgroups; ++tg, ++b_iter) {
             const uint32_t st = bslot;
             if (b_iter >= nb) mbar_wait(&bar_bempty[st], bphase ^ 1);
@@ -1071,7 +1192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, (ch * p.ntaps + tg * tps) * 8, &bar_bfull[st]);
             if (b_iter == 0) tl_mark(p, 10);
           }
-        if (item == static_cast<int>(blockIdx.x)) tl_mark(p, 11);
+        if (item == cid) tl_mark(p, 11);
       }
     }
   }
@@ -1081,6 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.ks > 1) cluster_sync();  // no CTA leaves while a peer may still touch its shared memory
   if (warp == 8) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kTmemCols)
@@ -1128,6 +1250,37 @@ int tps_for(int n_tile, int ntaps) {
   if (n_tile <= 32) return 9;  // a whole chunk (<= 36 KB) per TMA
   if (n_tile <= 64) return 3;
   return 1;
+}
+
+// (N tile, split-K) for a launch whose tile count is known on the host (the
+// dense pass / dense-fallback layers): minimise rounds over the SMs x the
+// per-CTA chain — max(MMA issue at ~max(47, 40 + N/4) cycles per MMA, weight
+// stream at ~40 B/cycle per SM) — plus ~2000 cycles per reduce-scatter. The
+// split must leave each CTA >= 1 chunk and own a multiple of 16 columns.
+void plan_static(int items_m, int n_pad, int nchunks, int ntaps, int sms, long long red_cap, int* nt_out,
+                 int* ks_out) {
+  double best = -1.0;
+  for (int ks = 1; ks <= 8; ks <<= 1) {
+    if (ks > nchunks) break;
+    for (int c = 16; c <= kMaxNTile; c <<= 1) {
+      const int nt = std::min(c, n_pad);
+      if (n_pad % nt != 0 || nt % (16 * ks) != 0) continue;
+      if (ks > 1 && static_cast<long long>(ks - 1) * 128 * (nt / ks) * 4 > red_cap) continue;
+      const long long ctas = static_cast<long long>(items_m) * (n_pad / nt) * ks;
+      const long long rounds = (ctas + sms - 1) / sms;
+      const int chunks = (nchunks + ks - 1) / ks;
+      const double mma = static_cast<double>(chunks) * ntaps * 4 * std::max(47, 40 + nt / 4);
+      const double wts = static_cast<double>(chunks) * ntaps * nt * 128 / 40.0;
+      const double red = ks > 1 ? (ks - 1.0) / ks * 128.0 * nt * 4.0 / 10.0 + 3000.0 : 0.0;
+      const double t = rounds * (std::max(mma, wts) + red + 8000.0);
+      if (best < 0 || t < best * 0.97) {  // prefer the smaller split on near ties
+        best = t;
+        *nt_out = nt;
+        *ks_out = ks;
+      }
+      if (nt == n_pad) break;
+    }
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1281,10 +1434,34 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     p.xf_table = src.n * src.c;
   }
   p.xf_bytes = xform ? (2 * p.xf_table * 4 + 127) / 128 * 128 : 0;
+  // Static tile count: N tile and split-K planned here; the device keeps them.
+  p.ks = 1;
+  p.nt_fixed = 0;
+  static const bool no_splitk = std::getenv("SIGE_NO_SPLITK") != nullptr;
+  static const int force_ks = std::getenv("SIGE_FORCE_SPLITK") ? std::atoi(std::getenv("SIGE_FORCE_SPLITK")) : 0;
+  if (!tiles.count_dev) {
+    int nt = 0, ks = 1;
+    // Shared memory left for the reduction buffer beside the minimal rings (2 A stages, 2 weight stages).
+    const long long red_cap = 225LL * 1024 - (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 -
+                              p.xf_bytes - 2LL * p.a_bytes - 2LL * max_stage;
+    plan_static((tiles.count + p.T - 1) / p.T, p.n_pad, p.nchunks, p.ntaps, sm_count(), no_splitk ? -1 : red_cap, &nt,
+                &ks);
+    // Test hook: force a split (largest power of two <= the request that the geometry allows).
+    for (int f = force_ks; f > 1 && ks == 1; f >>= 1) {
+      const int ntf = std::min(p.n_pad, kMaxNTile);
+      if (f <= p.nchunks && ntf % (16 * f) == 0 && static_cast<long long>(f - 1) * 128 * (ntf / f) * 4 <= red_cap) {
+        nt = ntf;
+        ks = f;
+      }
+    }
+    p.nt_fixed = nt;
+    p.ks = ks;
+  }
+  p.red_bytes = p.ks > 1 ? (p.ks - 1) * 128 * (p.nt_fixed / p.ks) * 4 : 0;
   // Ring depths: up to 4 A stages, the rest of shared memory is the B ring
   // (at least two of the largest weight stages).
   constexpr size_t kSmemBudget = 225 * 1024;
-  const size_t fixed = sizeof(int32_t) * p.phases * p.T * p.Mt + p.xf_bytes;
+  const size_t fixed = (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 + p.xf_bytes + p.red_bytes;
   p.na = kMaxNA;
   auto b_room = [&] { return static_cast<long long>(kSmemBudget) - static_cast<long long>(fixed) -
                              static_cast<long long>(p.na) * p.a_bytes; };
@@ -1318,19 +1495,32 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   }
   static const int dbg = std::getenv("SIGE_TC_DEBUG") ? std::atoi(std::getenv("SIGE_TC_DEBUG")) : 0;
   p.dbg = dbg;
-  const long long max_items = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
-  const int grid = static_cast<int>(std::max(1LL, std::min<long long>(max_items, sm_count())));
+  long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
+  if (p.nt_fixed) max_ctas = static_cast<long long>((tiles.count + p.T - 1) / p.T) * (p.n_pad / p.nt_fixed) * p.ks;
+  const int sms = sm_count() / p.ks * p.ks;
+  const int grid = static_cast<int>(std::max<long long>(p.ks, std::min<long long>(max_ctas, sms)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na_attr = 0;
   static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
+  if (!no_pdl) {
+    attr[na_attr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na_attr].val.programmaticStreamSerializationAllowed = 1;
+    ++na_attr;
+  }
+  if (p.ks > 1) {
+    attr[na_attr].id = cudaLaunchAttributeClusterDimension;
+    attr[na_attr].val.clusterDim.x = p.ks;
+    attr[na_attr].val.clusterDim.y = 1;
+    attr[na_attr].val.clusterDim.z = 1;
+    ++na_attr;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cfg.numAttrs = na_attr;
   SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
   after_launch("k_conv_tc");
   if (timeline) {
@@ -1346,8 +1536,9 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     for (int i = 0; i < grid; ++i)
       if (h[1024 + i]) last = std::max(last, h[1024 + i] - t0);
     std::fprintf(stderr,
-                 "[tc] %dx%d c%d->%d k%d s%d T%d Mt%d grid %d na %d nb %d async %d: span %.2f us, last entry %.2f us\n",
-                 tiles.bh, tiles.bw, cw.c_in, cw.c_out, cw.k, cw.stride, p.T, p.Mt, grid, p.na, p.nb, p.async_a,
+                 "[tc] %dx%d c%d->%d k%d s%d T%d Mt%d grid %d ks %d nt %d na %d nb %d async %d: span %.2f us, last entry %.2f us\n",
+                 tiles.bh, tiles.bw, cw.c_in, cw.c_out, cw.k, cw.stride, p.T, p.Mt, grid, p.ks, p.nt_fixed, p.na, p.nb,
+                 p.async_a,
                  (tend - t0) * 1e-3, last * 1e-3);
     for (int c = 0; c < 2; ++c) {
       if (h[c * 64 + 12] > h[c * 64 + 0])
