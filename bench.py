@@ -119,6 +119,62 @@ def measured_peaks():
         return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+# ------------------------------------------------------- op-level HBM --
+
+def ops_roofline(sb, torch, hbm_peak, reps=20):
+    """HBM roofline of the reference-API data-movement ops (mask.hpp /
+    kernels.hpp drop-ins through the C ABI) at a bandwidth-sized workload:
+    8 independent requests (batch 8) of 128 x 256 x 256 fp32 activations with
+    a 30 %-area edit (b = 6 tiles after dilation 1). Algorithmic bytes: gather
+    2 G C win^2 4, scatter (in place) 2 G C b^2 4, difference mask 2 N C H W 4 + H W.
+    L2 (126 MB) is flushed before every timed call."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n, c, h, w, b = 8, 128, 256, 256, 6
+    g = torch.Generator(device="cpu").manual_seed(11)
+    orig = torch.rand((n, c, h, w), generator=g).to(dev) * 2 - 1
+    edited = orig.clone()
+    side = int(round((0.30 * h * w) ** 0.5))
+    edited[:, :, 40:40 + side, 60:60 + side] += 0.25
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            e.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(e))
+        ts.sort()
+        return ts[len(ts) // 2] * 1e-3  # median seconds
+
+    mask = sb.compute_difference_mask(orig, edited, 1e-3)
+    idx = sb.mask_to_block_indices(sb.dilate_mask(mask, 1), b, n)
+    G = int(idx.shape[0])
+    win = b + 2
+    blocks = sb.gather(edited, idx, b, 3, 1)
+    out_blocks = torch.rand((G, c, b, b), generator=g).to(dev)
+    base = orig.clone()
+    out = {}
+    for name, fn, nbytes in [
+        ("difference_mask", lambda: sb.compute_difference_mask(orig, edited, 1e-3), 2 * n * c * h * w * 4 + h * w),
+        ("gather", lambda: sb.gather(edited, idx, b, 3, 1), 2 * G * c * win * win * 4),
+        ("scatter_inplace", lambda: sb.scatter_inplace(out_blocks, idx, base), 2 * G * c * b * b * 4),
+    ]:
+        t = timed(fn)
+        gbs = nbytes / t / 1e9
+        out[name] = {"us": round(t * 1e6, 2), "bytes": int(nbytes), "achieved_gbs": round(gbs, 1),
+                     "frac": round(gbs / hbm_peak, 4)}
+    out["workload"] = f"batch {n} x {c}x{h}x{w} fp32, 30% edit, {G} tiles b={b}, L2 flushed"
+    del blocks
+    return out
+
+
 # ------------------------------------------------------------ reference --
 
 def reference_setup(model_name, fx, seed, n_threads, cache_from=None):
@@ -352,6 +408,12 @@ def main_ours(args):
                      "algorithmic_flops_per_step": conv_flops, "traffic": None},
         "clocks": clocks,
     }
+    if world == 1:
+        try:
+            line["ops_hbm"] = ops_roofline(sb, torch, hbm_peak)
+            line["ops_hbm"]["peak_gbs"] = hbm_peak
+        except Exception as e:  # report, never hide
+            line["ops_hbm"] = {"error": str(e)}
     if not args.no_cpu_baseline and world == 1:
         try:
             nthreads = os.cpu_count() or 1

@@ -163,22 +163,53 @@ __global__ void k_blockify(const uint8_t* __restrict__ m, int h, int w, int b, i
 __global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
                          const int32_t* __restrict__ idx, int count, int win, int stride, int pad,
                          DevEpilogue epi, float* __restrict__ out) {
-  long long wsz = (long long)win * win;
-  long long total = (long long)count * c * wsz;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-       q += (long long)gridDim.x * blockDim.x) {
-    long long i = q / (c * wsz);
-    int rem = static_cast<int>(q - i * c * wsz);
-    int ch = rem / static_cast<int>(wsz);
-    int cell = rem - ch * static_cast<int>(wsz);
-    int wy = cell / win, wx = cell - wy * win;
-    int n = idx[3 * i], sy = idx[3 * i + 1] * stride - pad + wy, sx = idx[3 * i + 2] * stride - pad + wx;
-    float v = 0.0f;
-    if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
-      v = __ldg(x + (((size_t)n * c + ch) * h + sy) * w + sx);
-      v = dev_epi(epi, v, ch, c, n);
+  // One tile per blockIdx.x (grid-stride). A thread owns quads (4 consecutive
+  // outputs of the tile slab (C, win, win), indices advanced incrementally,
+  // one 16-byte store each) and keeps two quads = 8 loads in flight.
+  constexpr int kQ = 2;
+  const int wsz = win * win, slab = c * wsz;
+  const bool vec = (slab & 3) == 0;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1) * stride - pad,
+              ox = __ldg(idx + 3 * i + 2) * stride - pad;
+    const size_t plane0 = static_cast<size_t>(n) * c;
+    float* o = out + static_cast<size_t>(i) * slab;
+    for (int q0 = threadIdx.x * 4; q0 < slab; q0 += blockDim.x * 4 * kQ) {
+      float v[kQ][4];
+#pragma unroll
+      for (int k = 0; k < kQ; ++k) {
+        const int q = q0 + k * blockDim.x * 4;
+        int ch = q / wsz, cell = q - ch * wsz;
+        int wy = cell / win, wx = cell - wy * win;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[k][e] = 0.0f;
+          if (q + e < slab) {
+            const int sy = oy + wy, sx = ox + wx;
+            if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
+              v[k][e] = __ldg(x + ((plane0 + ch) * h + sy) * w + sx);
+              if (epi.num_steps) v[k][e] = dev_epi(epi, v[k][e], ch, c, n);
+            }
+          }
+          if (++wx == win) {
+            wx = 0;
+            if (++wy == win) {
+              wy = 0;
+              ++ch;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kQ; ++k) {
+        const int q = q0 + k * blockDim.x * 4;
+        if (q >= slab) break;
+        if (vec)
+          *reinterpret_cast<float4*>(o + q) = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        else
+          for (int e = 0; e < 4 && q + e < slab; ++e) o[q + e] = v[k][e];
+      }
     }
-    out[q] = v;
   }
 }
 
@@ -187,23 +218,35 @@ __global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
 __global__ void k_scatter(const float* __restrict__ blocks, int count, int c, int b,
                           const int32_t* __restrict__ idx, float* __restrict__ base, int h, int w,
                           int mode) {
-  long long bsz = (long long)b * b;
-  long long total = (long long)count * c * bsz;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-       q += (long long)gridDim.x * blockDim.x) {
-    long long i = q / (c * bsz);
-    int rem = static_cast<int>(q - i * c * bsz);
-    int ch = rem / static_cast<int>(bsz);
-    int cell = rem - ch * static_cast<int>(bsz);
-    int y = idx[3 * i + 1] + cell / b, xx = idx[3 * i + 2] + cell % b;
-    if (y >= h || xx >= w) continue;
-    float* d = base + (((size_t)idx[3 * i] * c + ch) * h + y) * w + xx;
-    float v = blocks[q];
-    *d = mode ? __fadd_rn(*d, v) : v;
+  // One tile per blockIdx.x (grid-stride); lanes walk the tile slab
+  // contiguously (coalesced block reads; a warp store covers whole tile rows),
+  // 8 independent elements per thread in flight.
+  constexpr int kU = 8;
+  const int bsz = b * b, slab = c * bsz;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int n = __ldg(idx + 3 * i), r0 = __ldg(idx + 3 * i + 1), c0 = __ldg(idx + 3 * i + 2);
+    const float* src = blocks + static_cast<size_t>(i) * slab;
+    for (int q0 = threadIdx.x; q0 < slab; q0 += blockDim.x * kU) {
+      float v[kU];
+#pragma unroll
+      for (int e = 0; e < kU; ++e) {
+        const int q = q0 + e * blockDim.x;
+        v[e] = q < slab ? __ldg(src + q) : 0.0f;
+      }
+#pragma unroll
+      for (int e = 0; e < kU; ++e) {
+        const int q = q0 + e * blockDim.x;
+        if (q >= slab) continue;
+        const int ch = q / bsz, cell = q - ch * bsz;
+        const int y = r0 + cell / b, x = c0 + cell % b;
+        if (y >= h || x >= w) continue;
+        float* d = base + ((static_cast<size_t>(n) * c + ch) * h + y) * w + x;
+        *d = mode ? __fadd_rn(*d, v[e]) : v[e];
+      }
+    }
   }
 }
 
-// build_scatter_map (kernels.cpp:134-169), fill then per-tile writes.
 __global__ void k_map_fill(sige_scatter_entry* map, long long hw) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < hw;
        p += (long long)gridDim.x * blockDim.x) {
@@ -433,8 +476,8 @@ void op_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, i
                       "x" + std::to_string(ow));
   if (count == 0) return;
   int win = s * b + k - s;
-  k_gather<<<grid_for((long long)count * c * win * win), kThreads, 0, st>>>(
-      x, c, h, w, idx, count, win, s, (k - 1) / 2, epi, out);
+  k_gather<<<std::min(count, sm_count() * 16), kThreads, 0, st>>>(x, c, h, w, idx, count, win, s, (k - 1) / 2,
+                                                                 epi, out);
   after_launch("k_gather");
 }
 
@@ -442,8 +485,8 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
                 int n, int c, int h, int w, bool add, cudaStream_t st) {
   if (channels != c) throw ConfigError(std::string(add ? "scatter_add" : "scatter") + ": channel mismatch");
   if (count == 0) return;
-  k_scatter<<<grid_for((long long)count * c * b * b), kThreads, 0, st>>>(blocks, count, c, b, idx,
-                                                                         base, h, w, add ? 1 : 0);
+  k_scatter<<<std::min(count, sm_count() * 16), kThreads, 0, st>>>(blocks, count, c, b, idx, base, h, w,
+                                                                  add ? 1 : 0);
   after_launch("k_scatter");
 }
 
