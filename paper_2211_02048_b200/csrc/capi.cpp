@@ -61,6 +61,10 @@ const char* sige_last_error(void) { return g_err.c_str(); }
 const char* sige_version(void) { return "sige_b200 0.1 (sm_100a)"; }
 uint64_t sige_kernel_launch_count(void) { return g_launches.load(); }
 
+// Developer instrumentation, not part of the reference-facing ABI: per-launch
+// [start, end] globaltimer of k_conv_tc launches when SIGE_TC_GTL=1.
+int sige_debug_conv_timeline(unsigned long long* out, int cap) { return sige_b200::debug_conv_timeline(out, cap); }
+
 void sige_run_config_default(sige_run_config* c) {  // graph.hpp:87-101
   c->step = 0;
   c->mask_threshold = 1e-3f;

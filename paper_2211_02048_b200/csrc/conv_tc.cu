@@ -58,6 +58,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.hpp"
 #include "engine_kernels.hpp"
@@ -73,6 +74,8 @@ constexpr int kMaxNA = 4;          // A ring stages (max)
 constexpr int kMaxNB = 16;         // B (weight) ring slots (max)
 constexpr int kMaxNTile = 256;     // accumulator columns per TMEM buffer
 constexpr int kTmemCols = 2 * kMaxNTile;  // two accumulators: epilogue of item i overlaps MMA of item i+1
+constexpr int kGtlLaunchesDev = 1024;  // == kGtlLaunches (timeline buffer layout)
+constexpr int kDynSmem = 222 * 1024;  // dynamic shared memory per CTA (+ ~4 KB static, 227 KB cap)
 constexpr int kBatch = 4;          // 16-byte groups staged per thread per batch (synchronous path)
 
 struct TcParams {
@@ -92,11 +95,21 @@ struct TcParams {
   int xform;      // 1: async + in-shared-memory transform: [scale-shift (table), act] applied after landing
   int xf_act;     // activation of the transform chain
   int xf_table;   // floats per table (n * C) of the scale-shift table in shared memory
+  double gn_inv_count;  // 1 / values per (n, group) of the GroupNorm-from-statistics source
   uint32_t lbo_a, idesc_base;
   int a_bytes, b_ring_bytes, xf_bytes;  // A stage bytes; B ring bytes (slots sized per launch from the N tile)
   int tps[5];     // taps per weight stage for n_tile = 16, 32, 64, 128, 256
+  // Host-precomputed per N-width tables (no integer divisions on the device's
+  // setup path — each costs a ~100-cycle MUFU/IMAD chain): width (0 = not
+  // usable), N slices (n_pad / width), weight stages per chunk, ring slots.
+  int w_nt[5], w_slices[5], w_tgroups[5], w_nb[5];
+  float w_inv_slices[5];
+  int ks_log2;    // log2(ks)
+  int c_lo[9];    // split-K chunk range of rank r: [c_lo[r], c_lo[r + 1])
   unsigned long long* tl;  // debug timeline (SIGE_TC_TIMELINE), nullptr normally
   int dbg;                 // SIGE_TC_DEBUG bits (experiments only)
+  unsigned long long* gtl;  // SIGE_TC_GTL: per-launch [first CTA start, last CTA end] (graph-safe)
+  int gtl_idx;
 };
 
 // ------------------------------------------------------------- PTX ------
@@ -631,34 +644,54 @@ __device__ __forceinline__ void st4(float* p, const float* v) {
 // destination carries an activation buffer, act = chain(written value) —
 // the consumer's pending GroupNorm scale-shift + activation evaluated once
 // per output pixel. One vector path; everything else goes out of line.
+// Per-item epilogue operands staged while the MMAs run: per-channel bias and
+// the act chain's leading scale-shift in shared memory (sb, ssc/ssh, indexed
+// by column within the item; nullptr = read from global), and this row's
+// residual operand prefetched into registers one 16-column block ahead.
+struct EpiOps {
+  const float* sb = nullptr;   // bias[16] of this block (shared)
+  const float* ssc = nullptr;  // act scale-shift step 0 params [16] (shared), or nullptr
+  const float* ssh = nullptr;
+  const float* aux = nullptr;  // residual / addend operand [16] (registers), or nullptr
+};
+
+__device__ __forceinline__ bool addend_vectorizable(const Dst& d) {
+  return d.mode != kAddSrc || (d.addend.layout == kNHWC && !d.addend.half && d.addend.up == 0 &&
+                               d.addend.epi.num_steps == 0 && (d.addend.c & 3) == 0);
+}
+
+__device__ __forceinline__ const float* aux_ptr(const Dst& d, size_t pix, int n, int y, int x, int oc0) {
+  return d.mode == kAddSrc ? d.addend.ptr + ((static_cast<size_t>(n) * d.addend.h + y) * d.addend.w + x) * d.addend.c + oc0
+                           : d.aux + pix + oc0;
+}
+
 __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v,
-                                      float* written) {
+                                      float* written, const EpiOps& ops) {
   const Dst& d = p.dst;
   const int cnt = min(16, p.c_out - oc0);
   if (cnt <= 0) return;
-  const bool addend_vec = d.mode != kAddSrc || (d.addend.layout == kNHWC && !d.addend.half && d.addend.up == 0 &&
-                                                d.addend.epi.num_steps == 0 && (d.addend.c & 3) == 0);
-  if (cnt < 16 || (d.c & 3) != 0 || !addend_vec) {
+  if (cnt < 16 || (d.c & 3) != 0 || !addend_vectorizable(d)) {
     out_slow(d, p.bias, p.c_out, pix, n, y, x, oc0, v, cnt);
     if (d.gn_stats)
       for (int j = 0; j < 16; ++j) written[j] = j < cnt ? v[j] : 0.0f;
     return;
   }
   const size_t at = pix + oc0;
-  float t[16];
   if (p.bias) {
 #pragma unroll
-    for (int j = 0; j < 16; j += 4) ld4(p.bias + oc0 + j, t + j);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], ops.sb[j]);
   }
   float* o = d.ptr + at;
   if (d.mode != kStore) {
-    const float* src = d.mode == kAddSrc
-                           ? d.addend.ptr + ((static_cast<size_t>(n) * d.addend.h + y) * d.addend.w + x) * d.addend.c + oc0
-                           : d.aux + at;
+    float t[16];
+    if (ops.aux) {
 #pragma unroll
-    for (int j = 0; j < 16; j += 4) ld4(src + j, t + j);
+      for (int j = 0; j < 16; ++j) t[j] = ops.aux[j];
+    } else {
+      const float* src = aux_ptr(d, pix, n, y, x, oc0);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) ld4(src + j, t + j);
+    }
     if (d.mode == kResShortcut) {
       float cur[16];
 #pragma unroll
@@ -680,7 +713,17 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
     for (int j = 0; j < 16; ++j) written[j] = v[j];
   }
   if (d.act) {
-    tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
+    if (ops.ssc) {  // [SS (staged), ACT...]
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(__fmul_rn(ops.ssc[j], v[j]), ops.ssh[j]);
+      for (int s2 = 1; s2 < d.act_epi.num_steps; ++s2) {
+        const int k = d.act_epi.act[s2];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = tc_act(v[j], k);
+      }
+    } else {
+      tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
+    }
     if (d.act_half) {
       uint4* h = reinterpret_cast<uint4*>(static_cast<__half*>(d.act) + at);
       h[0] = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
@@ -738,19 +781,23 @@ __device__ __forceinline__ void gn_accumulate(const Dst& d, int c_out, int oc0, 
 // N=16: 47, 64: 65, 128: 76, 256: 130), every item runs the same number of
 // MMAs, so pick the width minimising rounds x cost-per-MMA over the SMs.
 __device__ __forceinline__ int pick_n_tile(const TcParams& p, int items_m) {
-  int best = min(p.n_pad, kMaxNTile);
-  long long best_cost = -1;
-  for (int c = 16; c <= kMaxNTile; c <<= 1) {
-    const int nt = min(c, p.n_pad);
-    if (p.n_pad % nt != 0) continue;
-    const long long items = static_cast<long long>(items_m) * (p.n_pad / nt);
-    const long long rounds = (items + p.min_items - 1) / p.min_items;
-    const long long cost = rounds * max(47, 40 + nt / 4) * 1024 + nt;  // ties -> narrower
-    if (best_cost < 0 || cost < best_cost) {
+  // Returns the width index. Division-free: rounds = ceil(items / SMs) via a
+  // float reciprocal and one fix-up (items < 2^24).
+  int best = -1;
+  unsigned best_cost = 0xffffffffu;
+  const float inv_sms = 1.0f / static_cast<float>(p.min_items);
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int nt = p.w_nt[i];
+    if (nt == 0) continue;
+    const int items = items_m * p.w_slices[i];
+    int rounds = static_cast<int>(static_cast<float>(items) * inv_sms);  // floor, maybe one short
+    if (rounds * p.min_items < items) ++rounds;
+    const unsigned cost = static_cast<unsigned>(rounds) * static_cast<unsigned>(max(47, 40 + nt / 4)) * 512u + nt;
+    if (cost < best_cost) {  // ties -> narrower
       best_cost = cost;
-      best = nt;
+      best = i;
     }
-    if (nt == p.n_pad) break;
   }
   return best;
 }
@@ -808,7 +855,10 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
 //   warps 4-7  epilogue: TMEM accumulator (i & 1) -> bias / residual -> dst
 //   warp 8     TMEM allocation + the single MMA-issuing thread
 //   warp 9     weight producer: one TMA per ring stage (1, 3 or 9 taps)
-template <bool F16, int K, int S>
+// SYNC: the instantiation carries the synchronous (converting / chained)
+// staging path; the F16 production kernels (every source an fp16 twin or act
+// buffer) are built without it — half the code, fewer cold instruction fetches.
+template <bool F16, int K, int S, bool SYNC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -817,6 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t bar_red_full, bar_red_empty;  // split-K reduce-scatter (ks > 1)
   __shared__ uint32_t tmem_base;
   __shared__ int4 s_tile[16];  // producers' current item tiles: (n, window origin y, x, -); n = -1 empty slot
+  __shared__ float s_bias[kMaxNTile], s_asc[kMaxNTile], s_ash[kMaxNTile];  // epilogue operands of the item
 
   uint8_t* abuf0 = smem;
   uint8_t* bbuf = smem + p.na * p.a_bytes;
@@ -826,6 +877,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* red_buf = reinterpret_cast<float*>(bbuf + p.b_ring_bytes + p.xf_bytes +
                                             ((sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128) * 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0 && p.gtl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.gtl + 2 * p.gtl_idx, t);
+  }
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
     tl_cta(p, 1024);
@@ -869,58 +925,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   // previous conv started; weights are static. Both are safe before the wait.
   const int items_m = (count + p.T - 1) / p.T;
   if (threadIdx.x == 0 && items_m >= 0) tl_mark(p, 48);
-  const int n_tile = p.nt_fixed ? p.nt_fixed : pick_n_tile(p, items_m);
+  const int nti = p.nt_fixed ? nt_index(p.nt_fixed) : pick_n_tile(p, items_m);
+  const int n_tile = p.w_nt[nti];
   // Split-K: the cluster's CTAs share each item, CTA `rank` runs K chunks
   // [c_begin, c_end) and owns output columns [rank, rank + 1) * n_tile / ks.
   const int rank = p.ks > 1 ? static_cast<int>(cluster_rank()) : 0;
-  const int cid = blockIdx.x / p.ks, ncl = gridDim.x / p.ks;
-  const int c_begin = rank * p.nchunks / p.ks, c_end = (rank + 1) * p.nchunks / p.ks;
-  const int n_slices = p.n_pad / n_tile;
+  const int cid = blockIdx.x >> p.ks_log2, ncl = gridDim.x >> p.ks_log2;
+  const int c_begin = p.c_lo[rank], c_end = p.c_lo[rank + 1];
+  const int n_slices = p.w_slices[nti];
+  const float inv_slices = p.w_inv_slices[nti];
   const int n_items = items_m * n_slices;
-  const int nti = nt_index(n_tile);
   const int tps = p.tps[nti];
-  const int tgroups = p.ntaps / tps;
+  const int tgroups = p.w_tgroups[nti];
   const uint32_t lbo_b = static_cast<uint32_t>(n_tile * 16);
   const uint32_t tap_b = static_cast<uint32_t>(n_tile * 128);  // one tap of B in smem
   const uint32_t idesc = p.idesc_base | (static_cast<uint32_t>(n_tile >> 3) << 17);
   // B ring: slots of one TMA stage (tps taps x n_tile rows x 128 B) each.
   const uint32_t b_stage = static_cast<uint32_t>(tps) * tap_b;
-  const uint32_t nb = min(static_cast<uint32_t>(kMaxNB), static_cast<uint32_t>(p.b_ring_bytes) / b_stage);
+  const uint32_t nb = static_cast<uint32_t>(p.w_nb[nti]);
+  if (threadIdx.x == 0) tl_mark(p, 55);
   if (threadIdx.x == 0) pdl_trigger();  // the next layer may start its own setup
 
   if (warp < 4) {
     // ---------------- A producers ----------------
+    if (threadIdx.x == 0) tl_mark(p, 54);
     pdl_wait();  // the source was written by the previous kernel
+    if (threadIdx.x == 0 && p.gtl) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMin(p.gtl + 2 * kGtlLaunchesDev + p.gtl_idx, t);
+    }
     if (threadIdx.x == 0) tl_mark(p, 49);
     const uint32_t a0 = smem_u32(abuf0);
     if (p.xform) {
-      // Scale-shift table of the transform: folded from GroupNorm statistics
-      // (written by the previous conv's epilogue) or copied from the chain.
+      // Scale-shift table of the transform, for this CTA's input channels only
+      // (its K chunks): folded from the GroupNorm statistics the previous
+      // conv's epilogue accumulated (reciprocal count from the host, rsqrt —
+      // this sits on the critical path right after the dependency wait), or
+      // copied from the chain.
       const Src& s = p.src;
-      for (int i = threadIdx.x; i < p.xf_table; i += kProdThreads) {
-        const int n = i / s.c, c = i - n * s.c;
+      const int c_lo = c_begin * 64, c_hi = min(s.c, c_end * 64);
+      const int span = c_hi - c_lo;
+      const int cpg = s.gn_stats ? s.c / s.gn_groups : 1;
+      for (int i = threadIdx.x; i < s.n * span; i += kProdThreads) {
+        const int n = i / span, c = c_lo + (i - n * span);
         float sc, sh;
         if (s.gn_stats) {
-          const int g = c / (s.c / s.gn_groups);
-          const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + g);
-          const double mean = st[0] / s.gn_count;
-          double var = st[1] / s.gn_count - mean * mean;
-          if (var < 0.0) var = 0.0;
-          sc = __fdiv_rn(__ldg(s.gn_gamma + c), __fsqrt_rn(__fadd_rn(static_cast<float>(var), s.gn_eps)));
-          sh = __fsub_rn(__ldg(s.gn_beta + c), __fmul_rn(static_cast<float>(mean), sc));
+          const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + c / cpg);
+          const double mean = st[0] * p.gn_inv_count;
+          const float var = fmaxf(static_cast<float>(st[1] * p.gn_inv_count - mean * mean), 0.0f);
+          sc = __ldg(s.gn_gamma + c) * rsqrtf(var + s.gn_eps);
+          sh = fmaf(-static_cast<float>(mean), sc, __ldg(s.gn_beta + c));
         } else {
-          const int off = s.epi.per_sample[0] ? i : c;
+          const int off = s.epi.per_sample[0] ? n * s.c + c : c;
           sc = __ldg(s.epi.scale[0] + off);
           sh = __ldg(s.epi.shift[0] + off);
         }
-        xf_scale[i] = sc;
-        xf_shift[i] = sh;
+        xf_scale[n * s.c + c] = sc;
+        xf_shift[n * s.c + c] = sh;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
     }
-    uint32_t a_iter = 0, it = 0;
+    uint32_t a_iter = 0, it = 0, aphase = 0;
+    int aslot = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
-      const int mi = item / n_slices;
+      const int mi = static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices);  // item / n_slices
       const int g0 = mi * p.T, nt = min(p.T, count - g0);
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));  // previous item's s_tile readers done
       if (threadIdx.x < p.T) {
@@ -945,8 +1014,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ch = c_begin; ch <= c_end; ++ch) {
           int sidx = -1;
           if (ch < c_end) {
-            sidx = static_cast<int>(a_iter % p.na);
-            if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
+            sidx = aslot;
+            if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
+            if (++aslot == p.na) {
+              aslot = 0;
+              aphase ^= 1;
+            }
             stage_a_async_fast(p, a0 + sidx * p.a_bytes, ch, pix_off);
             asm volatile("cp.async.commit_group;" ::: "memory");
             ++a_iter;
@@ -964,8 +1037,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         for (int ch = c_begin; ch < c_end; ++ch, ++a_iter) {
-          const int sidx = static_cast<int>(a_iter % p.na);
-          if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], ((a_iter / p.na) - 1) & 1);
+          const int sidx = aslot;
+          if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
+          if (++aslot == p.na) {
+            aslot = 0;
+            aphase ^= 1;
+          }
           if (p.async_a) {
             // The arrival fires when this thread's copies have landed, so the
             // producers run ahead to the next free stage without waiting.
@@ -975,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               stage_a_async<F16>(p, a0 + sidx * p.a_bytes, ch, row_tab, s_tile);
             cp_async_arrive(&bar_afull[sidx]);
           } else {
-            stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+            if constexpr (SYNC) stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
             fence_proxy_async();
             mbar_arrive(&bar_afull[sidx]);
           }
@@ -995,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int oy = rr / p.P, ox = rr - oy * p.P;
     uint32_t it = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
-      const int mi = item / n_slices, ni = item % n_slices;
+      const int mi = static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices), ni = item - mi * n_slices;
       const int g = mi * p.T + t;
       bool valid = t < p.T && g < count && oy < p.tiles.bh && ox < p.tiles.bw;
       int n = 0, y = 0, x = 0;
@@ -1006,33 +1083,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         valid = y < p.dst.h && x < p.dst.w;
       }
       const size_t pix = ((static_cast<size_t>(n) * p.dst.h + y) * p.dst.w + x) * p.dst.c;
-      // While the MMAs run: pull this item's per-channel params (bias, the act
-      // chain's scale/shift) and this row's residual operand into L1, so the
-      // epilogue's loads hit instead of paying an L2 round trip each.
-      const int slice = n_tile / p.ks, own0 = rank * slice;  // this CTA's output columns within the item
+      const int slice = n_tile >> p.ks_log2, own0 = rank * slice;  // this CTA's output columns within the item
+      // While the MMAs run: stage this item's per-channel operands (bias and
+      // the act chain's leading scale-shift, for the columns this CTA writes)
+      // in shared memory, and prefetch this row's first residual block.
+      const DevEpilogue& ae = p.dst.act_epi;
+      bool act_pre = p.dst.act && ae.num_steps >= 1 && ae.kind[0] == SIGE_EPI_SCALE_SHIFT &&
+                     (!ae.per_sample[0] || p.dst.n == 1);
+      for (int s2 = 1; s2 < ae.num_steps; ++s2) act_pre = act_pre && ae.kind[s2] == SIGE_EPI_ACTIVATION;
       {
-        const int oc0 = ni * n_tile + own0, nb = slice * 4;  // bytes of one slice of per-channel floats
-        const int lines = (nb + 127) / 128;
-        int li = threadIdx.x - kProdThreads;
-        if (p.bias && li < lines) prefetch_l1(p.bias + oc0 + li * 32);
-        li -= lines;
-        const DevEpilogue& ae = p.dst.act_epi;
-        for (int sstep = 0; sstep < ae.num_steps && p.dst.act; ++sstep) {
-          if (ae.kind[sstep] != SIGE_EPI_SCALE_SHIFT) continue;
-          const int reps = ae.per_sample[sstep] ? p.dst.n : 1;
-          for (int r = 0; r < reps; ++r) {
-            const int off = (ae.per_sample[sstep] ? r * p.dst.c : 0) + oc0;
-            if (li >= 0 && li < lines) prefetch_l1(ae.scale[sstep] + off + li * 32);
-            if (li >= lines && li < 2 * lines) prefetch_l1(ae.shift[sstep] + off + (li - lines) * 32);
-            li -= 2 * lines;
+        const int oc0 = ni * n_tile + own0;
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // previous item's readers done
+        for (int j = threadIdx.x - kProdThreads; j < slice; j += kEpiThreads) {
+          const int oc = oc0 + j;
+          s_bias[j] = p.bias && oc < p.c_out ? __ldg(p.bias + oc) : 0.0f;
+          if (act_pre) {
+            s_asc[j] = oc < p.c_out ? __ldg(ae.scale[0] + oc) : 0.0f;
+            s_ash[j] = oc < p.c_out ? __ldg(ae.shift[0] + oc) : 0.0f;
           }
         }
-        if (valid && (p.dst.mode == kResMain || p.dst.mode == kResShortcut)) {
-          for (int b = 0; b < nb; b += 128) {
-            prefetch_l1(p.dst.aux + pix + oc0 + b / 4);
-            if (p.dst.mode == kResShortcut) prefetch_l1(p.dst.ptr + pix + oc0 + b / 4);
-          }
-        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));
+      }
+      const bool pre_aux = valid && p.dst.mode != kStore && addend_vectorizable(p.dst) && (p.dst.c & 3) == 0;
+      float aux_next[16];
+      if (pre_aux && ni * n_tile + own0 + 16 <= p.c_out) {
+        const float* src = aux_ptr(p.dst, pix, n, y, x, ni * n_tile + own0);
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) ld4(src + j, aux_next + j);
       }
       const uint32_t acc = it & 1;
       mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
@@ -1044,9 +1121,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[16];
           tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
           if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
+          float aux_cur[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) aux_cur[j] = aux_next[j];
+          const int oc = ni * n_tile + cb;
+          if (pre_aux && cb + 16 < n_tile && oc + 32 <= p.c_out) {  // next block's residual operand
+            const float* src = aux_ptr(p.dst, pix, n, y, x, oc + 16);
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) ld4(src + j, aux_next + j);
+          }
+          EpiOps ops;
+          ops.sb = s_bias + cb;
+          if (act_pre) {
+            ops.ssc = s_asc + cb;
+            ops.ssh = s_ash + cb;
+          }
+          ops.aux = pre_aux && oc + 16 <= p.c_out ? aux_cur : nullptr;
           float wv[16];
-          if (valid) out16(p, pix, n, y, x, ni * n_tile + cb, v, wv);
-          if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + cb, n, valid, wv);
+          if (valid) out16(p, pix, n, y, x, oc, v, wv, ops);
+          if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid, wv);
         }
       } else {
         // Split-K reduce-scatter over DSMEM: every CTA parks the partial
@@ -1102,7 +1195,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           float wv[16];
-          if (valid) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv);
+          EpiOps ops;
+          ops.sb = s_bias + b * 16;
+          if (act_pre) {
+            ops.ssc = s_asc + b * 16;
+            ops.ssh = s_ash + b * 16;
+          }
+          if (valid) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv, ops);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + own0 + b * 16, n, valid, wv);
         }
         __syncwarp();
@@ -1179,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b0 = smem_u32(bbuf);
       const uint32_t stage_bytes = b_stage;
       for (int item = cid; item < n_items; item += ncl) {
-        const int ni = item % n_slices;
+        const int ni = item - static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices) * n_slices;
         for (int ch = c_begin; ch < c_end; ++ch)
           for (int tg = 0; tg < tgroups; ++tg, ++b_iter) {
             const uint32_t st = bslot;
@@ -1203,6 +1302,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (p.ks > 1) cluster_sync();  // no CTA leaves while a peer may still touch its shared memory
+  if (threadIdx.x == 0 && p.gtl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(p.gtl + 2 * p.gtl_idx + 1, t);
+  }
   if (warp == 8) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kTmemCols)
@@ -1295,6 +1399,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 }  // namespace
+
+// Graph-safe launch timeline (developer instrumentation, SIGE_TC_GTL=1): every
+// k_conv_tc launch records [first CTA start, last CTA end] in a device array
+// indexed by launch order; sige_debug_conv_timeline() reads and resets it.
+constexpr int kGtlLaunches = 1024;
+static const bool g_gtl_on = std::getenv("SIGE_TC_GTL") != nullptr;
+static unsigned long long* g_gtl_buf = nullptr;  // allocated at the first instrumented launch
+static void gtl_reset() {
+  std::vector<unsigned long long> init(3 * kGtlLaunches, ~0ull);  // [start, end] pairs, then wait-done
+  for (int i = 0; i < kGtlLaunches; ++i) init[2 * i + 1] = 0;
+  SIGE_CUDA(cudaMemcpy(g_gtl_buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+}
+static int g_gtl_next = 0;
+
+int debug_conv_timeline(unsigned long long* out, int cap) {
+  if (!g_gtl_buf) return 0;
+  SIGE_CUDA(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(3 * kGtlLaunches);
+  SIGE_CUDA(cudaMemcpy(h.data(), g_gtl_buf, h.size() * 8, cudaMemcpyDeviceToHost));
+  const int n = std::min(cap, kGtlLaunches);
+  for (int i = 0; i < n; ++i) {  // out: [start, end, first wait-done] per launch
+    out[3 * i] = h[2 * i];
+    out[3 * i + 1] = h[2 * i + 1];
+    out[3 * i + 2] = h[2 * kGtlLaunches + i];
+  }
+  gtl_reset();
+  g_gtl_next = 0;
+  return n;
+}
 
 void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, ConvW* cw, cudaStream_t st) {
   const int ck = f16 ? 64 : 32;
@@ -1432,6 +1565,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     for (int i = 0; i < e.num_steps; ++i)
       if (e.kind[i] == SIGE_EPI_ACTIVATION) p.xf_act = e.act[i];
     p.xf_table = src.n * src.c;
+    p.gn_inv_count = src.gn_stats ? 1.0 / src.gn_count : 0.0;
   }
   p.xf_bytes = xform ? (2 * p.xf_table * 4 + 127) / 128 * 128 : 0;
   // Static tile count: N tile and split-K planned here; the device keeps them.
@@ -1442,7 +1576,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   if (!tiles.count_dev) {
     int nt = 0, ks = 1;
     // Shared memory left for the reduction buffer beside the minimal rings (2 A stages, 2 weight stages).
-    const long long red_cap = 225LL * 1024 - (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 -
+    const long long red_cap = static_cast<long long>(kDynSmem) - (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 -
                               p.xf_bytes - 2LL * p.a_bytes - 2LL * max_stage;
     plan_static((tiles.count + p.T - 1) / p.T, p.n_pad, p.nchunks, p.ntaps, sm_count(), no_splitk ? -1 : red_cap, &nt,
                 &ks);
@@ -1460,7 +1594,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.red_bytes = p.ks > 1 ? (p.ks - 1) * 128 * (p.nt_fixed / p.ks) * 4 : 0;
   // Ring depths: up to 4 A stages, the rest of shared memory is the B ring
   // (at least two of the largest weight stages).
-  constexpr size_t kSmemBudget = 225 * 1024;
+  constexpr size_t kSmemBudget = kDynSmem;
   const size_t fixed = (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 + p.xf_bytes + p.red_bytes;
   p.na = kMaxNA;
   auto b_room = [&] { return static_cast<long long>(kSmemBudget) - static_cast<long long>(fixed) -
@@ -1471,20 +1605,40 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
                       " B of shared memory");
   p.b_ring_bytes = static_cast<int>(std::min<long long>(b_room(), 16LL * max_stage) / 128 * 128);
   p.nb = p.b_ring_bytes / max_stage;  // (report only; the device sizes slots per N tile)
+  // Per-width tables for the device (see TcParams).
+  {
+    int prev = 0;
+    for (int i = 0; i < 5; ++i) {
+      const int c = 16 << i, nt = std::min(c, p.n_pad);
+      const bool ok = p.n_pad % nt == 0 && nt != prev;
+      p.w_nt[i] = ok ? nt : 0;
+      p.w_slices[i] = ok ? p.n_pad / nt : 1;
+      p.w_inv_slices[i] = 1.0f / static_cast<float>(p.w_slices[i]);
+      p.w_tgroups[i] = p.ntaps / p.tps[i];
+      p.w_nb[i] = ok ? std::min(kMaxNB, p.b_ring_bytes / (p.tps[i] * nt * 128)) : 0;
+      if (ok) prev = nt;
+    }
+    p.ks_log2 = p.ks == 1 ? 0 : p.ks == 2 ? 1 : p.ks == 4 ? 2 : 3;
+    for (int r = 0; r <= p.ks; ++r) p.c_lo[r] = r * p.nchunks / p.ks;
+  }
   const size_t smem = fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
   using KernelFn = void (*)(TcParams, TcMaps);
   KernelFn fn = nullptr;
+  const bool sync = !p.async_a;
+#define SIGE_TC_PICK(F, KK, SS) (sync ? k_conv_tc<F, KK, SS, true> : k_conv_tc<F, KK, SS, false>)
   if (cw.k == 1)
-    fn = f16 ? k_conv_tc<true, 1, 1> : k_conv_tc<false, 1, 1>;
+    fn = f16 ? SIGE_TC_PICK(true, 1, 1) : SIGE_TC_PICK(false, 1, 1);
   else if (cw.stride == 1)
-    fn = f16 ? k_conv_tc<true, 3, 1> : k_conv_tc<false, 3, 1>;
+    fn = f16 ? SIGE_TC_PICK(true, 3, 1) : SIGE_TC_PICK(false, 3, 1);
   else
-    fn = f16 ? k_conv_tc<true, 3, 2> : k_conv_tc<false, 3, 2>;
+    fn = f16 ? SIGE_TC_PICK(true, 3, 2) : SIGE_TC_PICK(false, 3, 2);
+#undef SIGE_TC_PICK
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    for (KernelFn f : {k_conv_tc<true, 1, 1>, k_conv_tc<false, 1, 1>, k_conv_tc<true, 3, 1>, k_conv_tc<false, 3, 1>,
-                       k_conv_tc<true, 3, 2>, k_conv_tc<false, 3, 2>})
-      SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+    for (KernelFn f : {k_conv_tc<true, 1, 1, true>, k_conv_tc<false, 1, 1, true>, k_conv_tc<true, 3, 1, true>,
+                       k_conv_tc<false, 3, 1, true>, k_conv_tc<true, 3, 2, true>, k_conv_tc<false, 3, 2, true>,
+                       k_conv_tc<true, 1, 1, false>, k_conv_tc<true, 3, 1, false>, k_conv_tc<true, 3, 2, false>})
+      SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
   });
   static unsigned long long* tl_buf = nullptr;
   static const bool timeline = std::getenv("SIGE_TC_TIMELINE") != nullptr;
@@ -1495,6 +1649,14 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   }
   static const int dbg = std::getenv("SIGE_TC_DEBUG") ? std::atoi(std::getenv("SIGE_TC_DEBUG")) : 0;
   p.dbg = dbg;
+  if (g_gtl_on) {
+    if (!g_gtl_buf) {
+      SIGE_CUDA(cudaMalloc(&g_gtl_buf, 3 * kGtlLaunches * 8));
+      gtl_reset();
+    }
+    p.gtl = g_gtl_buf;
+    p.gtl_idx = g_gtl_next++ % kGtlLaunches;
+  }
   long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
   if (p.nt_fixed) max_ctas = static_cast<long long>((tiles.count + p.T - 1) / p.T) * (p.n_pad / p.nt_fixed) * p.ks;
   const int sms = sm_count() / p.ks * p.ks;

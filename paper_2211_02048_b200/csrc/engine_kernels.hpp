@@ -123,6 +123,8 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
                     cudaStream_t st);
 // Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
 // k_pad and the TMA descriptors of `cw`).
+// Developer instrumentation (SIGE_TC_GTL=1): per-launch conv spans, read + reset.
+int debug_conv_timeline(unsigned long long* out, int cap);
 void pack_weights_tc(const float* w_dev_ref, int c_out, int c_in, int k, int f16, ConvW* cw,
                      cudaStream_t st);
 

@@ -1,0 +1,54 @@
+"""Per-launch conv spans and inter-launch gaps of one graph-replayed sparse edit
+(config 2, F16). Needs SIGE_TC_GTL=1 (device-side globaltimer stamps written by
+every k_conv_tc launch; see conv_tc.cu debug_conv_timeline)."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, ".")
+os.environ.setdefault("SIGE_TC_GTL", "1")
+import torch  # noqa: E402
+
+import paper_2211_02048_b200 as sb  # noqa: E402
+from paper_2211_02048_b200 import _capi  # noqa: E402
+
+lib = sb._lib()
+lib.sige_debug_conv_timeline.restype = C.c_int
+lib.sige_debug_conv_timeline.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+
+m = sb.Model("ddim_stack")
+c, h, w = m.in_shape
+o, e = sb.make_edit_fixture("rect1", 1, c, h, w, 7)
+eng = sb.Engine(m, math=sb.MATH_F16)
+eng.precompute(o.cuda())
+cfg = sb.default_config(dilate_full=5, min_sparse_res=64)
+ed = e.cuda()
+out = torch.empty(eng.output_shape(), device="cuda")
+for _ in range(4):
+    eng.sparse_forward(ed, config=cfg, out=out)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 3072)()
+lib.sige_debug_conv_timeline(buf, 1024)  # reset
+flush = torch.empty(128 * 1024 * 1024, device="cuda")
+flush.zero_()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+eng.sparse_forward(ed, config=cfg, out=out)
+b.record()
+torch.cuda.synchronize()
+n = lib.sige_debug_conv_timeline(buf, 1024)
+rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n) if buf[3 * i + 1]]
+t0 = rows[0][0]
+print(f"step {a.elapsed_time(b):.3f} ms (events), {len(rows)} conv launches")
+print("idx   start(us)  wait_done  end     work=end-wait  handoff=wait-prev_end")
+prev_end = None
+tot_work = tot_hand = 0.0
+for i, (s, en, wd) in enumerate(rows):
+    work = (en - wd) / 1e3
+    hand = (wd - prev_end) / 1e3 if prev_end else 0.0
+    tot_work += work
+    tot_hand += hand
+    print(f"{i:3d} {(s - t0) / 1e3:9.2f} {(wd - t0) / 1e3:9.2f} {(en - t0) / 1e3:9.2f} {work:8.2f} {hand:8.2f}")
+    prev_end = en
+print(f"sum work {tot_work:.1f} us, sum handoff (incl. non-conv kernels) {tot_hand:.1f} us, "
+      f"first->last {(rows[-1][1] - t0) / 1e3:.1f} us")
