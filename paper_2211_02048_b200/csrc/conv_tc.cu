@@ -948,44 +948,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < 4) {
     // ---------------- A producers ----------------
-    if (threadIdx.x == 0) tl_mark(p, 54);
-    pdl_wait();  // the source was written by the previous kernel
-    if (threadIdx.x == 0 && p.gtl) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMin(p.gtl + 2 * kGtlLaunchesDev + p.gtl_idx, t);
-    }
-    if (threadIdx.x == 0) tl_mark(p, 49);
     const uint32_t a0 = smem_u32(abuf0);
-    if (p.xform) {
-      // Scale-shift table of the transform, for this CTA's input channels only
-      // (its K chunks): folded from the GroupNorm statistics the previous
-      // conv's epilogue accumulated (reciprocal count from the host, rsqrt —
-      // this sits on the critical path right after the dependency wait), or
-      // copied from the chain.
-      const Src& s = p.src;
-      const int c_lo = c_begin * 64, c_hi = min(s.c, c_end * 64);
-      const int span = c_hi - c_lo;
-      const int cpg = s.gn_stats ? s.c / s.gn_groups : 1;
-      for (int i = threadIdx.x; i < s.n * span; i += kProdThreads) {
-        const int n = i / span, c = c_lo + (i - n * span);
-        float sc, sh;
-        if (s.gn_stats) {
-          const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + c / cpg);
-          const double mean = st[0] * p.gn_inv_count;
-          const float var = fmaxf(static_cast<float>(st[1] * p.gn_inv_count - mean * mean), 0.0f);
-          sc = __ldg(s.gn_gamma + c) * rsqrtf(var + s.gn_eps);
-          sh = fmaf(-static_cast<float>(mean), sc, __ldg(s.gn_beta + c));
-        } else {
-          const int off = s.epi.per_sample[0] ? n * s.c + c : c;
-          sc = __ldg(s.epi.scale[0] + off);
-          sh = __ldg(s.epi.shift[0] + off);
-        }
-        xf_scale[n * s.c + c] = sc;
-        xf_shift[n * s.c + c] = sh;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
-    }
     uint32_t a_iter = 0, it = 0, aphase = 0;
     int aslot = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
@@ -1005,6 +968,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool fast_units = F16 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
+      if (it == 0) {
+        // Everything above reads only the tile lists (IndexPlan output, complete
+        // before the previous conv started); the activations and GroupNorm
+        // statistics below were produced by the previous kernel.
+        if (threadIdx.x == 0) tl_mark(p, 54);
+        pdl_wait();  // the source / GroupNorm statistics were written by the previous kernel
+        if (threadIdx.x == 0 && p.gtl) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          atomicMin(p.gtl + 2 * kGtlLaunchesDev + p.gtl_idx, t);
+        }
+        if (threadIdx.x == 0) tl_mark(p, 49);
+        if (p.xform) {
+          // Scale-shift table of the transform, for this CTA's input channels only
+          // (its K chunks): folded from the GroupNorm statistics the previous
+          // conv's epilogue accumulated (reciprocal count from the host, rsqrt —
+          // this sits on the critical path right after the dependency wait), or
+          // copied from the chain.
+          const Src& s = p.src;
+          const int c_lo = c_begin * 64, c_hi = min(s.c, c_end * 64);
+          const int span = c_hi - c_lo;
+          const int cpg = s.gn_stats ? s.c / s.gn_groups : 1;
+          for (int i = threadIdx.x; i < s.n * span; i += kProdThreads) {
+            const int n = i / span, c = c_lo + (i - n * span);
+            float sc, sh;
+            if (s.gn_stats) {
+              const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + c / cpg);
+              const double mean = st[0] * p.gn_inv_count;
+              const float var = fmaxf(static_cast<float>(st[1] * p.gn_inv_count - mean * mean), 0.0f);
+              sc = __ldg(s.gn_gamma + c) * rsqrtf(var + s.gn_eps);
+              sh = fmaf(-static_cast<float>(mean), sc, __ldg(s.gn_beta + c));
+            } else {
+              const int off = s.epi.per_sample[0] ? n * s.c + c : c;
+              sc = __ldg(s.epi.scale[0] + off);
+              sh = __ldg(s.epi.shift[0] + off);
+            }
+            xf_scale[n * s.c + c] = sc;
+            xf_shift[n * s.c + c] = sh;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+        }
+      }
       if (p.xform) {
         // Async copy of chunk c, then transform of chunk c-1 (landed: this
         // thread's copies are complete after wait_group 1, the other
