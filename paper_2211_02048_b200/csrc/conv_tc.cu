@@ -56,7 +56,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -1066,6 +1068,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 4);
     }
+    // A CTA without items still orders its completion after the previous
+    // grid's (the next kernel's dependency wait relies on this transitively).
+    if (it == 0) pdl_wait();
     // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp < 8) {
@@ -1574,59 +1579,52 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   }
   p.xf_bytes = xform ? (2 * p.xf_table * 4 + 127) / 128 * 128 : 0;
   // Static tile count: N tile and split-K planned here; the device keeps them.
-  p.ks = 1;
-  p.nt_fixed = 0;
   static const bool no_splitk = std::getenv("SIGE_NO_SPLITK") != nullptr;
   static const int force_ks = std::getenv("SIGE_FORCE_SPLITK") ? std::atoi(std::getenv("SIGE_FORCE_SPLITK")) : 0;
-  if (!tiles.count_dev) {
-    int nt = 0, ks = 1;
-    // Shared memory left for the reduction buffer beside the minimal rings (2 A stages, 2 weight stages).
-    const long long red_cap = static_cast<long long>(kDynSmem) - (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 -
-                              p.xf_bytes - 2LL * p.a_bytes - 2LL * max_stage;
-    plan_static((tiles.count + p.T - 1) / p.T, p.n_pad, p.nchunks, p.ntaps, sm_count(), no_splitk ? -1 : red_cap, &nt,
-                &ks);
-    // Test hook: force a split (largest power of two <= the request that the geometry allows).
-    for (int f = force_ks; f > 1 && ks == 1; f >>= 1) {
-      const int ntf = std::min(p.n_pad, kMaxNTile);
-      if (f <= p.nchunks && ntf % (16 * f) == 0 && static_cast<long long>(f - 1) * 128 * (ntf / f) * 4 <= red_cap) {
-        nt = ntf;
-        ks = f;
-      }
-    }
+  static const bool no_tune = std::getenv("SIGE_NO_TUNE") != nullptr;
+  const long long rowtab_bytes = (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128;
+  // Shared memory left for the reduction buffer beside the minimal rings (2 A stages, 2 weight stages).
+  const long long red_cap =
+      static_cast<long long>(kDynSmem) - rowtab_bytes - p.xf_bytes - 2LL * p.a_bytes - 2LL * max_stage;
+  const int items_m = (tiles.count + p.T - 1) / p.T;
+
+  // Completes p for an (N tile, split) choice (nt = 0: chosen on the device);
+  // returns the dynamic shared memory size and sets the grid.
+  int grid = 1;
+  auto configure = [&](int nt, int ks) -> size_t {
     p.nt_fixed = nt;
     p.ks = ks;
-  }
-  p.red_bytes = p.ks > 1 ? (p.ks - 1) * 128 * (p.nt_fixed / p.ks) * 4 : 0;
-  // Ring depths: up to 4 A stages, the rest of shared memory is the B ring
-  // (at least two of the largest weight stages).
-  constexpr size_t kSmemBudget = kDynSmem;
-  const size_t fixed = (sizeof(int32_t) * p.phases * p.T * p.Mt + 127) / 128 * 128 + p.xf_bytes + p.red_bytes;
-  p.na = kMaxNA;
-  auto b_room = [&] { return static_cast<long long>(kSmemBudget) - static_cast<long long>(fixed) -
-                             static_cast<long long>(p.na) * p.a_bytes; };
-  while (p.na > 2 && b_room() < 2LL * max_stage) --p.na;
-  if (b_room() < 2LL * max_stage)
-    throw ConfigError("conv (tensor core): staging needs " + std::to_string(fixed + p.na * p.a_bytes + 2 * max_stage) +
-                      " B of shared memory");
-  p.b_ring_bytes = static_cast<int>(std::min<long long>(b_room(), 16LL * max_stage) / 128 * 128);
-  p.nb = p.b_ring_bytes / max_stage;  // (report only; the device sizes slots per N tile)
-  // Per-width tables for the device (see TcParams).
-  {
+    p.red_bytes = ks > 1 ? (ks - 1) * 128 * (nt / ks) * 4 : 0;
+    const size_t fixed = static_cast<size_t>(rowtab_bytes) + p.xf_bytes + p.red_bytes;
+    p.na = kMaxNA;
+    auto b_room = [&] { return static_cast<long long>(kDynSmem) - static_cast<long long>(fixed) -
+                               static_cast<long long>(p.na) * p.a_bytes; };
+    while (p.na > 2 && b_room() < 2LL * max_stage) --p.na;
+    if (b_room() < 2LL * max_stage)
+      throw ConfigError("conv (tensor core): staging needs " + std::to_string(fixed + p.na * p.a_bytes + 2 * max_stage) +
+                        " B of shared memory");
+    p.b_ring_bytes = static_cast<int>(std::min<long long>(b_room(), 16LL * max_stage) / 128 * 128);
+    p.nb = p.b_ring_bytes / max_stage;  // (report only; the device sizes slots per N tile)
     int prev = 0;
-    for (int i = 0; i < 5; ++i) {
-      const int c = 16 << i, nt = std::min(c, p.n_pad);
-      const bool ok = p.n_pad % nt == 0 && nt != prev;
-      p.w_nt[i] = ok ? nt : 0;
-      p.w_slices[i] = ok ? p.n_pad / nt : 1;
+    for (int i = 0; i < 5; ++i) {  // per-width tables for the device (see TcParams)
+      const int c = 16 << i, w = std::min(c, p.n_pad);
+      const bool ok = p.n_pad % w == 0 && w != prev;
+      p.w_nt[i] = ok ? w : 0;
+      p.w_slices[i] = ok ? p.n_pad / w : 1;
       p.w_inv_slices[i] = 1.0f / static_cast<float>(p.w_slices[i]);
       p.w_tgroups[i] = p.ntaps / p.tps[i];
-      p.w_nb[i] = ok ? std::min(kMaxNB, p.b_ring_bytes / (p.tps[i] * nt * 128)) : 0;
-      if (ok) prev = nt;
+      p.w_nb[i] = ok ? std::min(kMaxNB, p.b_ring_bytes / (p.tps[i] * w * 128)) : 0;
+      if (ok) prev = w;
     }
-    p.ks_log2 = p.ks == 1 ? 0 : p.ks == 2 ? 1 : p.ks == 4 ? 2 : 3;
-    for (int r = 0; r <= p.ks; ++r) p.c_lo[r] = r * p.nchunks / p.ks;
-  }
-  const size_t smem = fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
+    p.ks_log2 = ks == 1 ? 0 : ks == 2 ? 1 : ks == 4 ? 2 : 3;
+    for (int r = 0; r <= ks; ++r) p.c_lo[r] = r * p.nchunks / ks;
+    long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
+    if (nt) max_ctas = static_cast<long long>(items_m) * (p.n_pad / nt) * ks;
+    const int sms = sm_count() / ks * ks;
+    grid = static_cast<int>(std::max<long long>(ks, std::min<long long>(max_ctas, sms)));
+    return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
+  };
+
   using KernelFn = void (*)(TcParams, TcMaps);
   KernelFn fn = nullptr;
   const bool sync = !p.async_a;
@@ -1645,6 +1643,111 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
                        k_conv_tc<true, 1, 1, false>, k_conv_tc<true, 3, 1, false>, k_conv_tc<true, 3, 2, false>})
       SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
   });
+  static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
+  auto launch = [&](size_t smem) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na_attr = 0;
+    if (!no_pdl) {
+      attr[na_attr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na_attr].val.programmaticStreamSerializationAllowed = 1;
+      ++na_attr;
+    }
+    if (p.ks > 1) {
+      attr[na_attr].id = cudaLaunchAttributeClusterDimension;
+      attr[na_attr].val.clusterDim.x = p.ks;
+      attr[na_attr].val.clusterDim.y = 1;
+      attr[na_attr].val.clusterDim.z = 1;
+      ++na_attr;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na_attr;
+    SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
+    after_launch("k_conv_tc");
+  };
+
+  int nt_plan = 0, ks_plan = 1;
+  if (!tiles.count_dev) {
+    // Empirical plan (cuDNN-benchmark style): the first launch of a static
+    // shape outside graph capture times every (N tile, split) candidate and
+    // caches the fastest; the candidates are re-run with the same operands,
+    // which is idempotent for the modes a static launch uses (store, residual
+    // main, add) once GroupNorm-statistics accumulation is switched off for
+    // the trials. Inside a capture (or SIGE_NO_TUNE) the analytic plan is used.
+    using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
+    static std::map<Key, std::pair<int, int>> plans;
+    static std::mutex plans_mu;
+    const Key key{cw.c_in, cw.c_out, cw.k, cw.stride, tiles.count, tiles.bh, tiles.bw, f16, p.async_a, p.xform,
+                  dst.mode};
+    bool have = false;
+    {
+      std::lock_guard<std::mutex> g(plans_mu);
+      auto itp = plans.find(key);
+      if (itp != plans.end()) {
+        nt_plan = itp->second.first;
+        ks_plan = itp->second.second;
+        have = true;
+      }
+    }
+    if (!have) {
+      plan_static(items_m, p.n_pad, p.nchunks, p.ntaps, sm_count(), no_splitk ? -1 : red_cap, &nt_plan, &ks_plan);
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      SIGE_CUDA(cudaStreamIsCapturing(st, &cap));
+      const bool tunable = !no_tune && force_ks == 0 && cap == cudaStreamCaptureStatusNone &&
+                           (dst.mode == kStore || dst.mode == kResMain || dst.mode == kAddSrc);
+      if (tunable) {
+        double* const gn_saved = p.dst.gn_stats;
+        p.dst.gn_stats = nullptr;  // trials must not accumulate statistics
+        cudaEvent_t e0, e1;
+        SIGE_CUDA(cudaEventCreate(&e0));
+        SIGE_CUDA(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int ks = 1; ks <= 8; ks <<= 1) {
+          if (ks > p.nchunks || (ks > 1 && no_splitk)) break;
+          for (int c = 16; c <= kMaxNTile; c <<= 1) {
+            const int nt = std::min(c, p.n_pad);
+            if (p.n_pad % nt != 0 || nt % (16 * ks) != 0) continue;
+            if (ks > 1 && static_cast<long long>(ks - 1) * 128 * (nt / ks) * 4 > red_cap) continue;
+            const size_t sm = configure(nt, ks);
+            float ms_best = 1e30f;
+            for (int rep = 0; rep < 3; ++rep) {
+              SIGE_CUDA(cudaEventRecord(e0, st));
+              launch(sm);
+              SIGE_CUDA(cudaEventRecord(e1, st));
+              SIGE_CUDA(cudaEventSynchronize(e1));
+              float ms = 0.0f;
+              SIGE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+              ms_best = std::min(ms_best, ms);
+            }
+            if (ms_best < best * 0.98f) {  // prefer the earlier (smaller split / width) on near ties
+              best = ms_best;
+              nt_plan = nt;
+              ks_plan = ks;
+            }
+            if (nt == p.n_pad) break;
+          }
+        }
+        SIGE_CUDA(cudaEventDestroy(e0));
+        SIGE_CUDA(cudaEventDestroy(e1));
+        p.dst.gn_stats = gn_saved;
+        std::lock_guard<std::mutex> g(plans_mu);
+        plans[key] = {nt_plan, ks_plan};
+      }
+    }
+    // Test hook: force a split (largest power of two <= the request that the geometry allows).
+    for (int f = force_ks; f > 1 && ks_plan == 1; f >>= 1) {
+      const int ntf = std::min(p.n_pad, kMaxNTile);
+      if (f <= p.nchunks && ntf % (16 * f) == 0 && static_cast<long long>(f - 1) * 128 * (ntf / f) * 4 <= red_cap) {
+        nt_plan = ntf;
+        ks_plan = f;
+      }
+    }
+  }
+  const size_t smem = configure(nt_plan, ks_plan);
   static unsigned long long* tl_buf = nullptr;
   static const bool timeline = std::getenv("SIGE_TC_TIMELINE") != nullptr;
   if (timeline) {
@@ -1662,34 +1765,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     p.gtl = g_gtl_buf;
     p.gtl_idx = g_gtl_next++ % kGtlLaunches;
   }
-  long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
-  if (p.nt_fixed) max_ctas = static_cast<long long>((tiles.count + p.T - 1) / p.T) * (p.n_pad / p.nt_fixed) * p.ks;
-  const int sms = sm_count() / p.ks * p.ks;
-  const int grid = static_cast<int>(std::max<long long>(p.ks, std::min<long long>(max_ctas, sms)));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  int na_attr = 0;
-  static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
-  if (!no_pdl) {
-    attr[na_attr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na_attr].val.programmaticStreamSerializationAllowed = 1;
-    ++na_attr;
-  }
-  if (p.ks > 1) {
-    attr[na_attr].id = cudaLaunchAttributeClusterDimension;
-    attr[na_attr].val.clusterDim.x = p.ks;
-    attr[na_attr].val.clusterDim.y = 1;
-    attr[na_attr].val.clusterDim.z = 1;
-    ++na_attr;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na_attr;
-  SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
-  after_launch("k_conv_tc");
+  launch(smem);
   if (timeline) {
     static unsigned long long h[4096];
     SIGE_CUDA(cudaMemcpyAsync(h, tl_buf, sizeof h, cudaMemcpyDeviceToHost, st));

@@ -378,7 +378,16 @@ __device__ __forceinline__ bool tile_elem(const Tiles& t, int count, int c, int 
   return y < h && x < w;
 }
 
+// Programmatic dependent launch for the small kernels between convolutions:
+// wait for the previous grid (everything read here was produced by it or
+// earlier), then let the next kernel launch and run its own prologue.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_tiles_apply(Src s, Tiles t, float* __restrict__ dst, int dst_layout) {
+  pdl_enter();
   const int count = t.count_dev ? *t.count_dev : t.count;
   const long long total = static_cast<long long>(count) * t.bh * t.bw * s.c;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
@@ -392,6 +401,7 @@ __global__ void k_tiles_apply(Src s, Tiles t, float* __restrict__ dst, int dst_l
 }
 
 __global__ void k_identity_join(Src s, Tiles t, Dst d) {
+  pdl_enter();
   const int count = t.count_dev ? *t.count_dev : t.count;
   const long long total = static_cast<long long>(count) * t.bh * t.bw * d.c;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
@@ -406,6 +416,7 @@ __global__ void k_identity_join(Src s, Tiles t, Dst d) {
 }
 
 __global__ void k_restore(const RestoreJob* __restrict__ jobs, int max_tiles) {
+  pdl_enter();
   const RestoreJob j = jobs[blockIdx.y];
   const int count = min(*j.count, max_tiles);
   const long long per = static_cast<long long>(j.b) * j.b * j.c;
@@ -453,6 +464,7 @@ __global__ void k_materialize_act(Src s, void* __restrict__ dst, int half) {
 
 __global__ void k_finalize(Src r, const float* __restrict__ cached, const int32_t* __restrict__ any,
                            float* __restrict__ out) {
+  pdl_enter();
   const bool use = *any != 0;
   const long long total = static_cast<long long>(r.n) * r.c * r.h * r.w;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
@@ -586,6 +598,20 @@ void launch_bn_fold(int c, float eps, const float* gamma, const float* beta, con
   after_launch("k_bn_fold");
 }
 
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SIGE_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
 void launch_materialize_act(const Src& src, void* dst, int half, cudaStream_t st) {
   const long long total = static_cast<long long>(src.n) * src.c * src.h * src.w;
   Src s = src;
@@ -604,14 +630,14 @@ void launch_tiles_apply(const Src& src, const Tiles& tiles, float* dst, int dst_
                         cudaStream_t st) {
   const long long total = static_cast<long long>(tiles.capacity) * tiles.bh * tiles.bw * src.c;
   if (total == 0) return;
-  k_tiles_apply<<<grid_cap(total, 256), 256, 0, st>>>(src, tiles, dst, dst_layout);
+  launch_pdl(k_tiles_apply, dim3(grid_cap(total, 256)), dim3(256), st, src, tiles, dst, dst_layout);
   after_launch("k_tiles_apply");
 }
 
 void launch_identity_join(const Src& src, const Tiles& tiles, const Dst& dst, cudaStream_t st) {
   const long long total = static_cast<long long>(tiles.capacity) * tiles.bh * tiles.bw * dst.c;
   if (total == 0) return;
-  k_identity_join<<<grid_cap(total, 256), 256, 0, st>>>(src, tiles, dst);
+  launch_pdl(k_identity_join, dim3(grid_cap(total, 256)), dim3(256), st, src, tiles, dst);
   after_launch("k_identity_join");
 }
 
@@ -619,14 +645,14 @@ void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_elems_per_
                     cudaStream_t st) {
   if (num_jobs == 0) return;
   const int gx = std::min(grid_cap(max_elems_per_job, 256), 64);
-  k_restore<<<dim3(gx, num_jobs), 256, 0, st>>>(jobs_dev, 1 << 30);
+  launch_pdl(k_restore, dim3(gx, num_jobs), dim3(256), st, jobs_dev, 1 << 30);
   after_launch("k_restore");
 }
 
 void launch_finalize(const Src& result, const float* cached_final, const int32_t* any, float* out,
                      cudaStream_t st) {
   const long long total = static_cast<long long>(result.n) * result.c * result.h * result.w;
-  k_finalize<<<grid_cap(total, 256), 256, 0, st>>>(result, cached_final, any, out);
+  launch_pdl(k_finalize, dim3(grid_cap(total, 256)), dim3(256), st, result, cached_final, any, out);
   after_launch("k_finalize");
 }
 
