@@ -95,6 +95,7 @@ struct TcParams {
   int na, nb;     // A / B ring stages in use
   int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
   int xform;      // 1: async + in-shared-memory transform: [scale-shift (table), act] applied after landing
+  int tma_a;      // 1: A windows by TMA (one 4-D box per tile and 16-byte channel group), see launch_conv_tc
   int xf_act;     // activation of the transform chain
   int xf_table;   // floats per table (n * C) of the scale-shift table in shared memory
   double gn_inv_count;  // 1 / values per (n, group) of the GroupNorm-from-statistics source
@@ -224,6 +225,15 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
       "[%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -862,7 +872,8 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
 // buffer) are built without it — half the code, fewer cold instruction fetches.
 template <bool F16, int K, int S, bool SYNC>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps) {
+    k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps,
+              const __grid_constant__ CUtensorMap amap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[kMaxNA], bar_afree[kMaxNA];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
@@ -900,7 +911,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_bempty[i], 1);
     }
     for (int i = 0; i < p.na; ++i) {
-      mbar_init(&bar_afull[i], kProdThreads);
+      mbar_init(&bar_afull[i], p.tma_a ? 1 : kProdThreads);
       mbar_init(&bar_afree[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -967,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
       int unit_n[kUnitRegs];
-      const bool fast_units = F16 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
+      const bool fast_units = F16 && p.async_a && !p.tma_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
       if (it == 0) {
@@ -1012,7 +1023,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
         }
       }
-      if (p.xform) {
+      if (p.tma_a) {
+        // One thread streams the item's windows: per chunk one 4-D box
+        // (8 channels x window) per tile and 16-byte channel group, landing
+        // as that group's rows (pitch = window width = P); out-of-canvas
+        // cells and channels >= C come back zero-filled (gather's zero fill).
+        if (threadIdx.x == 0) {
+          const uint32_t bytes = static_cast<uint32_t>(nt * 8 * p.win_h * p.win_w * 16);
+          for (int ch = c_begin; ch < c_end; ++ch, ++a_iter) {
+            const int sidx = aslot;
+            if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
+            if (++aslot == p.na) {
+              aslot = 0;
+              aphase ^= 1;
+            }
+            mbar_expect_tx(&bar_afull[sidx], bytes);
+            const uint32_t base = a0 + sidx * p.a_bytes;
+            for (int t = 0; t < nt; ++t) {
+              const int4 tl = s_tile[t];
+              for (int g = 0; g < 8; ++g)
+                tma_4d(base + g * p.lbo_a + t * p.Mt * 16, &amap, ch * 64 + g * 8, tl.z, tl.y, tl.x,
+                       &bar_afull[sidx]);
+            }
+            if (it == 0 && ch - c_begin < 8) tl_mark(p, 14 + ch - c_begin);
+          }
+        } else {
+          a_iter += c_end - c_begin;
+        }
+      } else if (p.xform) {
         // Async copy of chunk c, then transform of chunk c-1 (landed: this
         // thread's copies are complete after wait_group 1, the other
         // producers' after the named barrier), fence, arrive. Drained at the
@@ -1570,6 +1608,34 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     p.src = src;
   }
   p.xform = xform ? 1 : 0;
+  // TMA windows: F16 fp16 channels-last sources streamed as-is (no chain, no
+  // upsample), stride 1 — one box per (tile, 16-byte channel group).
+  CUtensorMap amap{};
+  p.tma_a = 0;
+  // Off by default: with 16-byte inner boxes the TMA path measured no faster
+  // than the per-thread cp.async ring on config 2 (profiles/r1_*); SIGE_TMA_A=1 enables it.
+  static const bool use_tma_a = std::getenv("SIGE_TMA_A") != nullptr;
+  if (use_tma_a && f16 && p.async_a && !xform && cw.stride == 1 && p.src.up == 0 && p.src.half && p.phases == 1) {
+    const Src& a = p.src;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.w),
+                                static_cast<cuuint64_t>(a.h), static_cast<cuuint64_t>(a.n)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c) * 2, static_cast<cuuint64_t>(a.w) * a.c * 2,
+                                   static_cast<cuuint64_t>(a.h) * a.w * a.c * 2};
+    const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(p.win_w), static_cast<cuuint32_t>(p.win_h), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<float*>(a.ptr), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS && p.win_w * p.win_h <= p.Mt) {
+      p.tma_a = 1;
+      // TMA destinations must be 128-byte aligned: group planes a multiple of
+      // 8 rows apart (the odd pitch only helped the per-thread staging stores).
+      int rows = p.phases * p.T * p.Mt + pad_rows + 8;
+      rows = (rows + 7) / 8 * 8;
+      p.lbo_a = static_cast<uint32_t>(rows * 16);
+      p.a_bytes = (rows * 16 * 8 + 1023) / 1024 * 1024;
+    }
+  }
   p.xf_act = SIGE_ACT_NONE;
   if (xform) {
     for (int i = 0; i < e.num_steps; ++i)
@@ -1625,7 +1691,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
   };
 
-  using KernelFn = void (*)(TcParams, TcMaps);
+  using KernelFn = void (*)(TcParams, TcMaps, CUtensorMap);
   KernelFn fn = nullptr;
   const bool sync = !p.async_a;
 #define SIGE_TC_PICK(F, KK, SS) (sync ? k_conv_tc<F, KK, SS, true> : k_conv_tc<F, KK, SS, false>)
@@ -1666,7 +1732,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     }
     cfg.attrs = attr;
     cfg.numAttrs = na_attr;
-    SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps));
+    SIGE_CUDA(cudaLaunchKernelEx(&cfg, fn, p, cw.maps, amap));
     after_launch("k_conv_tc");
   };
 
