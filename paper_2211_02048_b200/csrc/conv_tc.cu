@@ -1529,13 +1529,16 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
       src.gn_stats ? (e.num_steps == 0 || (e.num_steps == 1 && e.kind[0] == SIGE_EPI_ACTIVATION))
                    : (e.num_steps >= 1 && e.num_steps <= 2 && e.kind[0] == SIGE_EPI_SCALE_SHIFT &&
                       (e.num_steps == 1 || e.kind[1] == SIGE_EPI_ACTIVATION));
-  const bool twin_ok = f16 && src.twin && src.layout == kNHWC && !src.half && src.c == cw.c_in && src.c % 8 == 0;
+  const int twin_c = src.twin_c ? src.twin_c : src.c;
+  const bool twin_ok = f16 && src.twin && !src.half && src.c == cw.c_in && twin_c % 8 == 0;
   bool xform = twin_ok && chain_ok && cw.stride == 1 && static_cast<long long>(src.n) * src.c <= 4096;
   if (src.gn_stats && !xform)
     throw ConfigError("conv (tensor core): GroupNorm-from-statistics source needs the F16 transform path");
   if (twin_ok && (e.num_steps == 0 || xform)) {
-    p.src.ptr = static_cast<const float*>(src.twin);  // stream the fp16 twin
+    p.src.ptr = static_cast<const float*>(src.twin);  // stream the fp16 twin (channels-last)
     p.src.half = 1;
+    p.src.layout = kNHWC;
+    p.src.c = twin_c;  // padded channels are zero (and have zero weights)
   }
   p.tiles = tiles;
   p.dst = dst;
@@ -1596,8 +1599,8 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   // 1e-2 bar), so TF32 stages synchronously with cvt.rna like every
   // converting / chained source.
   const int unit_ch = f16 ? 8 : 4;
-  p.async_a = f16 && p.src.layout == kNHWC && (p.src.epi.num_steps == 0 || xform) && p.src.c == cw.c_in &&
-                      p.src.c % unit_ch == 0 && p.src.half != 0
+  p.async_a = f16 && p.src.layout == kNHWC && (p.src.epi.num_steps == 0 || xform) && p.src.c >= cw.c_in &&
+                      (p.src.c == cw.c_in || !xform) && p.src.c % unit_ch == 0 && p.src.half != 0
                   ? 1
                   : 0;
   if (xform && p.phases * p.T * p.Mt * 8 > kUnitRegs * kProdThreads) {

@@ -229,6 +229,29 @@ void Engine::attach_twin(DevTensor& t, const std::string& key) {
   if (wants_twin(key, t.layout, t.half) && !t.h16) t.h16 = alloc(t.numel() * 2);
 }
 
+// The NCHW input as a Src; in F16 mode with its fp16 channels-last twin
+// (converted here when `convert`, i.e. outside the captured step).
+Src Engine::input_src(const float* ptr, cudaStream_t st, bool convert) {
+  DevTensor in;
+  in.p = const_cast<float*>(ptr);
+  in.n = batch_;
+  in.c = in_c_;
+  in.h = in_h_;
+  in.w = in_w_;
+  in.layout = kNCHW;
+  Src s = plain(in);
+  if (math_ == SIGE_MATH_F16) {
+    if (!in_twin_) {
+      in_twin_c_ = (in_c_ + 7) / 8 * 8;
+      in_twin_ = alloc(static_cast<size_t>(batch_) * in_h_ * in_w_ * in_twin_c_ * 2);
+    }
+    if (convert) launch_input_twin(ptr, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, st);
+    s.twin = in_twin_;
+    s.twin_c = in_twin_c_;
+  }
+  return s;
+}
+
 void Engine::force_twin(DevTensor& t) {
   if (math_ == SIGE_MATH_F16 && t.layout == kNHWC && !t.half && !t.h16) t.h16 = alloc(t.numel() * 2);
 }
@@ -611,14 +634,7 @@ void Engine::precompute(const float* original, int step, cudaStream_t st) {
 }
 
 void Engine::dense_forward(const float* input, bool reused, int step, float* out, cudaStream_t st) {
-  DevTensor in;
-  in.p = const_cast<float*>(input);
-  in.n = batch_;
-  in.c = in_c_;
-  in.h = in_h_;
-  in.w = in_w_;
-  in.layout = kNCHW;
-  dense_walk(plain(in), step, false, reused, out, st);
+  dense_walk(input_src(input, st, true), step, false, reused, out, st);
 }
 
 // ------------------------------------------------------ cache exchange --
@@ -814,8 +830,15 @@ struct ProgramBuilder {
     int blocks_entry = -1;
     Engine* eng = &E;
     // Source pointer resolution at launch time for steps that read the input.
-    auto bind = [eng](Src s, bool is_input) {
-      if (is_input) s.ptr = eng->cur_in_;
+    // The first layers read the per-call input (and, in F16, its fp16 twin
+    // written by k_input_twin at the start of the call).
+    const Src in_src = E.input_src(nullptr, nullptr, false);
+    auto bind = [eng, in_src](Src s, bool is_input) {
+      if (is_input) {
+        s.ptr = eng->cur_in_;
+        s.twin = in_src.twin;
+        s.twin_c = in_src.twin_c;
+      }
       return s;
     };
     for (size_t i = 0; i < E.layers_.size(); ++i) {
@@ -1158,6 +1181,7 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
   }
   launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
               static_cast<int>(P.entries.size()), st);
+  if (in_twin_) launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, st);
   for (auto& f : P.steps) f(st);
   if (!P.restores.empty())
     launch_restore(P.restores_dev, static_cast<int>(P.restores.size()),

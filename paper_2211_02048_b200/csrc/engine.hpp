@@ -110,6 +110,11 @@ class Engine {
     return math_ == SIGE_MATH_F16 && L.norm_kind != SIGE_NORM_BATCH;
   }
   double* dense_stats_ = nullptr;  // statistics arena of dense walks (zeroed per walk)
+  // F16: fp16 channels-last copy of the current input (channels padded to 8),
+  // written by k_input_twin at the start of each call; the first conv streams it.
+  void* in_twin_ = nullptr;
+  int in_twin_c_ = 0;
+  Src input_src(const float* ptr, cudaStream_t st, bool convert);
   size_t dense_stats_len_ = 0;
   size_t stats_len() const;        // doubles needed by all ResBlocks of the model
   DevNorm& norm_slot(int step, const std::string& key, int np);

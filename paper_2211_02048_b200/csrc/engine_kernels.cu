@@ -491,6 +491,20 @@ __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b, 
   }
 }
 
+__global__ void k_input_twin(const float* __restrict__ in, int n, int c, int h, int w, int c_pad,
+                             __half* __restrict__ out) {
+  pdl_enter();
+  const long long total = static_cast<long long>(n) * h * w * c_pad;
+  const long long hw = static_cast<long long>(h) * w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int ch = static_cast<int>(q % c_pad);
+    const long long p = q / c_pad;  // (n, pixel)
+    const long long nn = p / hw, pix = p - nn * hw;
+    out[q] = ch < c ? __float2half_rn(__ldg(in + (nn * c + ch) * hw + pix)) : __float2half_rn(0.0f);
+  }
+}
+
 __global__ void k_to_half(const float* __restrict__ a, __half* __restrict__ o, long long n) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x)
@@ -664,6 +678,13 @@ void launch_add_h(const float* a, const float* b, float* out, void* out_h16, siz
   k_add<<<grid_cap(static_cast<long long>(n), 256), 256, 0, st>>>(a, b, out, static_cast<__half*>(out_h16),
                                                                   static_cast<long long>(n));
   after_launch("k_add");
+}
+
+void launch_input_twin(const float* in, int n, int c, int h, int w, int c_pad, void* out, cudaStream_t st) {
+  const long long total = static_cast<long long>(n) * h * w * c_pad;
+  launch_pdl(k_input_twin, dim3(grid_cap(total, 256)), dim3(256), st, in, n, c, h, w, c_pad,
+             static_cast<__half*>(out));
+  after_launch("k_input_twin");
 }
 
 void launch_to_half(const float* src, void* dst_h16, size_t n, cudaStream_t st) {

@@ -31,6 +31,7 @@ struct Src {
   // fp16 channels-last copy of the same values (F16 mode): the tensor-core
   // conv streams it with cp.async when no element-wise chain is pending.
   const void* twin = nullptr;
+  int twin_c = 0;  // channel stride of the twin (>= c, zero-padded; 0 = c)
   // GroupNorm folded from raw statistics (F16 dense-fallback ResBlocks): when
   // gn_stats != nullptr the chain is [scale-shift from (sum, sum of squares)
   // per (n, group) in doubles, then `epi`]; scale = gamma / sqrt(var + eps),
@@ -188,6 +189,9 @@ void launch_finalize(const Src& result, const float* cached_final, const int32_t
 void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st);
 // Same, also writing out_h16 = fp16(out) when out_h16 != nullptr.
 void launch_add_h(const float* a, const float* b, float* out, void* out_h16, size_t n, cudaStream_t st);
+// NCHW fp32 (n, c, h, w) -> NHWC fp16 with the channels zero-padded to c_pad
+// (the fp16 twin of the edited input that the first convolution streams).
+void launch_input_twin(const float* in, int n, int c, int h, int w, int c_pad, void* out, cudaStream_t st);
 // dst_h16 = fp16(src) elementwise (same layout).
 void launch_to_half(const float* src, void* dst_h16, size_t n, cudaStream_t st);
 // Layout conversions.
