@@ -109,6 +109,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def conv_traffic():
+    """DRAM bytes per k_conv_tc launch (read + write) from the committed ncu
+    capture of one sparse step (profiles/r1_conv_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_conv_traffic.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -405,7 +415,7 @@ def main_ours(args):
                      "achieved": round(achieved_tf, 3), "peak": bf16_peak, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / bf16_peak, 5), "peak_source": f"dense bf16 cuBLAS, {peak_src}",
                      "launches_per_step": n_conv, "conv_ms_per_step": round(conv_ms, 4),
-                     "algorithmic_flops_per_step": conv_flops, "traffic": None},
+                     "algorithmic_flops_per_step": conv_flops, "traffic": conv_traffic()},
         "clocks": clocks,
     }
     if world == 1:
