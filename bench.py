@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--math", default="f16", choices=["f16", "tf32", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-edits", type=int, default=2)
+    ap.add_argument("--requests", type=int, default=8, help="independent requests in flight on one GPU (config 5)")
     return ap.parse_args()
 
 
@@ -183,6 +184,57 @@ def ops_roofline(sb, torch, hbm_peak, reps=20):
     out["workload"] = f"batch {n} x {c}x{h}x{w} fp32, 30% edit, {G} tiles b={b}, L2 flushed"
     del blocks
     return out
+
+
+# --------------------------------------------------- batched requests --
+
+def batched_requests(sb, torch, model, cfg, math, R=8, rounds=10, sms=None):
+    """BASELINE config 5 on one GPU: R independent edit requests (own original,
+    own edit from seed 7 + i, own cache) in flight together, one CUDA stream
+    and one graph-replayed sparse_forward per request per round. Throughput =
+    R edits / round time (CUDA events on a joining stream, L2 flushed)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    c, h, w = model.in_shape
+    engines, streams, inputs, outs = [], [], [], []
+    for i in range(R):
+        o, e = sb.make_edit_fixture(WORKLOAD["fixture"], 1, c, h, w, WORKLOAD["seed"] + i)
+        eng = sb.Engine(model, batch=1, math=math)
+        if sms:
+            eng.set_sm_budget(sms)  # the requests' latency-bound kernels share the SMs
+        eng.precompute(o.to(dev))
+        engines.append(eng)
+        streams.append(torch.cuda.Stream())
+        inputs.append(e.to(dev))
+        outs.append(torch.empty(eng.output_shape(), device=dev))
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    main = torch.cuda.current_stream()
+
+    def one_round():
+        for st in streams:  # fork: every request stream starts after the flush
+            st.wait_stream(main)
+        for eng, st, x, y in zip(engines, streams, inputs, outs):
+            with torch.cuda.stream(st):
+                eng.sparse_forward(x, config=cfg, out=y)
+        for st in streams:  # join
+            main.wait_stream(st)
+
+    for _ in range(3):
+        one_round()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(rounds):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(main)
+        one_round()
+        b.record(main)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = sum(ts) / len(ts)
+    return {"requests_per_gpu": R, "sm_budget_per_request": sms, "ms_per_round": round(ms, 4),
+            "edits_per_s": round(R * 1e3 / ms, 1),
+            "ms_per_edit_amortised": round(ms / R, 4),
+            "workload": "config 5 on one GPU: independent requests, one stream + graph each, L2 flushed per round"}
 
 
 # ------------------------------------------------------------ reference --
@@ -418,6 +470,14 @@ def main_ours(args):
                      "algorithmic_flops_per_step": conv_flops, "traffic": conv_traffic()},
         "clocks": clocks,
     }
+    if world == 1 and args.requests > 1:
+        try:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            # measured best on B200 (tools/requests.py): 8 requests x 1/4 of the SMs each
+            line["batched_requests"] = batched_requests(sb, torch, model, cfg, math, R=args.requests,
+                                                        sms=max(1, sms // 4))
+        except Exception as e:  # report, never hide
+            line["batched_requests"] = {"error": str(e)}
     if world == 1:
         try:
             line["ops_hbm"] = ops_roofline(sb, torch, hbm_peak)

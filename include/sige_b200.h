@@ -298,6 +298,12 @@ int sige_engine_set_profiling(sige_engine* eng, int enable);
  * each (edited, mask, out) pointer binding is captured once and replayed with a
  * single graph launch. Results are identical either way. */
 int sige_engine_set_graphs(sige_engine* eng, int enable);
+/* SM budget of this engine's launches (0 = every SM): with several engines
+ * (independent requests) in flight on one GPU each launch sizes its grid and
+ * N tile for its share, so the requests' latency-bound kernels run side by
+ * side instead of each filling the GPU. No reference counterpart (the
+ * reference runs one request per call, graph.hpp:224-226). */
+int sige_engine_set_sm_budget(sige_engine* eng, int sms);
 int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows,
                              sige_stream_t stream);
 /* Newline-separated cache listing for `step`: "T <key> <n> <c> <h> <w>" for

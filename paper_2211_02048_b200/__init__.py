@@ -430,6 +430,10 @@ class Engine:
         _check(_lib().sige_engine_trace(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
         return rows[: n.value].clone()
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Launch grids sized for `sms` SMs (0 = all): several engines in flight share the GPU."""
+        _check(_lib().sige_engine_set_sm_budget(self.h, int(sms)))
+
     def set_graphs(self, on: bool) -> None:
         _check(_lib().sige_engine_set_graphs(self.h, int(on)))
 

@@ -187,6 +187,7 @@ SYMBOLS = {
     "sige_engine_cache_bytes": (_sz, [_vp]),
     "sige_engine_set_profiling": (_i, [_vp, _i]),
     "sige_engine_set_graphs": (_i, [_vp, _i]),
+    "sige_engine_set_sm_budget": (_i, [_vp, _i]),
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),

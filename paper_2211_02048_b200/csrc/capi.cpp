@@ -408,6 +408,10 @@ int sige_engine_set_profiling(sige_engine* eng, int enable) {
   return guarded([&] { eng->impl->set_profiling(enable != 0); });
 }
 
+int sige_engine_set_sm_budget(sige_engine* eng, int sms) {
+  return guarded([&] { eng->impl->set_sm_budget(sms); });
+}
+
 int sige_engine_set_graphs(sige_engine* eng, int enable) {
   return guarded([&] { eng->impl->set_graphs(enable != 0); });
 }

@@ -1516,7 +1516,9 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
 }
 
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st) {
+                    cudaStream_t st, int sm_budget) {
+  const int sms_all = sm_count();
+  const int sms_use = sm_budget > 0 ? std::min(sm_budget, sms_all) : sms_all;
   if (!cw.w_tc) throw ConfigError("conv (tensor core): weights were not packed for this path");
   if (tiles.capacity == 0) return;
   TcParams p{};
@@ -1589,7 +1591,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   int max_stage = 0;
   const int sizes[5] = {16, 32, 64, 128, 256};
   for (int i = 0; i < 5; ++i) max_stage = std::max(max_stage, p.tps[i] * std::min(sizes[i], p.n_pad) * 128);
-  p.min_items = sm_count();
+  p.min_items = sms_use;
   const uint32_t fmt = f16 ? 0u : 2u;
   p.idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(128 >> 4) << 24);
   // A staged by cp.async when the source already holds the MMA operand —
@@ -1689,7 +1691,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     for (int r = 0; r <= ks; ++r) p.c_lo[r] = r * p.nchunks / ks;
     long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
     if (nt) max_ctas = static_cast<long long>(items_m) * (p.n_pad / nt) * ks;
-    const int sms = sm_count() / ks * ks;
+    const int sms = std::max(ks, sms_use / ks * ks);
     grid = static_cast<int>(std::max<long long>(ks, std::min<long long>(max_ctas, sms)));
     return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
   };
@@ -1747,11 +1749,11 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     // which is idempotent for the modes a static launch uses (store, residual
     // main, add) once GroupNorm-statistics accumulation is switched off for
     // the trials. Inside a capture (or SIGE_NO_TUNE) the analytic plan is used.
-    using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
+    using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int, int>;
     static std::map<Key, std::pair<int, int>> plans;
     static std::mutex plans_mu;
     const Key key{cw.c_in, cw.c_out, cw.k, cw.stride, tiles.count, tiles.bh, tiles.bw, f16, p.async_a, p.xform,
-                  dst.mode};
+                  dst.mode, sms_use};
     bool have = false;
     {
       std::lock_guard<std::mutex> g(plans_mu);
@@ -1763,7 +1765,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
       }
     }
     if (!have) {
-      plan_static(items_m, p.n_pad, p.nchunks, p.ntaps, sm_count(), no_splitk ? -1 : red_cap, &nt_plan, &ks_plan);
+      plan_static(items_m, p.n_pad, p.nchunks, p.ntaps, sms_use, no_splitk ? -1 : red_cap, &nt_plan, &ks_plan);
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
       SIGE_CUDA(cudaStreamIsCapturing(st, &cap));
       const bool tunable = !no_tune && force_ks == 0 && cap == cudaStreamCaptureStatusNone &&

@@ -416,7 +416,7 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     SIGE_CUDA(cudaEventRecord(rec.a, st));
   }
   if (tensor_cores())
-    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st);
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
   if (profiling_) {
@@ -1189,6 +1189,12 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
 }
 
 void Engine::set_graphs(bool on) { use_graphs_ = on; }
+
+void Engine::set_sm_budget(int sms) {
+  if (sms < 0) throw ConfigError("engine: SM budget must be >= 0");
+  if (sms != sm_budget_) invalidate_programs();  // captured launches carry the old grids
+  sm_budget_ = sms;
+}
 
 int Engine::trace(uint64_t* rows, int cap, cudaStream_t st) {
   if (!last_program_) return 0;

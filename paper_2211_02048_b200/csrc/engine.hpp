@@ -82,6 +82,7 @@ class Engine {
   size_t cache_bytes() const;
   void set_profiling(bool on);
   void set_graphs(bool on);
+  void set_sm_budget(int sms);
   int profile_read(double* rows, int cap, cudaStream_t st);
   std::string cache_entries(int step) const;
   int in_channels() const { return in_c_; }
@@ -139,6 +140,7 @@ class Engine {
   void run_program(Program& P, const float* edited, const uint8_t* mask, const sige_run_config& cfg,
                    cudaStream_t st);
   bool use_graphs_ = true;
+  int sm_budget_ = 0;  // 0 = every SM
   cudaStream_t cap_stream_ = nullptr;
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
 

@@ -121,7 +121,7 @@ void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, cons
 // Same contract on tcgen05 tensor cores (kind::tf32, fp32 TMEM accumulators).
 // conv_tc.cu.
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st);
+                    cudaStream_t st, int sm_budget = 0);
 // Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
 // k_pad and the TMA descriptors of `cw`).
 // Developer instrumentation (SIGE_TC_GTL=1): per-launch conv spans, read + reset.
