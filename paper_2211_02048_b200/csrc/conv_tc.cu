@@ -665,7 +665,29 @@ struct EpiOps {
   const float* ssc = nullptr;  // act scale-shift step 0 params [16] (shared), or nullptr
   const float* ssh = nullptr;
   const float* aux = nullptr;  // residual / addend operand [16] (registers), or nullptr
+  bool join = false;           // kResMain: this pixel lies in an active shortcut tile (fused identity join)
 };
+
+__device__ __forceinline__ bool tile_active(const uint32_t* bm, int b, int w, int y, int x) {
+  const int tx = (w + b - 1) / b;
+  const int t = (y / b) * tx + x / b;
+  return (__ldg(bm + (t >> 5)) >> (t & 31)) & 1u;
+}
+
+// x - aux for 16 channels of the block input at (n, y, x) (identity join term).
+__device__ __forceinline__ void join_term(const Dst& d, int n, int y, int x, int oc0, const float* aux, float* out) {
+  const Src& s = d.join_x;
+  if (s.layout == kNHWC && !s.half && s.up == 0 && s.epi.num_steps == 0 && (s.c & 3) == 0) {
+    const float* src = s.ptr + ((static_cast<size_t>(n) * s.h + y) * s.w + x) * s.c + oc0;
+    float xv[16];
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) ld4(src + j, xv + j);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = __fsub_rn(xv[j], aux[j]);
+  } else {
+    for (int j = 0; j < 16; ++j) out[j] = __fsub_rn(tc_epi(s.epi, src_raw(s, n, oc0 + j, y, x), oc0 + j, s.c, n), aux[j]);
+  }
+}
 
 __device__ __forceinline__ bool addend_vectorizable(const Dst& d) {
   return d.mode != kAddSrc || (d.addend.layout == kNHWC && !d.addend.half && d.addend.up == 0 &&
@@ -716,6 +738,12 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+      if (ops.join) {  // out = (m + sc_orig) + (x - sc_orig), the reference's order
+        float jt[16];
+        join_term(d, n, y, x, oc0, t, jt);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], jt[j]);
+      }
     }
   }
 #pragma unroll
@@ -1153,6 +1181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));
       }
       const bool pre_aux = valid && p.dst.mode != kStore && addend_vectorizable(p.dst) && (p.dst.c & 3) == 0;
+      const bool in_join = p.dst.join_bm && valid && tile_active(p.dst.join_bm, p.dst.join_b, p.dst.w, y, x);
       float aux_next[16];
       if (pre_aux && ni * n_tile + own0 + 16 <= p.c_out) {
         const float* src = aux_ptr(p.dst, pix, n, y, x, ni * n_tile + own0);
@@ -1185,6 +1214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ops.ssh = s_ash + cb;
           }
           ops.aux = pre_aux && oc + 16 <= p.c_out ? aux_cur : nullptr;
+          ops.join = in_join;
           float wv[16];
           if (valid) out16(p, pix, n, y, x, oc, v, wv, ops);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid, wv);
@@ -1249,6 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ops.ssc = s_asc + b * 16;
             ops.ssh = s_ash + b * 16;
           }
+          ops.join = in_join;
           if (valid) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv, ops);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + own0 + b * 16, n, valid, wv);
         }
@@ -1261,6 +1292,65 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
       if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 6);
+    }
+    // Join phase (fused identity shortcut): shortcut-tile pixels outside every
+    // active main tile — disjoint from the pixels the conv items wrote — get
+    // dst += x - aux (kernels.cpp:320-334); units = (pixel, 16 channels).
+    if (p.dst.join_bm) {
+      const Dst& d = p.dst;
+      const int jcount = d.join_tiles.count_dev ? *d.join_tiles.count_dev : d.join_tiles.count;
+      const int jb = d.join_b, per = jb * jb, cbl = (p.c_out + 15) / 16;
+      const long long total = static_cast<long long>(jcount) * per * cbl;
+      for (long long u = static_cast<long long>(blockIdx.x) * kEpiThreads + (threadIdx.x - kProdThreads); u < total;
+           u += static_cast<long long>(gridDim.x) * kEpiThreads) {
+        const int g = static_cast<int>(u / (per * cbl));
+        const int rem = static_cast<int>(u - static_cast<long long>(g) * per * cbl);
+        const int cell = rem / cbl, oc0 = (rem - cell * cbl) * 16;
+        const int n = __ldg(d.join_tiles.idx + 3 * g), y = __ldg(d.join_tiles.idx + 3 * g + 1) + cell / jb,
+                  x = __ldg(d.join_tiles.idx + 3 * g + 2) + cell % jb;
+        if (y >= d.h || x >= d.w || tile_active(d.main_bm, d.main_b, d.w, y, x)) continue;
+        const size_t at = ((static_cast<size_t>(n) * d.h + y) * d.w + x) * d.c + oc0;
+        const int cnt = min(16, p.c_out - oc0);
+        float v[16], a[16], jt[16];
+        if (cnt == 16 && (d.c & 3) == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            const float4 c4 = *reinterpret_cast<const float4*>(d.ptr + at + j);
+            v[j] = c4.x, v[j + 1] = c4.y, v[j + 2] = c4.z, v[j + 3] = c4.w;
+            ld4(d.aux + at + j, a + j);
+          }
+          join_term(d, n, y, x, oc0, a, jt);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], jt[j]);
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) st4(d.ptr + at + j, v + j);
+          if (d.act) {
+            tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
+            if (d.act_half) {
+              uint4* hh = reinterpret_cast<uint4*>(static_cast<__half*>(d.act) + at);
+              hh[0] = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+              hh[1] = make_uint4(pack_h2(v[8], v[9]), pack_h2(v[10], v[11]), pack_h2(v[12], v[13]),
+                                 pack_h2(v[14], v[15]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) st4(static_cast<float*>(d.act) + at + j, v + j);
+            }
+          }
+        } else {
+          for (int j = 0; j < cnt; ++j) {
+            const float xv = tc_epi(d.join_x.epi, src_raw(d.join_x, n, oc0 + j, y, x), oc0 + j, d.join_x.c, n);
+            const float w = __fadd_rn(d.ptr[at + j], __fsub_rn(xv, __ldg(d.aux + at + j)));
+            d.ptr[at + j] = w;
+            if (d.act) {
+              const float av = tc_epi(d.act_epi, w, oc0 + j, d.c, n);
+              if (d.act_half)
+                static_cast<__half*>(d.act)[at + j] = __float2half_rn(av);
+              else
+                static_cast<float*>(d.act)[at + j] = av;
+            }
+          }
+        }
+      }
     }
   } else if (warp == 8) {
     // ---------------- MMA issuer (whole warp, converged) ----------------

@@ -765,6 +765,8 @@ struct ProgramBuilder {
     e.idx = static_cast<int32_t*>(E.alloc(static_cast<size_t>(e.capacity) * 3 * sizeof(int32_t)));
     e.count = static_cast<int32_t*>(E.alloc(sizeof(int32_t)));
     SIGE_CUDA(cudaMemset(e.count, 0, sizeof(int32_t)));
+    const int grid_tiles = ((h + b - 1) / b) * ((w + b - 1) / b);
+    e.bm = static_cast<uint32_t*>(E.alloc(static_cast<size_t>((grid_tiles + 31) / 32) * sizeof(uint32_t)));
     P.entries.push_back(e);
     return memo[key] = static_cast<int>(P.entries.size()) - 1;
   }
@@ -1035,14 +1037,30 @@ struct ProgramBuilder {
             if (!(reuse && E.use_act())) epi_push_act(mid.epi, L.act);
             Dst d2 = to_dst(ws, kResMain);
             d2.aux = osc.p;
-            conv_step(mid, tm, c2w, d2);
+            // Identity shortcut on the tensor cores: the join (graph.cpp:854-879,
+            // kernels.cpp:320-334) is fused into conv2 — no separate launch.
+            const bool fuse_join = !L.has_shortcut && E.tensor_cores();
+            if (fuse_join) {
+              d2.join_bm = P.entries[es].bm;
+              d2.main_bm = P.entries[em].bm;
+              d2.join_b = P.entries[es].b;
+              d2.main_b = P.entries[em].b;
+              d2.join_tiles = ts;
+              add([eng, mid, tm, c2w, d2, x0, fin, bind](cudaStream_t st) {
+                Dst dd = d2;
+                dd.join_x = bind(x0, fin);
+                eng->conv(mid, tm, c2w, dd, st);
+              });
+            } else {
+              conv_step(mid, tm, c2w, d2);
+            }
             restore(ws, csum, em);
             // 3. shortcut tiles (graph.cpp:854-879)
             Dst d3 = to_dst(ws, kResShortcut);
             d3.aux = osc.p;
             if (L.has_shortcut) {
               add([eng, x0, ts, scw, d3, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), ts, scw, d3, st); });
-            } else {
+            } else if (!fuse_join) {
               add([x0, ts, d3, fin, bind](cudaStream_t st) { launch_identity_join(bind(x0, fin), ts, d3, st); });
             }
             restore(ws, csum, es);

@@ -154,6 +154,7 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
     }
     const unsigned bal = __ballot_sync(0xffffffffu, on);
     if (lane == 0) warp_sums[wid] = __popc(bal);
+    if (e.bm && lane == 0 && t0 + wid * 32 < tiles) e.bm[(t0 + wid * 32) >> 5] = bal;  // tile activity bitmap
     __syncthreads();
     if (wid == 0) {
       int v = lane < nw ? warp_sums[lane] : 0;

@@ -67,6 +67,17 @@ enum OutMode : int {
   kAddSrc = 3,       // dst[p] = v + addend(p)          (dense ResBlock join add(m, sc), graph.cpp:812)
 };
 
+// The tile list a conv runs over: `count` triplets {n, r, c} (output-res
+// tile origins, BlockIndexSet order), count read from the device when
+// count_dev != nullptr (produced by the on-device IndexPlan).
+struct Tiles {
+  const int32_t* idx = nullptr;
+  const int32_t* count_dev = nullptr;
+  int count = 0;     // used when count_dev == nullptr
+  int capacity = 0;  // upper bound for grid sizing
+  int bh = 0, bw = 0;  // tile shape at output resolution (square for sparse)
+};
+
 struct Dst {
   float* ptr = nullptr;  // NHWC, (n, h, w, c)
   int n = 1, c = 0, h = 0, w = 0;
@@ -79,6 +90,16 @@ struct Dst {
   void* act = nullptr;
   int act_half = 0;
   DevEpilogue act_epi;
+  // Identity-shortcut join fused into conv2 (kResMain, kernels.cpp:320-334):
+  // main-tile pixels that also lie in an active shortcut tile get
+  // + (x - aux); the shortcut-tile pixels outside every active main tile are
+  // joined (dst += x - aux) by the same kernel's join phase. join_bm / main_bm:
+  // activity bitmaps of the shortcut (join_b) and main (main_b) tile grids.
+  const uint32_t* join_bm = nullptr;
+  const uint32_t* main_bm = nullptr;
+  int join_b = 0, main_b = 0;
+  Src join_x;    // the block input x
+  Tiles join_tiles;  // the shortcut tile list
   // Optional GroupNorm statistics of the written values: += (sum, sum of
   // squares) per (n, group) into gn_stats[2 * (n * gn_groups + g)] (doubles,
   // zeroed by the caller) — the next layer folds them (Src::gn_stats).
@@ -86,16 +107,6 @@ struct Dst {
   int gn_groups = 0;
 };
 
-// The tile list a conv runs over: `count` triplets {n, r, c} (output-res
-// tile origins, BlockIndexSet order), count read from the device when
-// count_dev != nullptr (produced by the on-device IndexPlan).
-struct Tiles {
-  const int32_t* idx = nullptr;
-  const int32_t* count_dev = nullptr;
-  int count = 0;     // used when count_dev == nullptr
-  int capacity = 0;  // upper bound for grid sizing
-  int bh = 0, bw = 0;  // tile shape at output resolution (square for sparse)
-};
 
 // TMA descriptors of a packed weight tensor, one per N-slice width
 // (16, 32, 64, 128, 256) with the taps batched per ring stage.
@@ -139,6 +150,7 @@ struct PlanEntryDev {
   int32_t* idx;    // capacity triplets
   int32_t* count;  // device int
   int capacity;
+  uint32_t* bm;    // activity bitmap of the (h/b, w/b) tile grid, row-major (shared by the batch)
 };
 // Both set *any = 1 when at least one pixel is set (the caller zeroes it).
 void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
