@@ -420,6 +420,24 @@ __global__ void k_restore(const RestoreJob* __restrict__ jobs, int max_tiles) {
   pdl_enter();
   const RestoreJob j = jobs[blockIdx.y];
   const int count = min(*j.count, max_tiles);
+  const int esz = j.half ? 2 : 4;
+  if (j.layout == kNHWC && (j.c * esz) % 16 == 0) {
+    // Channels-last: each clipped tile row is one contiguous run of
+    // (cells x C) elements — copied as 16-byte vectors, one tile per CTA pass.
+    const int vrow_full = j.b * j.c * esz / 16;
+    for (int g = blockIdx.x; g < count; g += gridDim.x) {
+      const int n = j.idx[3 * g], y0 = j.idx[3 * g + 1], x0 = j.idx[3 * g + 2];
+      const int rows = min(j.b, j.h - y0), cells = min(j.b, j.w - x0);
+      const int vrow = cells * j.c * esz / 16;
+      for (int q = threadIdx.x; q < rows * vrow_full; q += blockDim.x) {
+        const int r = q / vrow_full, v = q - r * vrow_full;
+        if (r >= rows || v >= vrow) continue;
+        const size_t off = (((static_cast<size_t>(n) * j.h + y0 + r) * j.w + x0) * j.c) * esz / 16 + v;
+        reinterpret_cast<uint4*>(j.dst)[off] = reinterpret_cast<const uint4*>(j.src)[off];
+      }
+    }
+    return;
+  }
   const long long per = static_cast<long long>(j.b) * j.b * j.c;
   const long long total = static_cast<long long>(count) * per;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
@@ -659,7 +677,9 @@ void launch_identity_join(const Src& src, const Tiles& tiles, const Dst& dst, cu
 void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_elems_per_job,
                     cudaStream_t st) {
   if (num_jobs == 0) return;
-  const int gx = std::min(grid_cap(max_elems_per_job, 256), 64);
+  // x: tiles of a job (one CTA pass per tile on the channels-last path); y: jobs.
+  const int gx = std::max(1, std::min(sm_count() * 4 / std::max(1, num_jobs) + 1, 256));
+  (void)max_elems_per_job;
   launch_pdl(k_restore, dim3(gx, num_jobs), dim3(256), st, jobs_dev, 1 << 30);
   after_launch("k_restore");
 }
