@@ -396,6 +396,34 @@ def main_ours(args):
         dts.append(a.elapsed_time(b))
     dense_ms = sum(dts) / len(dts)
 
+    # ---- dense pass through PyTorch / cuDNN (fp16 channels-last, CUDA graph)
+    dense_torch = None
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from torch_dense import TorchDense
+
+        tdn = TorchDense(model).capture(edited_d.clone())
+        for _ in range(3):
+            tdn.replay()
+        torch.cuda.synchronize()
+        tts = []
+        for _ in range(max(3, min(10, args.steps))):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            tdn.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            tts.append(a.elapsed_time(b))
+        dense_torch = sum(tts) / len(tts)
+        # agreement with the engine's dense pass (both fp16 operands)
+        ref = eng.dense_forward(edited_d)
+        dev_rel = float((tdn.out.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+        del tdn
+    except Exception as e:  # report, never hide
+        dense_torch = f"unavailable: {e}"
+        dev_rel = None
+
     # ---- e2e through the C-ABI host-buffer entry point (pinned buffers)
     edited_h = edited.pin_memory()
     out_h = torch.empty(eng.output_shape(), dtype=torch.float32).pin_memory()
@@ -454,6 +482,9 @@ def main_ours(args):
                    "parallelism": f"request-sharded x{world} (no data-path collective)"},
         "speedup_vs_dense": round(dense_ms / ms_per_step, 3),
         "dense_ms": round(dense_ms, 4),
+        "dense_cudnn_ms": round(dense_torch, 4) if isinstance(dense_torch, float) else dense_torch,
+        "speedup_vs_dense_cudnn": round(dense_torch / ms_per_step, 3) if isinstance(dense_torch, float) else None,
+        "dense_cudnn_vs_engine_max_rel": dev_rel,
         "edits_per_s": round(world * 1e3 / ms_per_step, 2),
         "gather_scatter_gbs": round(gs_bytes / (ms_per_step * 1e-3) / 1e9, 2),
         "trace": {"active_blocks": active_blocks, "gathered_elems": gathered, "scattered_elems": scattered,
