@@ -198,6 +198,14 @@ __device__ __forceinline__ float4 ld_cluster_v4(uint32_t raddr) {
                : "memory");
   return v;
 }
+// Asynchronous remote store of 16 bytes into a peer CTA's shared memory that
+// completes `bytes` on the peer's mbarrier (no fence on the sender: the
+// transaction count carries the ordering, as for TMA).
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float a, float b, float c, float d, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
 }
@@ -946,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_acc_full[i], 1);
       mbar_init(&bar_acc_empty[i], kEpiThreads);
     }
-    mbar_init(&bar_red_full, (p.ks - 1) * (kEpiThreads / 32));   // one lane per epilogue warp of every sender
+    mbar_init(&bar_red_full, 1);  // the owner's arrive.expect_tx; the peers' st.async complete the bytes
     mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1220,35 +1228,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid, wv);
         }
       } else {
-        // Split-K reduce-scatter over DSMEM: every CTA parks the partial
-        // columns each peer owns in its own shared memory (slot d-1 for the
-        // owner at distance d; layout [slot][16-col block][float4 j][row], so
-        // a warp's accesses are contiguous), signals the owners, then sums
-        // the partials of its own columns in rank order (deterministic),
-        // reading the peers' slots remotely, and runs the epilogue on them.
-        if (it > 0) mbar_wait_cluster(&bar_red_empty, (it - 1) & 1);  // owners read the previous item
-        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 53);
+        // Split-K reduce-scatter over DSMEM: every CTA stores the partial
+        // columns each peer owns straight into that peer's shared memory with
+        // st.async (slot = distance-1; layout [slot][16-col block][float4 j]
+        // [row], conflict-free), whose bytes complete the peer's red_full
+        // mbarrier — no memory fence on the critical path. The owner then sums
+        // the partials of its columns in rank order (deterministic) and runs
+        // the epilogue on them.
         const int blocks = slice / 16;
+        const uint32_t red0 = smem_u32(red_buf);
+        if (threadIdx.x == kProdThreads) {  // this owner expects (ks-1) slots of 128 rows x slice fp32
+          mbar_expect_tx(&bar_red_full, static_cast<uint32_t>((p.ks - 1) * 128 * slice * 4));
+        }
+        if (it > 0) mbar_wait_cluster(&bar_red_empty, (it - 1) & 1);  // owners consumed the previous item
+        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 53);
         for (int d = 1; d < p.ks; ++d) {
           const int owner = (rank + d) % p.ks;
-          float4* slot = reinterpret_cast<float4*>(red_buf) + static_cast<size_t>(d - 1) * blocks * 4 * 128;
+          const uint32_t rbase = mapa(red0, static_cast<uint32_t>(owner)) +
+                                 static_cast<uint32_t>((d - 1) * blocks * 4 * 128 * 16 + m * 16);
+          const uint32_t rbar = mapa(smem_u32(&bar_red_full), static_cast<uint32_t>(owner));
           for (int b = 0; b < blocks; ++b) {
             float v[16];
             tmem_ld16(tbase + static_cast<uint32_t>(owner * slice + b * 16), v);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              slot[(b * 4 + j) * 128 + m] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              st_async_v4(rbase + static_cast<uint32_t>((b * 4 + j) * 128 * 16), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                          v[4 * j + 3], rbar);
           }
         }
-        // __syncwarp orders the warp's stores before lane 0's cluster-scope release.
-        __syncwarp();
-        if (lane == 0)
-          for (int d = 1; d < p.ks; ++d)
-            mbar_arrive_remote(mapa(smem_u32(&bar_red_full), static_cast<uint32_t>((rank + d) % p.ks)));
         if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 51);
         mbar_wait_cluster(&bar_red_full, it & 1);
         if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 52);
-        const uint32_t red0 = smem_u32(red_buf);
         for (int b = 0; b < blocks; ++b) {
           float tot[16];
 #pragma unroll
@@ -1261,14 +1271,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 16; ++j) tot[j] += v[j];
             } else {
               const int d = (rank - r2 + p.ks) % p.ks;  // distance from peer r2 to this owner
-              const uint32_t base = mapa(red0, static_cast<uint32_t>(r2)) +
-                                    static_cast<uint32_t>((((d - 1) * blocks + b) * 4 * 128 + m) * 16);
-              float4 f[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) f[j] = ld_cluster_v4(base + j * 128 * 16);
+              const float4* src = reinterpret_cast<const float4*>(red_buf) + (((d - 1) * blocks + b) * 4) * 128 + m;
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                tot[4 * j] += f[j].x, tot[4 * j + 1] += f[j].y, tot[4 * j + 2] += f[j].z, tot[4 * j + 3] += f[j].w;
+                const float4 f = src[j * 128];
+                tot[4 * j] += f.x, tot[4 * j + 1] += f.y, tot[4 * j + 2] += f.z, tot[4 * j + 3] += f.w;
               }
             }
           }
@@ -1283,10 +1290,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (valid) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv, ops);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + own0 + b * 16, n, valid, wv);
         }
-        __syncwarp();
-        if (lane == 0)
-          for (int d = 1; d < p.ks; ++d)  // this owner is done with the peers' slots
-            mbar_arrive_remote(mapa(smem_u32(&bar_red_empty), static_cast<uint32_t>((rank - d + p.ks) % p.ks)));
+        // Slots free again — only needed when another item follows (its
+        // sends wait on it); the release fence is off the single-item path.
+        if (item + ncl < n_items) {
+          __syncwarp();
+          if (lane == 0)
+            for (int d = 1; d < p.ks; ++d)
+              mbar_arrive_remote(mapa(smem_u32(&bar_red_empty), static_cast<uint32_t>((rank - d + p.ks) % p.ks)));
+        }
       }
       if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 47);
       tc_fence_before();
