@@ -32,8 +32,9 @@
 // (cp.async.mbarrier.arrive), so the producers keep up to 4 K chunks in flight.
 // Other sources are staged synchronously (load, chain, convert, st.shared).
 //
-// Weights are packed [chunk][tap][group][n_pad][16 B] and streamed by TMA
-// (cp.async.bulk.tensor.3d, one copy per ring stage covering 1, 3 or 9 taps
+// Weights are packed [chunk][tap][n_pad][128-byte K row] and streamed by TMA
+// with 128-byte swizzle (whole-row requests; the MMA reads them through
+// SWIZZLE_128B descriptors) (cp.async.bulk.tensor.3d, one copy per ring stage covering 1, 3 or 9 taps
 // of an N slice) through an up-to-8-stage mbarrier ring. The N slice (16..128)
 // is chosen on the device from the live tile count so even a layer with a
 // handful of tiles fills the SMs. Two TMEM accumulators: the epilogue of item
@@ -270,6 +271,16 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// K-major SWIZZLE_128B descriptor (weights: 128-byte K rows, 8-row groups
+// 1024 bytes apart). The hardware XORs the 16-byte column with address bits
+// [7,10) of each row — the same absolute-address rule the TMA writes by — so
+// a descriptor may start at any 128-byte row or 32-byte k-step with a zero
+// base offset (checked on B200 by tools/sw128_probe.cu).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
 }
 
 template <bool F16>
@@ -856,7 +867,7 @@ __device__ __forceinline__ int nt_index(int nt) {
 
 // MMA-issue state shared by the unrolled chunk bodies (uniform across the warp).
 struct MmaCtx {
-  uint32_t a0, b0, lbo_a16, lbo_b16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
+  uint32_t a0, b0, lbo_a16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
   uint64_t adesc0, bdesc0;
   uint64_t* bar_bfull;
   uint64_t* bar_bempty;
@@ -883,7 +894,7 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
         const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * 2 * c.lbo_a16) & 0x3FFFu);
-        const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2 * c.lbo_b16) & 0x3FFFu);
+        const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2) & 0x3FFFu);
         const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
         if (elect_one()) umma<F16>(c.tmem_d, ad, bd, c.idesc, accum);
       }
@@ -986,7 +997,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_items = items_m * n_slices;
   const int tps = p.tps[nti];
   const int tgroups = p.w_tgroups[nti];
-  const uint32_t lbo_b = static_cast<uint32_t>(n_tile * 16);
   const uint32_t tap_b = static_cast<uint32_t>(n_tile * 128);  // one tap of B in smem
   const uint32_t idesc = p.idesc_base | (static_cast<uint32_t>(n_tile >> 3) << 17);
   // B ring: slots of one TMA stage (tps taps x n_tile rows x 128 B) each.
@@ -1374,9 +1384,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.a0 = smem_u32(abuf0) >> 4;
     c.b0 = smem_u32(bbuf) >> 4;
     c.adesc0 = umma_desc(0, p.lbo_a, 128);
-    c.bdesc0 = umma_desc(0, lbo_b, 128);
+    c.bdesc0 = umma_desc_sw128(0);
     c.lbo_a16 = p.lbo_a >> 4;
-    c.lbo_b16 = lbo_b >> 4;
     c.tap_b16 = tap_b >> 4;
     c.plane16 = static_cast<uint32_t>(p.T * p.Mt);
     c.bstage16 = b_stage >> 4;
@@ -1437,7 +1446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               bphase ^= 1;
             }
             mbar_expect_tx(&bar_bfull[st], stage_bytes);
-            tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, (ch * p.ntaps + tg * tps) * 8, &bar_bfull[st]);
+            tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, ch * p.ntaps + tg * tps, &bar_bfull[st]);
             if (b_iter == 0) tl_mark(p, 10);
           }
         if (item == cid) tl_mark(p, 11);
@@ -1473,20 +1482,18 @@ template <bool F16>
 __global__ void k_pack_tc(const float* __restrict__ w, int c_out, int c_in, int k, int n_pad, int nchunks,
                           void* __restrict__ out) {
   const int ntaps = k * k;
-  constexpr int kG = F16 ? 8 : 4;
-  const long long total = static_cast<long long>(nchunks) * ntaps * 8 * n_pad * kG;
+  constexpr int kRow = F16 ? 64 : 32;  // one 128-byte K row per (chunk, tap, n)
+  const long long total = static_cast<long long>(nchunks) * ntaps * n_pad * kRow;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
     long long r = q;
-    const int e = static_cast<int>(r % kG);
-    r /= kG;
+    const int e = static_cast<int>(r % kRow);
+    r /= kRow;
     const int n = static_cast<int>(r % n_pad);
     r /= n_pad;
-    const int j = static_cast<int>(r % 8);
-    r /= 8;
     const int tap = static_cast<int>(r % ntaps);
     const int ch = static_cast<int>(r / ntaps);
-    const int ic = ch * 8 * kG + j * kG + e;
+    const int ic = ch * kRow + e;
     const float v = (n < c_out && ic < c_in) ? w[(static_cast<size_t>(n) * c_in + ic) * ntaps + tap] : 0.0f;
     if constexpr (F16)
       static_cast<__half*>(out)[q] = __float2half_rn(v);
@@ -1584,7 +1591,7 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
   cw->n_pad = n_pad_for(c_out);
   cw->k_pad = (c_in + ck - 1) / ck * ck;
   const int nchunks = cw->k_pad / ck, ntaps = k * k;
-  const size_t total = static_cast<size_t>(nchunks) * ntaps * 8 * cw->n_pad * (16 / esize);
+  const size_t total = static_cast<size_t>(nchunks) * ntaps * cw->n_pad * (128 / esize);
   void* out = nullptr;
   SIGE_CUDA(cudaMalloc(&out, total * esize));
   const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, sm_count() * 16LL)));
@@ -1595,22 +1602,23 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
   after_launch("k_pack_tc");
   SIGE_CUDA(cudaStreamSynchronize(st));
   cw->w_tc = out;
-  // One 3-D tensor map per N-slice width: dims (16-byte element group, n, (chunk, tap, group)),
-  // box (group, n_tile, taps_per_stage * 8) — a ring stage is one TMA.
+  // One 3-D tensor map per N-slice width: dims (128-byte K row, n, (chunk, tap)),
+  // box (row, n_tile, taps_per_stage), 128-byte swizzle — a ring stage is one
+  // TMA of whole 128-byte rows (the MMA reads it through SWIZZLE_128B descriptors).
   const int sizes[5] = {16, 32, 64, 128, 256};
   for (int i = 0; i < 5; ++i) {
     const int nt = std::min(sizes[i], cw->n_pad);
     const int tps = tps_for(nt, ntaps);
     cw->maps.tps[i] = tps;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(16 / esize), static_cast<cuuint64_t>(cw->n_pad),
-                                static_cast<cuuint64_t>(nchunks) * ntaps * 8};
-    const cuuint64_t strides[2] = {16, static_cast<cuuint64_t>(cw->n_pad) * 16};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(16 / esize), static_cast<cuuint32_t>(nt),
-                               static_cast<cuuint32_t>(tps * 8)};
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(128 / esize), static_cast<cuuint64_t>(cw->n_pad),
+                                static_cast<cuuint64_t>(nchunks) * ntaps};
+    const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(cw->n_pad) * 128};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / esize), static_cast<cuuint32_t>(nt),
+                               static_cast<cuuint32_t>(tps)};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode_fn()(&cw->maps.m[i], f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                              3, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   }

@@ -119,7 +119,7 @@ struct ConvW {
   int c_in = 0, c_out = 0, k = 1, stride = 1;
   const float* w = nullptr;     // (c_out, c_in, k, k) reference layout
   const float* bias = nullptr;  // c_out or nullptr
-  const void* w_tc = nullptr;   // tcgen05 packing [chunk][tap][group][n_pad][16 B] (conv_tc.cu)
+  const void* w_tc = nullptr;   // tcgen05 packing [chunk][tap][n_pad][128 B K row] (conv_tc.cu)
   int n_pad = 0;                // c_out rounded up for the tensor-core N dimension
   int k_pad = 0;                // channels rounded up per tap for the K dimension
   TcMaps maps{};
