@@ -96,7 +96,8 @@ struct TcParams {
   int na, nb;     // A / B ring stages in use
   int async_a;    // 1: A staged with cp.async straight from the source (no conversion)
   int xform;      // 1: async + in-shared-memory transform: [scale-shift (table), act] applied after landing
-  int tma_a;      // 1: A windows by TMA (one 4-D box per tile and 16-byte channel group), see launch_conv_tc
+  int tma_a;      // 1: A windows by TMA (one 128-byte-swizzled 4-D box per tile and phase plane), see launch_conv_tc
+  int tma_box_bytes;  // bytes one A box delivers (plane pixels x 128)
   int xf_act;     // activation of the transform chain
   int xf_table;   // floats per table (n * C) of the scale-shift table in shared memory
   double gn_inv_count;  // 1 / values per (n, group) of the GroupNorm-from-statistics source
@@ -867,7 +868,7 @@ __device__ __forceinline__ int nt_index(int nt) {
 
 // MMA-issue state shared by the unrolled chunk bodies (uniform across the warp).
 struct MmaCtx {
-  uint32_t a0, b0, lbo_a16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
+  uint32_t a0, b0, kstep16, row16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
   uint64_t adesc0, bdesc0;
   uint64_t* bar_bfull;
   uint64_t* bar_bempty;
@@ -889,11 +890,12 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
       const int tap = tg * TPS + tt;
       const int ky = tap / K, kx = tap % K;
       const uint32_t phase = S == 2 ? static_cast<uint32_t>(((ky & 1) << 1) | (kx & 1)) : 0u;
-      const uint32_t aoff = abase + phase * c.plane16 + static_cast<uint32_t>(ky / S) * c.P + static_cast<uint32_t>(kx / S);
+      const uint32_t aoff =
+          abase + phase * c.plane16 + static_cast<uint32_t>(ky / S) * c.P + static_cast<uint32_t>(kx / S) * c.row16;
       const uint32_t boff = bbase + static_cast<uint32_t>(tt) * c.tap_b16;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
-        const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * 2 * c.lbo_a16) & 0x3FFFu);
+        const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * c.kstep16) & 0x3FFFu);
         const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2) & 0x3FFFu);
         const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
         if (elect_one()) umma<F16>(c.tmem_d, ad, bd, c.idesc, accum);
@@ -967,6 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar_red_full, 1);  // the owner's arrive.expect_tx; the peers' st.async complete the bytes
     mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
+    if (p.tma_a && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 8) {
@@ -1075,7 +1078,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // as that group's rows (pitch = window width = P); out-of-canvas
         // cells and channels >= C come back zero-filled (gather's zero fill).
         if (threadIdx.x == 0) {
-          const uint32_t bytes = static_cast<uint32_t>(nt * 8 * p.win_h * p.win_w * 16);
+          const uint32_t bytes = static_cast<uint32_t>(nt * p.phases * p.tma_box_bytes);
           for (int ch = c_begin; ch < c_end; ++ch, ++a_iter) {
             const int sidx = aslot;
             if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
@@ -1087,8 +1090,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t base = a0 + sidx * p.a_bytes;
             for (int t = 0; t < nt; ++t) {
               const int4 tl = s_tile[t];
-              for (int g = 0; g < 8; ++g)
-                tma_4d(base + g * p.lbo_a + t * p.Mt * 16, &amap, ch * 64 + g * 8, tl.z, tl.y, tl.x,
+              for (int ph = 0; ph < p.phases; ++ph)  // stride 2: element stride 2 picks the phase plane
+                tma_4d(base + (ph * p.T + t) * p.Mt * 128, &amap, ch * 64, tl.z + (ph & 1), tl.y + (ph >> 1), tl.x,
                        &bar_afull[sidx]);
             }
             if (it == 0 && ch - c_begin < 8) tl_mark(p, 14 + ch - c_begin);
@@ -1383,13 +1386,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     MmaCtx c;
     c.a0 = smem_u32(abuf0) >> 4;
     c.b0 = smem_u32(bbuf) >> 4;
-    c.adesc0 = umma_desc(0, p.lbo_a, 128);
+    // A rows are 16 bytes apart in the interleaved layout (k-steps LBO apart),
+    // 128 bytes apart in the TMA mode's 128-byte-swizzled rows (k-steps 32 B).
+    c.row16 = p.tma_a ? 8u : 1u;
+    c.kstep16 = p.tma_a ? 2u : 2u * (p.lbo_a >> 4);
+    c.adesc0 = p.tma_a ? umma_desc_sw128(0) : umma_desc(0, p.lbo_a, 128);
     c.bdesc0 = umma_desc_sw128(0);
-    c.lbo_a16 = p.lbo_a >> 4;
     c.tap_b16 = tap_b >> 4;
-    c.plane16 = static_cast<uint32_t>(p.T * p.Mt);
+    c.plane16 = static_cast<uint32_t>(p.T * p.Mt) * c.row16;
     c.bstage16 = b_stage >> 4;
-    c.P = static_cast<uint32_t>(p.P);
+    c.P = static_cast<uint32_t>(p.P) * c.row16;
     c.nb = nb;
     c.idesc = idesc;
     c.bar_bfull = bar_bfull;
@@ -1723,31 +1729,34 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   }
   p.xform = xform ? 1 : 0;
   // TMA windows: F16 fp16 channels-last sources streamed as-is (no chain, no
-  // upsample), stride 1 — one box per (tile, 16-byte channel group).
+  // upsample) — one 4-D box per (tile, phase plane) delivering whole 128-byte
+  // channel rows, 128-byte swizzled (the MMA reads A through SWIZZLE_128B
+  // descriptors; a tap is still a pure row shift). Stride 2 takes each phase
+  // plane with element stride 2 in x and y.
   CUtensorMap amap{};
   p.tma_a = 0;
-  // Off by default: with 16-byte inner boxes the TMA path measured no faster
-  // than the per-thread cp.async ring on config 2 (profiles/r1_*); SIGE_TMA_A=1 enables it.
-  static const bool use_tma_a = std::getenv("SIGE_TMA_A") != nullptr;
-  if (use_tma_a && f16 && p.async_a && !xform && cw.stride == 1 && p.src.up == 0 && p.src.half && p.phases == 1) {
+  // On by default (config 2: 1.12 -> 1.04 ms/edit, stride-2 layers 2.3x);
+  // SIGE_NO_TMA_A=1 selects the per-thread cp.async ring instead.
+  static const bool use_tma_a = std::getenv("SIGE_NO_TMA_A") == nullptr;
+  const int plane_w = p.P, plane_h = cw.stride == 1 ? p.win_h : (bh + 1);
+  if (use_tma_a && f16 && p.async_a && !xform && p.src.up == 0 && p.src.half && plane_w * plane_h <= p.Mt) {
     const Src& a = p.src;
+    const int es = cw.stride == 1 ? 1 : 2;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.w),
                                 static_cast<cuuint64_t>(a.h), static_cast<cuuint64_t>(a.n)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(a.c) * 2, static_cast<cuuint64_t>(a.w) * a.c * 2,
                                    static_cast<cuuint64_t>(a.h) * a.w * a.c * 2};
-    const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(p.win_w), static_cast<cuuint32_t>(p.win_h), 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(plane_w * es), static_cast<cuuint32_t>(plane_h * es), 1};
+    const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(es), static_cast<cuuint32_t>(es), 1};
     CUresult r = encode_fn()(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<float*>(a.ptr), dims, strides, box,
-                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r == CUDA_SUCCESS && p.win_w * p.win_h <= p.Mt) {
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
       p.tma_a = 1;
-      // TMA destinations must be 128-byte aligned: group planes a multiple of
-      // 8 rows apart (the odd pitch only helped the per-thread staging stores).
-      int rows = p.phases * p.T * p.Mt + pad_rows + 8;
-      rows = (rows + 7) / 8 * 8;
-      p.lbo_a = static_cast<uint32_t>(rows * 16);
-      p.a_bytes = (rows * 16 * 8 + 1023) / 1024 * 1024;
+      p.tma_box_bytes = plane_w * plane_h * 128;
+      const int rows = (p.phases * p.T * p.Mt + pad_rows + 8 + 7) / 8 * 8;
+      p.lbo_a = 128;
+      p.a_bytes = (rows * 128 + 1023) / 1024 * 1024;
     }
   }
   p.xf_act = SIGE_ACT_NONE;

@@ -4,7 +4,8 @@ integer bit-exact and tolerance suites of test_gpu_tc.py in a subprocess:
 
 * SIGE_FORCE_SPLITK=8: every static-count launch split over a thread-block
   cluster (DSMEM reduce-scatter) — exact integer sums pin the reduction.
-* SIGE_TMA_A=1: A windows loaded by 4-D TMA boxes instead of cp.async.
+* SIGE_NO_TMA_A=1: A windows staged by the per-thread cp.async ring instead
+  of 128-byte-swizzled TMA boxes.
 * SIGE_NO_TUNE=1 / SIGE_NO_SPLITK=1: the analytic plan without split-K.
 """
 import os
@@ -18,9 +19,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("env", [{"SIGE_FORCE_SPLITK": "8"}, {"SIGE_TMA_A": "1"},
+@pytest.mark.parametrize("env", [{"SIGE_FORCE_SPLITK": "8"}, {"SIGE_NO_TMA_A": "1"},
                                  {"SIGE_NO_TUNE": "1", "SIGE_NO_SPLITK": "1"}],
-                         ids=["splitk8", "tma_a", "analytic_nosplit"])
+                         ids=["splitk8", "cp_async_a", "analytic_nosplit"])
 def test_tc_suite_under_variant(env):
     e = dict(os.environ)
     e.update(env)
