@@ -514,7 +514,9 @@ __device__ __forceinline__ void xform_chunk(const TcParams& p, uint8_t* abuf, in
     if (u >= units) break;
     const int cc = ch * 64 + (u & 7) * 8;
     if (pix_off[k] == kNoPix || cc >= p.c_in) continue;
-    uint4* at = reinterpret_cast<uint4*>(abuf + (u & 7) * p.lbo_a + (u >> 3) * 16);
+    // interleaved layout, or the TMA mode's 128-byte rows (16-byte column XOR row & 7)
+    uint4* at = reinterpret_cast<uint4*>(p.tma_a ? abuf + (u >> 3) * 128 + (((u & 7) ^ ((u >> 3) & 7)) << 4)
+                                                 : abuf + (u & 7) * p.lbo_a + (u >> 3) * 16);
     uint4 raw = *at;
     __half2* h = reinterpret_cast<__half2*>(&raw);
     const float4* sc4 = reinterpret_cast<const float4*>(xf_scale + unit_n[k] * C + cc);
@@ -924,7 +926,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps,
               const __grid_constant__ CUtensorMap amap) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[kMaxNA], bar_afree[kMaxNA];
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxNB], bar_bempty[kMaxNB], bar_afull[kMaxNA], bar_afree[kMaxNA],
+      bar_aland[kMaxNA];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
   __shared__ __align__(8) uint64_t bar_red_full, bar_red_empty;  // split-K reduce-scatter (ks > 1)
   __shared__ uint32_t tmem_base;
@@ -960,7 +963,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_bempty[i], 1);
     }
     for (int i = 0; i < p.na; ++i) {
-      mbar_init(&bar_afull[i], p.tma_a ? 1 : kProdThreads);
+      mbar_init(&bar_afull[i], p.tma_a && !p.xform ? 1 : kProdThreads);
+      mbar_init(&bar_aland[i], 1);  // TMA + transform: the boxes landed (before the in-smem chain)
       mbar_init(&bar_afree[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -1027,7 +1031,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
       int unit_n[kUnitRegs];
-      const bool fast_units = F16 && p.async_a && !p.tma_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
+      const bool fast_units =
+          F16 && p.async_a && (!p.tma_a || p.xform) && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
       if (it == 0) {
@@ -1074,30 +1079,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (p.tma_a) {
         // One thread streams the item's windows: per chunk one 4-D box
-        // (8 channels x window) per tile and 16-byte channel group, landing
-        // as that group's rows (pitch = window width = P); out-of-canvas
-        // cells and channels >= C come back zero-filled (gather's zero fill).
-        if (threadIdx.x == 0) {
-          const uint32_t bytes = static_cast<uint32_t>(nt * p.phases * p.tma_box_bytes);
-          for (int ch = c_begin; ch < c_end; ++ch, ++a_iter) {
-            const int sidx = aslot;
-            if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
+        // (64 channels x plane) per tile and phase plane, 128-byte rows;
+        // out-of-canvas cells and channels >= C come back zero-filled
+        // (gather's zero fill). With a pending chain the boxes land on
+        // bar_aland and the producers transform chunk c-1 (in-canvas units
+        // only) while chunk c is in flight, then arrive on bar_afull.
+        const uint32_t bytes = static_cast<uint32_t>(nt * p.phases * p.tma_box_bytes);
+        int prev_sidx = -1;
+        uint32_t prev_phase = 0;
+        const int ch_last = p.xform ? c_end : c_end - 1;
+        for (int ch = c_begin; ch <= ch_last; ++ch) {
+          int sidx = -1;
+          uint32_t sphase = 0;
+          if (ch < c_end) {
+            sidx = aslot;
+            sphase = aphase;
+            if (threadIdx.x == 0) {
+              if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
+              uint64_t* bar = p.xform ? &bar_aland[sidx] : &bar_afull[sidx];
+              mbar_expect_tx(bar, bytes);
+              const uint32_t base = a0 + sidx * p.a_bytes;
+              for (int t = 0; t < nt; ++t) {
+                const int4 tl = s_tile[t];
+                for (int ph = 0; ph < p.phases; ++ph)  // stride 2: element stride 2 picks the phase plane
+                  tma_4d(base + (ph * p.T + t) * p.Mt * 128, &amap, ch * 64, tl.z + (ph & 1), tl.y + (ph >> 1), tl.x,
+                         bar);
+              }
+              if (it == 0 && ch - c_begin < 8) tl_mark(p, 14 + ch - c_begin);
+            }
             if (++aslot == p.na) {
               aslot = 0;
               aphase ^= 1;
             }
-            mbar_expect_tx(&bar_afull[sidx], bytes);
-            const uint32_t base = a0 + sidx * p.a_bytes;
-            for (int t = 0; t < nt; ++t) {
-              const int4 tl = s_tile[t];
-              for (int ph = 0; ph < p.phases; ++ph)  // stride 2: element stride 2 picks the phase plane
-                tma_4d(base + (ph * p.T + t) * p.Mt * 128, &amap, ch * 64, tl.z + (ph & 1), tl.y + (ph >> 1), tl.x,
-                       &bar_afull[sidx]);
-            }
-            if (it == 0 && ch - c_begin < 8) tl_mark(p, 14 + ch - c_begin);
+            ++a_iter;
           }
-        } else {
-          a_iter += c_end - c_begin;
+          if (prev_sidx >= 0) {
+            mbar_wait(&bar_aland[prev_sidx], prev_phase);
+            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, pix_off, unit_n, xf_scale, xf_shift);
+            fence_proxy_async();
+            mbar_arrive(&bar_afull[prev_sidx]);
+          }
+          if (p.xform) {
+            prev_sidx = sidx;
+            prev_phase = sphase;
+          }
         }
       } else if (p.xform) {
         // Async copy of chunk c, then transform of chunk c-1 (landed: this
@@ -1728,8 +1753,9 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     p.src = src;
   }
   p.xform = xform ? 1 : 0;
-  // TMA windows: F16 fp16 channels-last sources streamed as-is (no chain, no
-  // upsample) — one 4-D box per (tile, phase plane) delivering whole 128-byte
+  // TMA windows: F16 fp16 channels-last sources (no upsample; a pending chain
+  // is applied in shared memory after the boxes land) — one 4-D box per
+  // (tile, phase plane) delivering whole 128-byte
   // channel rows, 128-byte swizzled (the MMA reads A through SWIZZLE_128B
   // descriptors; a tap is still a pure row shift). Stride 2 takes each phase
   // plane with element stride 2 in x and y.
@@ -1739,7 +1765,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   // SIGE_NO_TMA_A=1 selects the per-thread cp.async ring instead.
   static const bool use_tma_a = std::getenv("SIGE_NO_TMA_A") == nullptr;
   const int plane_w = p.P, plane_h = cw.stride == 1 ? p.win_h : (bh + 1);
-  if (use_tma_a && f16 && p.async_a && !xform && p.src.up == 0 && p.src.half && plane_w * plane_h <= p.Mt) {
+  if (use_tma_a && f16 && p.async_a && p.src.up == 0 && p.src.half && plane_w * plane_h <= p.Mt) {
     const Src& a = p.src;
     const int es = cw.stride == 1 ? 1 : 2;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.c), static_cast<cuuint64_t>(a.w),
