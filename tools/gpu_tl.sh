@@ -1,7 +1,5 @@
 #!/bin/bash
+# Graph timeline of one config-2 edit (per-launch spans + the [gtl i] launch descriptions on stderr).
 mkdir -p gpurun_out
-for M in tf32 f16; do
-SIGE_TC_TIMELINE=1 timeout 300 python tools/profile_layers.py --math $M --no-graphs > gpurun_out/timeline_$M.log 2>&1
-timeout 300 python tools/profile_layers.py --math $M > gpurun_out/layers_$M.log 2>&1
-done
+SIGE_TC_GTL=1 timeout 300 python tools/graph_timeline.py > gpurun_out/tl.log 2> gpurun_out/tl_desc.log
 exit 0

@@ -1,5 +1,6 @@
 """Per-launch conv spans and inter-launch gaps of one graph-replayed sparse edit
-(config 2, F16). Needs SIGE_TC_GTL=1 (device-side globaltimer stamps written by
+(config 2, F16); each row names its launch slot ([gtl i] — the library prints
+the slot's conv shape and plan to stderr at capture). Needs SIGE_TC_GTL=1 (device-side globaltimer stamps written by
 every k_conv_tc launch; see conv_tc.cu debug_conv_timeline)."""
 import ctypes as C
 import os
@@ -37,18 +38,19 @@ eng.sparse_forward(ed, config=cfg, out=out)
 b.record()
 torch.cuda.synchronize()
 n = lib.sige_debug_conv_timeline(buf, 1024)
-rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n) if buf[3 * i + 1]]
+rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2], i) for i in range(n) if buf[3 * i + 1]]
 t0 = rows[0][0]
 print(f"step {a.elapsed_time(b):.3f} ms (events), {len(rows)} conv launches")
 print("idx   start(us)  wait_done  end     work=end-wait  handoff=wait-prev_end")
 prev_end = None
 tot_work = tot_hand = 0.0
-for i, (s, en, wd) in enumerate(rows):
+for i, (s, en, wd, gi) in enumerate(rows):
     work = (en - wd) / 1e3
     hand = (wd - prev_end) / 1e3 if prev_end else 0.0
     tot_work += work
     tot_hand += hand
-    print(f"{i:3d} {(s - t0) / 1e3:9.2f} {(wd - t0) / 1e3:9.2f} {(en - t0) / 1e3:9.2f} {work:8.2f} {hand:8.2f}")
+    print(f"{i:3d} {(s - t0) / 1e3:9.2f} {(wd - t0) / 1e3:9.2f} {(en - t0) / 1e3:9.2f} {work:8.2f} {hand:8.2f}"
+          f"  [gtl {gi}]")
     prev_end = en
 print(f"sum work {tot_work:.1f} us, sum handoff (incl. non-conv kernels) {tot_hand:.1f} us, "
       f"first->last {(rows[-1][1] - t0) / 1e3:.1f} us")
