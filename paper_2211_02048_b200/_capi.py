@@ -12,7 +12,8 @@ import os
 import pathlib
 
 PKG_DIR = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "lib" / "libsige_b200.so"
+# SIGE_B200_LIB: developer override (A/B against another build of the same ABI).
+LIB_PATH = pathlib.Path(os.environ.get("SIGE_B200_LIB", PKG_DIR / "lib" / "libsige_b200.so"))
 
 SIGE_OK = 0
 SIGE_ERR_CONFIG = 2

@@ -46,9 +46,9 @@
 // weight stages overlap the previous layer's tail (griddepcontrol.wait guards
 // every access to data the previous kernel produced).
 //
-// Warp roles (320 threads): warps 0-3 produce A, warps 4-7 run the epilogue
-// (warp w reads TMEM lanes 32*(w%4)), warp 8 allocates TMEM and issues
-// tcgen05.mma (one thread), warp 9 issues the weight TMA (one thread).
+// Warp roles (256 threads): warps 0-1 produce A, warps 4-7 run the epilogue
+// (warp w reads TMEM lanes 32*(w%4)), warp 2 allocates TMEM and issues
+// tcgen05.mma (one thread), warp 3 issues the weight TMA (one thread).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -70,9 +70,14 @@ namespace sige_b200 {
 
 namespace {
 
-constexpr int kProdThreads = 128;  // warps 0-3: A producers
-constexpr int kEpiThreads = 128;   // warps 4-7: epilogue (TMEM lane quarter = warp % 4)
-constexpr int kThreads = kProdThreads + kEpiThreads + 64;  // + warp 8 (MMA), warp 9 (weight TMA)
+// 8 warps: 0-1 A producers, 2 MMA issuer (+ TMEM allocation), 3 weight TMA,
+// 4-7 epilogue (TMEM lane quarter = warp % 4). 256 threads leave every
+// thread up to 255 registers (ten warps capped the kernel at 168 and spilled).
+constexpr int kProdThreads = 64;    // warps 0-1: A producers
+constexpr int kEpiBase = 128;       // first epilogue thread (warp 4)
+constexpr int kEpiThreads = 128;    // warps 4-7: epilogue
+constexpr int kMmaWarp = 2, kWeightWarp = 3;
+constexpr int kThreads = 256;
 constexpr int kMaxNA = 4;          // A ring stages (max)
 constexpr int kMaxNB = 16;         // B (weight) ring slots (max)
 constexpr int kMaxNTile = 256;     // accumulator columns per TMEM buffer
@@ -430,7 +435,7 @@ __device__ __forceinline__ void stage_a_async(const TcParams& p, uint32_t abuf, 
 // units u = tid + 128 k (k < 12 covers every stride-1 geometry, <= 1536 units);
 // the window pixel of a unit is fixed for the whole item, only the channel
 // chunk moves, so the per-chunk work is one add + one cp.async per unit.
-constexpr int kUnitRegs = 12;
+constexpr int kUnitRegs = 24;
 constexpr uint32_t kNoPix = 0xffffffffu;
 __device__ __forceinline__ void unit_pixels(const TcParams& p, const int32_t* row_tab, const int4* s_tile,
                                             uint32_t (&pix_off)[kUnitRegs], int (&unit_n)[kUnitRegs]) {
@@ -919,13 +924,13 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
   }
 }
 
-// Warp roles (320 threads, one CTA per SM, persistent over work items =
+// Warp roles (256 threads, one CTA per SM, persistent over work items =
 // (group of T tiles, N slice)):
-//   warps 0-3  A producers: K chunk c of item i into A stage c % na (cp.async
+//   warps 0-1  A producers: K chunk c of item i into A stage c % na (cp.async
 //              ring, up to na-1 chunks in flight, or synchronous staging)
 //   warps 4-7  epilogue: TMEM accumulator (i & 1) -> bias / residual -> dst
-//   warp 8     TMEM allocation + the single MMA-issuing thread
-//   warp 9     weight producer: one TMA per ring stage (1, 3 or 9 taps)
+//   warp 2     TMEM allocation + the single MMA-issuing thread
+//   warp 3     weight producer: one TMA per ring stage (1, 3 or 9 taps)
 // SYNC: the instantiation carries the synchronous (converting / chained)
 // staging path; the F16 production kernels (every source an fp16 twin or act
 // buffer) are built without it — half the code, fewer cold instruction fetches.
@@ -984,7 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.tma_a && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(kTmemCols)
                  : "memory");
@@ -1020,7 +1025,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) tl_mark(p, 55);
   if (threadIdx.x == 0) pdl_trigger();  // the next layer may start its own setup
 
-  if (warp < 4) {
+  if (warp < kProdThreads / 32) {
     // ---------------- A producers ----------------
     const uint32_t a0 = smem_u32(abuf0);
     uint32_t a_iter = 0, it = 0, aphase = 0;
@@ -1193,7 +1198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (it == 0) pdl_wait();
     // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
     asm volatile("cp.async.wait_all;" ::: "memory");
-  } else if (warp < 8) {
+  } else if (warp >= kEpiBase / 32) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;                       // TMEM lane quarter of this warp
     const int m = q * 32 + lane;                  // TMEM lane = GEMM row
@@ -1230,7 +1235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!dry) {
         const int oc0 = ni * n_tile + own0;
         asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads));  // previous item's readers done
-        for (int j = threadIdx.x - kProdThreads; j < slice; j += kEpiThreads) {
+        for (int j = threadIdx.x - kEpiBase; j < slice; j += kEpiThreads) {
           const int oc = oc0 + j;
           s_bias[j] = p.bias && oc < p.c_out ? __ldg(p.bias + oc) : 0.0f;
           if (act_pre) {
@@ -1252,14 +1257,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!dry) {
         mbar_wait(&bar_acc_full[acc], (it >> 1) & 1);
         tc_fence_after();
-        if (threadIdx.x == kProdThreads && it < 2) tl_mark(p, it ? 56 : 5);
+        if (threadIdx.x == kEpiBase && it < 2) tl_mark(p, it ? 56 : 5);
       }
       const uint32_t tbase = taddr + (static_cast<uint32_t>(q * 32) << 16) + acc * kMaxNTile;
       if (p.ks == 1) {
         for (int cb = 0; cb < n_tile; cb += 16) {
           float v[16];
           if (!dry) tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
-          if (threadIdx.x == kProdThreads && it == 0 && cb == 0) tl_mark(p, 46);
+          if (threadIdx.x == kEpiBase && it == 0 && cb == 0) tl_mark(p, 46);
           float aux_cur[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) aux_cur[j] = aux_next[j];
@@ -1292,11 +1297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the epilogue on them.
         const int blocks = slice / 16;
         const uint32_t red0 = smem_u32(red_buf);
-        if (threadIdx.x == kProdThreads && !dry) {  // this owner expects (ks-1) slots of 128 rows x slice fp32
+        if (threadIdx.x == kEpiBase && !dry) {  // this owner expects (ks-1) slots of 128 rows x slice fp32
           mbar_expect_tx(&bar_red_full, static_cast<uint32_t>((p.ks - 1) * 128 * slice * 4));
         }
         if (it > 0) mbar_wait_cluster(&bar_red_empty, (it - 1) & 1);  // owners consumed the previous item
-        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 53);
+        if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 53);
         for (int d = 1; d < p.ks && !dry; ++d) {
           const int owner = (rank + d) % p.ks;
           const uint32_t rbase = mapa(red0, static_cast<uint32_t>(owner)) +
@@ -1311,9 +1316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           v[4 * j + 3], rbar);
           }
         }
-        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 51);
+        if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 51);
         if (!dry) mbar_wait_cluster(&bar_red_full, it & 1);
-        if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 52);
+        if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 52);
         for (int b = 0; b < blocks; ++b) {
           float tot[16];
 #pragma unroll
@@ -1360,10 +1365,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         pdl_wait();
         continue;
       }
-      if (threadIdx.x == kProdThreads && it < 2) tl_mark(p, it ? 57 : 47);
+      if (threadIdx.x == kEpiBase && it < 2) tl_mark(p, it ? 57 : 47);
       tc_fence_before();
       mbar_arrive(&bar_acc_empty[acc]);
-      if (threadIdx.x == kProdThreads && it == 0) tl_mark(p, 6);
+      if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 6);
       item += ncl;
       ++it;
     }
@@ -1375,7 +1380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int jcount = d.join_tiles.count_dev ? *d.join_tiles.count_dev : d.join_tiles.count;
       const int jb = d.join_b, per = jb * jb, cbl = (p.c_out + 15) / 16;
       const long long total = static_cast<long long>(jcount) * per * cbl;
-      for (long long u = static_cast<long long>(blockIdx.x) * kEpiThreads + (threadIdx.x - kProdThreads); u < total;
+      for (long long u = static_cast<long long>(blockIdx.x) * kEpiThreads + (threadIdx.x - kEpiBase); u < total;
            u += static_cast<long long>(gridDim.x) * kEpiThreads) {
         const int g = static_cast<int>(u / (per * cbl));
         const int rem = static_cast<int>(u - static_cast<long long>(g) * per * cbl);
@@ -1426,7 +1431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (whole warp, converged) ----------------
     // Descriptors are uniform: base descriptor with a zero start field plus
     // the (stage, tap, k-step) offset in 16-byte units; taps are unrolled at
@@ -1521,7 +1526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(p.gtl + 2 * p.gtl_idx + 1, t);
   }
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kTmemCols)
                  : "memory");
