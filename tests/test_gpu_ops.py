@@ -294,3 +294,29 @@ def test_conv_on_blocks_and_conv2d(orc, math):
 def test_conv_on_blocks_geometry_error():
     with pytest.raises(sb.ConfigError, match="conv_on_blocks: window 8 with k=3 s=1 yields 6, expected block 5"):
         sb.conv_on_blocks(cu(np.zeros((1, 2, 8, 8), np.float32)), cu(np.zeros((2, 2, 3, 3), np.float32)), None, 1, 5)
+
+
+@pytest.mark.parametrize("b", [1, 6, 13])
+def test_gather_scatter_long_runs_chunk_and_slice_edges(orc, b):
+    # Dense masks: row runs longer than one CTA chunk (256 columns), channel
+    # counts that split into several slices with a ragged last one, tiles at
+    # the fringe. Exercises the (channel, row, tile, column) walk of
+    # k_gather / k_scatter against the oracle bit for bit.
+    rng = np.random.default_rng(1000 + b)
+    for k, s in [(3, 1), (3, 2), (1, 1)]:
+        n, c, h, w = 2, 37, 61, 301
+        x = rng.uniform(-2, 2, (n, c, h, w)).astype(np.float32)
+        oh, ow = (h + 2 * ((k - 1) // 2) - k) // s + 1, (w + 2 * ((k - 1) // 2) - k) // s + 1
+        m = (rng.random((oh, ow)) < 0.6).astype(np.uint8)
+        idx, _ = orc.mask_to_block_indices(m, b, n)
+        epi = rand_epi_np(rng, c, n, silu=True, per_sample=True)
+        want = orc.gather(x, idx, b, oh, ow, k, s, epi)
+        assert bits_equal(host(sb.gather(cu(x), cu(idx), b, k, s, to_dev_epi(epi))), want)
+    m = (rng.random((h, w)) < 0.6).astype(np.uint8)
+    idx, _ = orc.mask_to_block_indices(m, b, n)
+    blocks = rng.uniform(-1, 1, (len(idx), c, b, b)).astype(np.float32)
+    base = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    assert bits_equal(host(sb.scatter(cu(blocks), cu(idx), cu(base))), orc.scatter(blocks, idx, base))
+    tb = cu(base)
+    sb.scatter_add_inplace(cu(blocks), cu(idx), tb)
+    assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
