@@ -158,76 +158,147 @@ __global__ void k_blockify(const uint8_t* __restrict__ m, int h, int w, int b, i
 
 // ---------------------------------------------------------------- blocks --
 
-// gather (kernels.cpp:39-86) and scatter (kernels.cpp:88-132) walk a CHUNK
-// of consecutive tiles per CTA pass in (channel, row, tile, column) order: the
-// index set is row-major (mask.cpp:103-136), so neighbouring tiles of a chunk
-// are usually horizontal neighbours and a warp's lanes then cover one
-// contiguous run of an image row (gather: overlapping windows read as one
-// coalesced span; scatter: b-wide tile rows merge into full-line stores).
-// Non-adjacent tiles stay correct, only less coalesced. Tile origins are
-// staged in shared memory; each thread keeps kU independent loads in flight.
-constexpr int kChunkCols = 256;  // columns (tiles x tile width) per chunk row
+// scatter (kernels.cpp:88-132) moves a CHUNK of consecutive tiles x a slice
+// of channels per CTA pass through shared memory, so both sides are
+// coalesced: the block-stack side as one contiguous run per tile, the image
+// side walked in (channel, row, tile, column) order — the index set is
+// row-major (mask.cpp:103-136), so a chunk's tiles are mostly horizontal
+// neighbours and a warp's b-wide tile rows merge into full-line stores.
+// (The same staging for gather measured slower than the per-tile walk below:
+// 114-250 us vs 100 us at the ops_hbm workload, profiles/r1_ops_hbm_iter.txt.) Non-adjacent
+// tiles stay correct, only less coalesced. Tiles larger than the staging
+// buffer fall back to a direct walk (staged = false).
+constexpr int kChunkCols = 256;  // image-side columns (tiles x tile width) per chunk
 constexpr int kMaxChunkTiles = 256;
+constexpr int kStageFloats = 8192;  // 32 KB staging buffer per CTA
+constexpr int kU = 8;               // independent loads in flight per thread
 
-__host__ __device__ inline int chunk_tiles(int width) {
-  int t = kChunkCols / width;
-  return t < 1 ? 1 : (t > kMaxChunkTiles ? kMaxChunkTiles : t);
+struct ChunkPlan {
+  int T;    // tiles per chunk
+  int cpi;  // channels per item
+  bool staged;
+};
+
+inline ChunkPlan chunk_plan(int c, int width) {
+  const int wsz = width * width;
+  ChunkPlan cp{};
+  cp.staged = wsz <= kStageFloats;
+  cp.T = std::max(1, std::min(kMaxChunkTiles, kChunkCols / width));
+  if (cp.staged) cp.T = std::max(1, std::min(cp.T, kStageFloats / wsz));
+  const int cap = cp.staged ? kStageFloats : 4096;
+  cp.cpi = std::max(1, std::min(c, cap / (cp.T * wsz)));
+  return cp;
 }
 
-// Channels per work item: ~4096 elements (kThreads x kU x 2) per CTA pass so
-// small index sets still spread over every SM.
-inline int slice_channels(int c, int rows_per_channel, int cols) {
-  long long per = static_cast<long long>(rows_per_channel) * cols;
-  long long k = 4096 / (per < 1 ? 1 : per);
-  return static_cast<int>(k < 1 ? 1 : (k > c ? c : k));
+__device__ __forceinline__ void load_origins(int (*s_org)[3], const int32_t* __restrict__ idx, int i0, int tc,
+                                             int stride, int pad) {
+  __syncthreads();
+  for (int t = threadIdx.x; t < tc; t += blockDim.x) {
+    s_org[t][0] = __ldg(idx + 3 * (i0 + t));
+    s_org[t][1] = __ldg(idx + 3 * (i0 + t) + 1) * stride - pad;
+    s_org[t][2] = __ldg(idx + 3 * (i0 + t) + 2) * stride - pad;
+  }
+  __syncthreads();
 }
 
-// gather: out-of-canvas cells are +0 and skip the epilogue.
-__global__ void __launch_bounds__(kThreads) k_gather(const float* __restrict__ x, int c, int h, int w,
-                                                     const int32_t* __restrict__ idx, int count, int win,
-                                                     int stride, int pad, int cpi, DevEpilogue epi,
-                                                     float* __restrict__ out) {
-  constexpr int kU = 8;
-  __shared__ int s_org[kMaxChunkTiles][3];  // n, top row, left column
-  const int T = chunk_tiles(win), wsz = win * win;
-  const size_t slab = static_cast<size_t>(c) * wsz;
-  const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi;
-  for (int it = blockIdx.x; it < chunks * slices; it += gridDim.x) {
-    const int ck = it / slices, c0 = (it - ck * slices) * cpi, c1 = min(c, c0 + cpi);
-    const int i0 = ck * T, tc = min(T, count - i0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < tc; t += blockDim.x) {
-      s_org[t][0] = __ldg(idx + 3 * (i0 + t));
-      s_org[t][1] = __ldg(idx + 3 * (i0 + t) + 1) * stride - pad;
-      s_org[t][2] = __ldg(idx + 3 * (i0 + t) + 2) * stride - pad;
+// Column walk shared by both kernels: the image side of an item is a grid of
+// rows (channel, tile row) x cols (tile, tile column). A thread owns one
+// column (one division per column and item) and a strided set of channels,
+// and walks each channel's tile rows with plain pointer arithmetic — no
+// per-element division (integer issue, not bandwidth, bounded a version that
+// decoded every element's coordinates).
+struct ColWalk {
+  int groups, group, col, col_step;
+  __device__ ColWalk(int cols) {
+    groups = cols >= static_cast<int>(blockDim.x) ? 1 : static_cast<int>(blockDim.x) / cols;
+    group = groups > 1 ? static_cast<int>(threadIdx.x) / cols : 0;
+    col = groups > 1 ? static_cast<int>(threadIdx.x) - group * cols : static_cast<int>(threadIdx.x);
+    col_step = groups > 1 ? cols : static_cast<int>(blockDim.x);
+    if (group >= groups) col = cols;  // spare threads
+  }
+};
+
+// Contiguous per-tile runs between shared memory and a block stack
+// (tile t's run of `run` floats at stack + t * slab), 16-byte vectors when the
+// geometry keeps them aligned.
+template <bool kToStack>
+__device__ __forceinline__ void stack_runs(float* stack, size_t slab, float* sbuf, int tc, int run, bool vec) {
+  const int v = vec ? 4 : 1, rv = run / v;
+  const int tpp = rv >= static_cast<int>(blockDim.x) ? 1 : static_cast<int>(blockDim.x) / rv;
+  int t = tpp > 1 ? static_cast<int>(threadIdx.x) / rv : 0;
+  const int j0 = tpp > 1 ? static_cast<int>(threadIdx.x) - t * rv : static_cast<int>(threadIdx.x);
+  const int jstep = tpp > 1 ? rv : static_cast<int>(blockDim.x);
+  if (t >= tpp) return;
+  for (; t < tc; t += tpp) {
+    float* g = stack + t * slab;
+    float* sm = sbuf + t * run;
+    for (int j = j0; j < rv; j += jstep) {
+      if (vec) {
+        if (kToStack)
+          reinterpret_cast<float4*>(g)[j] = reinterpret_cast<const float4*>(sm)[j];
+        else
+          reinterpret_cast<float4*>(sm)[j] = __ldg(reinterpret_cast<const float4*>(g) + j);
+      } else {
+        if (kToStack)
+          g[j] = sm[j];
+        else
+          sm[j] = __ldg(g + j);
+      }
     }
-    __syncthreads();
-    const int cols = tc * win;
-    const int total = (c1 - c0) * win * cols;
-    float* ob = out + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * wsz;
-    for (int e0 = threadIdx.x; e0 < total; e0 += blockDim.x * kU) {
-      float v[kU];
-      size_t dst[kU];
+  }
+}
+
+// gather (kernels.cpp:39-86): one thread per output value; out-of-canvas
+// cells are +0 and skip the epilogue.
+__global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
+                         const int32_t* __restrict__ idx, int count, int win, int stride, int pad,
+                         DevEpilogue epi, float* __restrict__ out) {
+  // One tile per blockIdx.x (grid-stride). A thread owns quads (4 consecutive
+  // outputs of the tile slab (C, win, win), indices advanced incrementally,
+  // one 16-byte store each) and keeps two quads = 8 loads in flight.
+  constexpr int kQ = 2;
+  const int wsz = win * win, slab = c * wsz;
+  const bool vec = (slab & 3) == 0;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1) * stride - pad,
+              ox = __ldg(idx + 3 * i + 2) * stride - pad;
+    const size_t plane0 = static_cast<size_t>(n) * c;
+    float* o = out + static_cast<size_t>(i) * slab;
+    for (int q0 = threadIdx.x * 4; q0 < slab; q0 += blockDim.x * 4 * kQ) {
+      float v[kQ][4];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * blockDim.x;
-        v[u] = 0.0f;
-        dst[u] = ~size_t(0);
-        if (e < total) {
-          const int row = e / cols, col = e - row * cols;
-          const int t = col / win, wx = col - t * win;
-          const int cl = row / win, wy = row - cl * win, ch = c0 + cl;
-          dst[u] = t * slab + static_cast<size_t>(row) * win + wx;
-          const int n = s_org[t][0], sy = s_org[t][1] + wy, sx = s_org[t][2] + wx;
-          if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
-            v[u] = __ldg(x + ((static_cast<size_t>(n) * c + ch) * h + sy) * w + sx);
-            if (epi.num_steps) v[u] = dev_epi(epi, v[u], ch, c, n);
+      for (int k = 0; k < kQ; ++k) {
+        const int q = q0 + k * blockDim.x * 4;
+        int ch = q / wsz, cell = q - ch * wsz;
+        int wy = cell / win, wx = cell - wy * win;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[k][e] = 0.0f;
+          if (q + e < slab) {
+            const int sy = oy + wy, sx = ox + wx;
+            if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
+              v[k][e] = __ldg(x + ((plane0 + ch) * h + sy) * w + sx);
+              if (epi.num_steps) v[k][e] = dev_epi(epi, v[k][e], ch, c, n);
+            }
+          }
+          if (++wx == win) {
+            wx = 0;
+            if (++wy == win) {
+              wy = 0;
+              ++ch;
+            }
           }
         }
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (dst[u] != ~size_t(0)) __stcs(ob + dst[u], v[u]);
+      for (int k = 0; k < kQ; ++k) {
+        const int q = q0 + k * blockDim.x * 4;
+        if (q >= slab) break;
+        if (vec)
+          *reinterpret_cast<float4*>(o + q) = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+        else
+          for (int e = 0; e < 4 && q + e < slab; ++e) o[q + e] = v[k][e];
+      }
     }
   }
 }
@@ -236,53 +307,41 @@ __global__ void __launch_bounds__(kThreads) k_gather(const float* __restrict__ x
 // mode 0 writes, mode 1 adds.
 __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ blocks, int count, int c, int b,
                                                       const int32_t* __restrict__ idx, float* __restrict__ base,
-                                                      int h, int w, int cpi, int mode) {
-  constexpr int kU = 8;
+                                                      int h, int w, int T, int cpi, int staged, int mode) {
   __shared__ int s_org[kMaxChunkTiles][3];
-  const int T = chunk_tiles(b), bsz = b * b;
-  const size_t slab = static_cast<size_t>(c) * bsz;
+  __shared__ __align__(16) float s_buf[kStageFloats];
+  const int bsz = b * b;
+  const size_t slab = static_cast<size_t>(c) * bsz, plane = static_cast<size_t>(h) * w;
   const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi;
   for (int it = blockIdx.x; it < chunks * slices; it += gridDim.x) {
-    const int ck = it / slices, c0 = (it - ck * slices) * cpi, c1 = min(c, c0 + cpi);
+    const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
     const int i0 = ck * T, tc = min(T, count - i0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < tc; t += blockDim.x) {
-      s_org[t][0] = __ldg(idx + 3 * (i0 + t));
-      s_org[t][1] = __ldg(idx + 3 * (i0 + t) + 1);
-      s_org[t][2] = __ldg(idx + 3 * (i0 + t) + 2);
-    }
-    __syncthreads();
-    const int cols = tc * b;
-    const int total = (c1 - c0) * b * cols;
+    load_origins(s_org, idx, i0, tc, 1, 0);
     const float* sb = blocks + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * bsz;
-    for (int e0 = threadIdx.x; e0 < total; e0 += blockDim.x * kU) {
-      float v[kU];
-      float* d[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * blockDim.x;
-        d[u] = nullptr;
-        v[u] = 0.0f;
-        if (e < total) {
-          const int row = e / cols, col = e - row * cols;
-          const int t = col / b, dx = col - t * b;
-          const int cl = row / b, dy = row - cl * b, ch = c0 + cl;
-          const int y = s_org[t][1] + dy, x = s_org[t][2] + dx;
-          v[u] = __ldcs(sb + t * slab + static_cast<size_t>(row) * b + dx);
-          if (y < h && x < w) d[u] = base + ((static_cast<size_t>(s_org[t][0]) * c + ch) * h + y) * w + x;
+    const int run = ncl * bsz;
+    if (staged) {
+      stack_runs<false>(const_cast<float*>(sb), slab, s_buf, tc, run, (bsz & 3) == 0);
+      __syncthreads();
+    }
+    // image side: rows (channel, tile row), cols (tile, tile column)
+    const int cols = tc * b;
+    ColWalk cw(cols);
+    for (; cw.col < cols; cw.col += cw.col_step) {
+      const int t = cw.col / b, dx = cw.col - t * b;
+      const int y0 = s_org[t][1], xx = s_org[t][2] + dx;
+      const int dy_hi = xx < w ? min(b, h - y0) : 0;  // fringe clipping
+      float* dpb = base + (static_cast<size_t>(s_org[t][0]) * c + c0) * plane + static_cast<size_t>(y0) * w + xx;
+      const float* sp = staged ? s_buf + t * run + dx : sb + t * slab + dx;
+      for (int cl = cw.group; cl < ncl; cl += cw.groups) {
+        float* dc = dpb + static_cast<size_t>(cl) * plane;
+        const float* sc = sp + cl * bsz;
+        if (mode) {
+#pragma unroll 4
+          for (int dy = 0; dy < dy_hi; ++dy) dc[dy * w] = __fadd_rn(dc[dy * w], staged ? sc[dy * b] : __ldg(sc + dy * b));
+        } else {
+#pragma unroll 8
+          for (int dy = 0; dy < dy_hi; ++dy) dc[dy * w] = staged ? sc[dy * b] : __ldg(sc + dy * b);
         }
-      }
-      if (mode) {
-        float o[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) o[u] = d[u] ? *d[u] : 0.0f;
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (d[u]) *d[u] = __fadd_rn(o[u], v[u]);
-      } else {
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (d[u]) *d[u] = v[u];
       }
     }
   }
@@ -517,9 +576,7 @@ void op_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, i
                       "x" + std::to_string(ow));
   if (count == 0) return;
   int win = s * b + k - s;
-  const int cpi = slice_channels(c, win, chunk_tiles(win) * win);
-  const long long items = static_cast<long long>((count + chunk_tiles(win) - 1) / chunk_tiles(win)) * ((c + cpi - 1) / cpi);
-  k_gather<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(x, c, h, w, idx, count, win, s, (k - 1) / 2, cpi,
+  k_gather<<<std::min(count, sm_count() * 16), kThreads, 0, st>>>(x, c, h, w, idx, count, win, s, (k - 1) / 2,
                                                                  epi, out);
   after_launch("k_gather");
 }
@@ -528,10 +585,10 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
                 int n, int c, int h, int w, bool add, cudaStream_t st) {
   if (channels != c) throw ConfigError(std::string(add ? "scatter_add" : "scatter") + ": channel mismatch");
   if (count == 0) return;
-  const int cpi = slice_channels(c, b, chunk_tiles(b) * b);
-  const long long items = static_cast<long long>((count + chunk_tiles(b) - 1) / chunk_tiles(b)) * ((c + cpi - 1) / cpi);
-  k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(blocks, count, c, b, idx, base, h, w, cpi,
-                                                                  add ? 1 : 0);
+  const ChunkPlan cp = chunk_plan(c, b);
+  const long long items = static_cast<long long>((count + cp.T - 1) / cp.T) * ((c + cp.cpi - 1) / cp.cpi);
+  k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
+      blocks, count, c, b, idx, base, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0);
   after_launch("k_scatter");
 }
 
