@@ -156,17 +156,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+constexpr uint32_t kSuspendHintNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0, spins = 0;
+  unsigned long long t0 = 0;
   do {
+    // With a suspend-time hint the waiting warp sleeps until the phase
+    // completes (or ~1 ms passes) instead of re-polling: idle roles (MMA,
+    // weights, epilogue) hammering try_wait occupied the shared-memory pipe
+    // the working role's LDS/STS go through.
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(kSuspendHintNs)
         : "memory");
-    // A lost arrival must fail loudly instead of hanging the device.
-    if (!done && ++spins > (1u << 24)) __trap();
+    // A lost arrival must fail loudly instead of hanging the device
+    // (wall-clock bound: a try may sleep up to the hint or return at once).
+    if (!done && (++spins & 63) == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 2000000000ull) __trap();
+    }
   } while (!done);
 }
 
@@ -492,36 +504,128 @@ __device__ __forceinline__ float xf_act(float v, int kind) {
   return v;
 }
 
-__device__ __forceinline__ void xform_chunk(const TcParams& p, uint8_t* abuf, int ch,
-                                            const uint32_t (&pix_off)[kUnitRegs], const int (&unit_n)[kUnitRegs],
-                                            const float* xf_scale, const float* xf_shift) {
-  const int units = p.phases * p.T * p.Mt * 8;
-  const int C = p.src.c;
-  const int act = p.xf_act;
-#pragma unroll
-  for (int k = 0; k < kUnitRegs; ++k) {
-    const int u = threadIdx.x + k * kProdThreads;
-    if (u >= units) break;
-    const int cc = ch * 64 + (u & 7) * 8;
-    if (pix_off[k] == kNoPix || cc >= p.c_in) continue;
-    // interleaved layout, or the TMA mode's 128-byte rows (16-byte column XOR row & 7)
-    uint4* at = reinterpret_cast<uint4*>(p.tma_a ? abuf + (u >> 3) * 128 + (((u & 7) ^ ((u >> 3) & 7)) << 4)
-                                                 : abuf + (u & 7) * p.lbo_a + (u >> 3) * 16);
-    uint4 raw = *at;
-    __half2* h = reinterpret_cast<__half2*>(&raw);
-    const float4* sc4 = reinterpret_cast<const float4*>(xf_scale + unit_n[k] * C + cc);
-    const float4* sh4 = reinterpret_cast<const float4*>(xf_shift + unit_n[k] * C + cc);
-    const float4 s0 = sc4[0], s1 = sc4[1], t0 = sh4[0], t1 = sh4[1];
-    const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-    const float sh[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __half22float2(h[j]);
-      h[j] = __floats2half2_rn(xf_act(fmaf(sc[2 * j], f.x, sh[2 * j]), act),
-                               xf_act(fmaf(sc[2 * j + 1], f.y, sh[2 * j + 1]), act));
-    }
-    *at = raw;
+// One packed fp16 pair (low half = lower channel) through scale-shift + act.
+template <int kAct>
+__device__ __forceinline__ uint32_t xf_pair(uint32_t w, float s0, float t0, float s1, float t1) {
+  float lo, hi;
+  asm("{\n .reg .f16 l, h;\n mov.b32 {l, h}, %2;\n cvt.f32.f16 %0, l;\n cvt.f32.f16 %1, h;\n}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(w));
+  lo = fmaf(s0, lo, t0);
+  hi = fmaf(s1, hi, t1);
+  if (kAct == SIGE_ACT_SILU) {
+    // tables pre-halved for SiLU: h = v / 2, silu(v) = v (1/2 + tanh(v/2) / 2) = h tanh(h) + h
+    lo = fmaf(lo, tanh_approx(lo), lo);
+    hi = fmaf(hi, tanh_approx(hi), hi);
+  } else {
+    lo = xf_act(lo, kAct);
+    hi = xf_act(hi, kAct);
   }
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+constexpr int kMaxARows = kUnitRegs * kProdThreads / 8;  // staged A rows (window pixels x phases) per item
+
+// Per staged A row: the sample index n of the pixel it carries, or -1 for
+// rows without pixel data (padding rows, empty tile slots, out-of-canvas
+// cells: gather's zero fill, which the transform must leave at +0).
+__device__ __forceinline__ void fill_row_samples(const TcParams& p, const int32_t* row_tab, const int4* s_tile,
+                                                 int16_t* s_rown) {
+  const Src& s = p.src;
+  const int rows = p.phases * p.T * p.Mt;
+  for (int r = threadIdx.x; r < rows; r += kProdThreads) {
+    const int32_t info = row_tab[r];
+    int n = -1;
+    if (info < 0) {
+      const int4 tl = s_tile[(info >> 24) & 0x7f];
+      const int y = tl.y + ((info >> 12) & 0xfff), x = tl.z + (info & 0xfff);
+      if (tl.x >= 0 && y >= 0 && y < s.h && x >= 0 && x < s.w) n = tl.x;
+    }
+    s_rown[r] = static_cast<int16_t>(n);
+  }
+}
+
+template <int kAct>
+__device__ __noinline__ void xform_chunk_t(uint8_t* abuf, int ch, const int16_t* s_rown, const float* xf_scale,
+                                           const float* xf_shift, int units, int C, int c_in, int tma_a, int lbo_a,
+                                           int tid, int nthr) {
+  // A thread's units u = tid + k * kProdThreads all sit in the same 16-byte
+  // channel group (kProdThreads % 8 == 0), so the folded scale/shift of the
+  // group are loaded once per sample, not per unit. Which units carry pixel
+  // data comes from the per-row table in shared memory (no per-unit register
+  // arrays: the producer branch runs at the kernel's 255-register cap), and
+  // the units go in batches of kXB — shared-memory loads first, then the
+  // math and the stores — so one warp per SMSP does not pay the load latency
+  // unit by unit.
+  static_assert(kProdThreads % 8 == 0, "unit channel group must be thread-invariant");
+  //
+  // Out of line on purpose: the producer branch runs at the kernel's
+  // 255-register cap, and inlined, this loop lived in local memory (SASS:
+  // LDL/STL around every value, ~4.5 us per 64-channel chunk of a 7x16 tile).
+  // As a call it gets its own registers; the spills happen once around it.
+  constexpr int kXB = 4;
+  const int g = tid & 7;
+  const int cc = ch * 64 + g * 8;
+  if (cc >= c_in) return;  // padding channels: zero fill stays
+  int cur_n = -1;
+  float sc[8], sh[8];
+  for (int u0 = tid; u0 < units; u0 += kXB * nthr) {
+    uint4 raw[kXB];
+    int nn[kXB];
+#pragma unroll
+    for (int j = 0; j < kXB; ++j) {
+      const int u = u0 + j * nthr, row = u >> 3;
+      nn[j] = -1;
+      raw[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (u < units) {
+        nn[j] = s_rown[row];
+        // interleaved layout, or the TMA mode's 128-byte rows (16-byte column XOR row & 7)
+        raw[j] = *reinterpret_cast<const uint4*>(tma_a ? abuf + row * 128 + ((g ^ (row & 7)) << 4)
+                                                         : abuf + g * lbo_a + row * 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kXB; ++j) {
+      const int n = nn[j];
+      if (n >= 0 && n != cur_n) {  // first unit / a new sample (batched requests only)
+        cur_n = n;
+        const float4* sc4 = reinterpret_cast<const float4*>(xf_scale + n * C + cc);
+        const float4* sh4 = reinterpret_cast<const float4*>(xf_shift + n * C + cc);
+        const float4 s0 = sc4[0], s1 = sc4[1], t0 = sh4[0], t1 = sh4[1];
+        sc[0] = s0.x, sc[1] = s0.y, sc[2] = s0.z, sc[3] = s0.w, sc[4] = s1.x, sc[5] = s1.y, sc[6] = s1.z, sc[7] = s1.w;
+        sh[0] = t0.x, sh[1] = t0.y, sh[2] = t0.z, sh[3] = t0.w, sh[4] = t1.x, sh[5] = t1.y, sh[6] = t1.z, sh[7] = t1.w;
+      }
+      // fp16 pairs unpacked / repacked in registers (taking the address of
+      // raw[j] to reinterpret it as __half2 put the batch in local memory);
+      // branch-free: every unit is computed, only units with pixel data are
+      // stored back (the zero fill stays +0)
+      uint4 t;
+      t.x = xf_pair<kAct>(raw[j].x, sc[0], sh[0], sc[1], sh[1]);
+      t.y = xf_pair<kAct>(raw[j].y, sc[2], sh[2], sc[3], sh[3]);
+      t.z = xf_pair<kAct>(raw[j].z, sc[4], sh[4], sc[5], sh[5]);
+      t.w = xf_pair<kAct>(raw[j].w, sc[6], sh[6], sc[7], sh[7]);
+      const int row = (u0 + j * nthr) >> 3;
+      if (n >= 0)
+        *reinterpret_cast<uint4*>(tma_a ? abuf + row * 128 + ((g ^ (row & 7)) << 4) : abuf + g * lbo_a + row * 16) = t;
+    }
+  }
+}
+
+// One loop body per activation (the executed instruction stream stays small).
+// Threads tid = 0 .. nthr-1 (nthr % 8 == 0) share the chunk's units.
+__device__ __forceinline__ void xform_chunk(const TcParams& p, uint8_t* abuf, int ch, const int16_t* s_rown,
+                                            const float* xf_scale, const float* xf_shift, int tid, int nthr) {
+  const int units = p.phases * p.T * p.Mt * 8;
+  if (p.xf_act == SIGE_ACT_SILU)
+    xform_chunk_t<SIGE_ACT_SILU>(abuf, ch, s_rown, xf_scale, xf_shift, units, p.src.c, p.c_in, p.tma_a, p.lbo_a, tid,
+                                 nthr);
+  else if (p.xf_act == SIGE_ACT_RELU)
+    xform_chunk_t<SIGE_ACT_RELU>(abuf, ch, s_rown, xf_scale, xf_shift, units, p.src.c, p.c_in, p.tma_a, p.lbo_a, tid,
+                                 nthr);
+  else
+    xform_chunk_t<-1>(abuf, ch, s_rown, xf_scale, xf_shift, units, p.src.c, p.c_in, p.tma_a, p.lbo_a, tid, nthr);
 }
 
 // The pending element-wise chain over a partial unit's values. Inlined: the
@@ -945,6 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t bar_red_full, bar_red_empty;  // split-K reduce-scatter (ks > 1)
   __shared__ uint32_t tmem_base;
   __shared__ int4 s_tile[16];  // producers' current item tiles: (n, window origin y, x, -); n = -1 empty slot
+  __shared__ int16_t s_rown[kMaxARows];  // transform: sample of each staged A row, -1 = no pixel data
   __shared__ float s_bias[kMaxNTile], s_asc[kMaxNTile], s_ash[kMaxNTile];  // epilogue operands of the item
 
   uint8_t* abuf0 = smem;
@@ -1015,6 +1120,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_slices = p.w_slices[nti];
   const float inv_slices = p.w_inv_slices[nti];
   const int n_items = items_m * n_slices;
+  // Epilogue warps help the producers transform the first item's chunks (see the epilogue branch).
+  const bool helpers = p.xform && p.tma_a && cid < n_items && p.dbg != 12;
   const int tps = p.tps[nti];
   const int tgroups = p.w_tgroups[nti];
   const uint32_t tap_b = static_cast<uint32_t>(n_tile * 128);  // one tap of B in smem
@@ -1044,9 +1151,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
       int unit_n[kUnitRegs];
-      const bool fast_units =
-          F16 && p.async_a && (!p.tma_a || p.xform) && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
+      const bool fast_units = F16 && p.async_a && !p.tma_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
+      if (p.xform) {
+        fill_row_samples(p, row_tab, s_tile, s_rown);
+        asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+      }
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 2);
       if (it == 0) {
         // Everything above reads only the tile lists (IndexPlan output, complete
@@ -1084,10 +1194,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               sc = __ldg(s.epi.scale[0] + off);
               sh = __ldg(s.epi.shift[0] + off);
             }
+            if (p.xf_act == SIGE_ACT_SILU) {  // halved for the transform's SiLU form (exact: power of two)
+              sc *= 0.5f;
+              sh *= 0.5f;
+            }
             xf_scale[n * s.c + c] = sc;
             xf_shift[n * s.c + c] = sh;
           }
           asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
+          // helpers (epilogue warps) transform item 0 with us: tables ready
+          if (helpers) asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));
         }
       }
       if (p.tma_a) {
@@ -1128,8 +1244,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (prev_sidx >= 0) {
             mbar_wait(&bar_aland[prev_sidx], prev_phase);
-            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, pix_off, unit_n, xf_scale, xf_shift);
+            if (threadIdx.x == 0 && it == 0 && ch - 1 == c_begin) tl_mark(p, 38);
+            const bool help = helpers && it == 0;
+            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, s_rown, xf_scale, xf_shift, threadIdx.x,
+                        help ? kProdThreads + kEpiThreads : kProdThreads);
+            if (threadIdx.x == 0 && it == 0 && ch - 1 == c_begin) tl_mark(p, 39);
             fence_proxy_async();
+            if (help) asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));  // helpers' units done
             mbar_arrive(&bar_afull[prev_sidx]);
           }
           if (p.xform) {
@@ -1161,7 +1282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               asm volatile("cp.async.wait_group 1;" ::: "memory");
             else
               asm volatile("cp.async.wait_group 0;" ::: "memory");
-            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, pix_off, unit_n, xf_scale, xf_shift);
+            xform_chunk(p, abuf0 + prev_sidx * p.a_bytes, ch - 1, s_rown, xf_scale, xf_shift, threadIdx.x,
+                        kProdThreads);
             fence_proxy_async();
             mbar_arrive(&bar_afull[prev_sidx]);
           }
@@ -1199,6 +1321,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kEpiBase / 32) {
+    if (helpers) {
+      // Transform helpers for the first item (TMA windows + GroupNorm/act
+      // chain): the in-shared-memory transform of a 64-channel chunk is
+      // latency-bound per warp (tools/xform_bench.cu: 6.9k cycles on the 2
+      // producer warps, 2.3k on 8), and these warps are idle until the first
+      // accumulator is ready. Item 0's chunk k sits in A slot k % na, phase
+      // (k / na) & 1; barrier 3 (producers + helpers) brackets the tables and
+      // every chunk, so the producers arrive on bar_afull only after all
+      // units of the chunk are transformed.
+      asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));  // tables folded
+      const int htid = kProdThreads + static_cast<int>(threadIdx.x) - kEpiBase;
+      for (int k = 0; k < c_end - c_begin; ++k) {
+        const int slot = k % p.na;
+        mbar_wait(&bar_aland[slot], static_cast<uint32_t>(k / p.na) & 1u);
+        xform_chunk(p, abuf0 + slot * p.a_bytes, c_begin + k, s_rown, xf_scale, xf_shift, htid,
+                    kProdThreads + kEpiThreads);
+        fence_proxy_async();
+        asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));
+      }
+    }
     // ---------------- epilogue ----------------
     const int q = warp & 3;                       // TMEM lane quarter of this warp
     const int m = q * 32 + lane;                  // TMEM lane = GEMM row
@@ -1841,7 +1983,20 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     p.ks = ks;
     p.red_bytes = ks > 1 ? (ks - 1) * 128 * (nt / ks) * 4 : 0;
     const size_t fixed = static_cast<size_t>(rowtab_bytes) + p.xf_bytes + p.red_bytes;
+    long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
+    if (nt) max_ctas = static_cast<long long>(items_m) * (p.n_pad / nt) * ks;
+    const int sms = std::max(ks, sms_use / ks * ks);
+    grid = static_cast<int>(std::max<long long>(ks, std::min<long long>(max_ctas, sms)));
     p.na = kMaxNA;
+    static const bool na_full = std::getenv("SIGE_NA_FULL") != nullptr;  // A/B switch
+    if (nt && max_ctas <= grid && !na_full) {
+      // Static launch, one item per CTA: A slots beyond the CTA's own K chunks
+      // would idle; their bytes go to the weight ring instead (with one chunk
+      // per CTA — deep split-K — the whole chunk's weights are then requested
+      // before the dependency wait instead of streaming behind the MMAs).
+      const int cpc = (p.nchunks + ks - 1) / ks;
+      p.na = std::max(1, std::min(kMaxNA, cpc));
+    }
     auto b_room = [&] { return static_cast<long long>(kDynSmem) - static_cast<long long>(fixed) -
                                static_cast<long long>(p.na) * p.a_bytes; };
     while (p.na > 2 && b_room() < 2LL * max_stage) --p.na;
@@ -1863,10 +2018,6 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
     }
     p.ks_log2 = ks == 1 ? 0 : ks == 2 ? 1 : ks == 4 ? 2 : 3;
     for (int r = 0; r <= ks; ++r) p.c_lo[r] = r * p.nchunks / ks;
-    long long max_ctas = static_cast<long long>((tiles.capacity + p.T - 1) / p.T) * (p.n_pad / 16);
-    if (nt) max_ctas = static_cast<long long>(items_m) * (p.n_pad / nt) * ks;
-    const int sms = std::max(ks, sms_use / ks * ks);
-    grid = static_cast<int>(std::max<long long>(ks, std::min<long long>(max_ctas, sms)));
     return fixed + static_cast<size_t>(p.na) * p.a_bytes + static_cast<size_t>(p.b_ring_bytes);
   };
 
