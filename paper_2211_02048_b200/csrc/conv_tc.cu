@@ -1135,6 +1135,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < kProdThreads / 32) {
     // ---------------- A producers ----------------
     const uint32_t a0 = smem_u32(abuf0);
+    // TMA windows of K chunk `ch` of the current item (s_tile) into A slot
+    // `sidx`: one 4-D box (64 channels x plane) per tile and phase plane.
+    auto issue_a = [&](int sidx, int ch, int nt) {
+      uint64_t* bar = p.xform ? &bar_aland[sidx] : &bar_afull[sidx];
+      mbar_expect_tx(bar, static_cast<uint32_t>(nt * p.phases * p.tma_box_bytes));
+      const uint32_t base = a0 + sidx * p.a_bytes;
+      for (int t = 0; t < nt; ++t) {
+        const int4 tl = s_tile[t];
+        for (int ph = 0; ph < p.phases; ++ph)  // stride 2: element stride 2 picks the phase plane
+          tma_4d(base + (ph * p.T + t) * p.Mt * 128, &amap, ch * 64, tl.z + (ph & 1), tl.y + (ph >> 1), tl.x, bar);
+      }
+    };
+    // The first item's first chunk is requested right after the dependency
+    // wait, ahead of the GroupNorm fold (the windows do not depend on it).
+    const bool early_a = p.tma_a && c_begin < c_end;
+    if (threadIdx.x == 0 && p.tma_a) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
     uint32_t a_iter = 0, it = 0, aphase = 0;
     int aslot = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
@@ -1170,6 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           atomicMin(p.gtl + 2 * kGtlLaunchesDev + p.gtl_idx, t);
         }
         if (threadIdx.x == 0) tl_mark(p, 49);
+        if (early_a && threadIdx.x == 0) issue_a(0, c_begin, nt);  // slot 0, first use: no free-wait
         if (p.xform) {
           // Scale-shift table of the transform, for this CTA's input channels only
           // (its K chunks): folded from the GroupNorm statistics the previous
@@ -1213,7 +1230,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (gather's zero fill). With a pending chain the boxes land on
         // bar_aland and the producers transform chunk c-1 (in-canvas units
         // only) while chunk c is in flight, then arrive on bar_afull.
-        const uint32_t bytes = static_cast<uint32_t>(nt * p.phases * p.tma_box_bytes);
         int prev_sidx = -1;
         uint32_t prev_phase = 0;
         const int ch_last = p.xform ? c_end : c_end - 1;
@@ -1223,17 +1239,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (ch < c_end) {
             sidx = aslot;
             sphase = aphase;
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0 && !(it == 0 && ch == c_begin && early_a)) {
               if (a_iter >= static_cast<uint32_t>(p.na)) mbar_wait(&bar_afree[sidx], aphase ^ 1);
-              uint64_t* bar = p.xform ? &bar_aland[sidx] : &bar_afull[sidx];
-              mbar_expect_tx(bar, bytes);
-              const uint32_t base = a0 + sidx * p.a_bytes;
-              for (int t = 0; t < nt; ++t) {
-                const int4 tl = s_tile[t];
-                for (int ph = 0; ph < p.phases; ++ph)  // stride 2: element stride 2 picks the phase plane
-                  tma_4d(base + (ph * p.T + t) * p.Mt * 128, &amap, ch * 64, tl.z + (ph & 1), tl.y + (ph >> 1), tl.x,
-                         bar);
-              }
+              issue_a(sidx, ch, nt);
               if (it == 0 && ch - c_begin < 8) tl_mark(p, 14 + ch - c_begin);
             }
             if (++aslot == p.na) {
