@@ -323,6 +323,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Split form of tmem_ld16 for software pipelining: the load is issued, and
+// the registers only become readable after tmem_wait_regs, whose in-out
+// operands keep the compiler from hoisting any use above the wait.
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -1411,9 +1430,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint32_t tbase = taddr + (static_cast<uint32_t>(q * 32) << 16) + acc * kMaxNTile;
       if (p.ks == 1) {
+        // Software-pipelined TMEM reads: block cb+16 is in flight while
+        // block cb's stores issue (one tcgen05.ld round trip per 16 columns
+        // was on the epilogue's critical path).
+        uint32_t rcur[16], rnext[16];
+        if (!dry) {
+          tmem_ld16_issue(tbase, rcur);
+          tmem_wait_regs(rcur);
+        }
         for (int cb = 0; cb < n_tile; cb += 16) {
           float v[16];
-          if (!dry) tmem_ld16(tbase + static_cast<uint32_t>(cb), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(rcur[j]);
+          const bool more = !dry && cb + 16 < n_tile;
+          if (more) tmem_ld16_issue(tbase + static_cast<uint32_t>(cb + 16), rnext);
           if (threadIdx.x == kEpiBase && it == 0 && cb == 0) tl_mark(p, 46);
           float aux_cur[16];
 #pragma unroll
@@ -1436,6 +1466,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (valid || dry) out16(p, pix, n, y, x, oc, v, wv, ops, dry);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid || dry, wv, dry);
           if (dry) break;
+          if (more) {
+            tmem_wait_regs(rnext);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rcur[j] = rnext[j];
+          }
         }
       } else {
         // Split-K reduce-scatter over DSMEM: every CTA stores the partial
