@@ -332,6 +332,30 @@ int sige_model_required_dilation(const sige_model_desc* model, int* out);
 /* model_weight_hash (models.hpp:17, models.cpp:185-207). */
 uint64_t sige_model_weight_hash(const sige_model_desc* model);
 
+/* ---- on-disk exchange formats (io.hpp:12-36, io.cpp) ----------------------
+ * Host buffers, host files. Same byte layouts and ConfigError messages as the
+ * reference; files written here load in the reference and vice versa. */
+
+/* save_tensor (io.hpp:14, io.cpp:34-51,87-91): SIGT v1, little-endian. */
+int sige_save_tensor(const char* path, const float* host, int n, int c, int h, int w);
+/* load_tensor (io.hpp:15, io.cpp:58-85,93-102): dims[4] = n,c,h,w; pass
+ * host = NULL to read the header only. Zero dimensions are rejected. */
+int sige_load_tensor(const char* path, float* host, size_t cap, int* dims);
+/* save_mask_pbm (io.hpp:18, io.cpp:104-114): plain PBM (P1). */
+int sige_save_mask_pbm(const char* path, const uint8_t* mask, int h, int w);
+/* load_mask_pbm (io.hpp:19, io.cpp:118-160): *h, *w always; mask = NULL for
+ * the header only. Comments and unseparated digits are accepted. */
+int sige_load_mask_pbm(const char* path, uint8_t* mask, size_t cap, int* h, int* w);
+/* save_block_stack (io.hpp:33, io.cpp:405-421): <prefix>.sigt payload
+ * (count, channels, block+overlap, block+overlap) + <prefix>.json sidecar
+ * ("sige_blocks_v1", byte-identical to the reference's dump). */
+int sige_save_block_stack(const char* prefix, const float* host, int count, int channels, int block, int overlap,
+                          int origin_block, int origin_h, int origin_w, const int32_t* idx);
+/* load_block_stack (io.hpp:34, io.cpp:423-457): meta[7] = {count, channels,
+ * block, overlap, origin_block, origin_h, origin_w}; host / idx may be NULL
+ * (header only). */
+int sige_load_block_stack(const char* prefix, float* host, size_t cap, int32_t* idx, size_t idx_cap, int* meta);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

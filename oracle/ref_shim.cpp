@@ -22,6 +22,9 @@
 #include "sige/models.hpp"
 #include "sige/norm.hpp"
 #include "sige/tensor.hpp"
+#ifdef SIGE_REF_IO
+#include "sige/io.hpp"
+#endif
 #include "sige_b200.h"
 
 using namespace sigeref;
@@ -643,3 +646,63 @@ int ref_cache_put_norm(void* cache, int step, const char* key, const float* scal
 }
 
 }  // extern "C"
+
+#ifdef SIGE_REF_IO
+// On-disk formats through the reference's own io.cpp (io.hpp:12-36): the
+// tests exchange files both ways with the library's sige_save_* / sige_load_*.
+extern "C" {
+
+int ref_io_save_tensor(const char* path, const float* x, int n, int c, int h, int w) {
+  return guarded([&] { save_tensor(path, to_tensor(x, n, c, h, w)); });
+}
+
+int ref_io_load_tensor(const char* path, float* out, size_t cap, int* dims) {
+  return guarded([&] {
+    Tensor t = load_tensor(path);
+    dims[0] = t.n, dims[1] = t.c, dims[2] = t.h, dims[3] = t.w;
+    if (out && cap >= t.data.size()) from_tensor(t, out);
+  });
+}
+
+int ref_io_save_mask_pbm(const char* path, const uint8_t* m, int h, int w) {
+  return guarded([&] { save_mask_pbm(path, to_mask(m, h, w)); });
+}
+
+int ref_io_load_mask_pbm(const char* path, uint8_t* out, size_t cap, int* h, int* w) {
+  return guarded([&] {
+    DifferenceMask m = load_mask_pbm(path);
+    *h = m.h, *w = m.w;
+    if (out && cap >= m.bits.size()) std::memcpy(out, m.bits.data(), m.bits.size());
+  });
+}
+
+int ref_io_save_block_stack(const char* prefix, const float* data, int count, int channels, int block, int overlap,
+                            int origin_block, int origin_h, int origin_w, const int32_t* idx) {
+  return guarded([&] {
+    BlockStack st;
+    st.channels = channels;
+    st.block = block;
+    st.overlap = overlap;
+    st.origin = to_index_set(idx, count, origin_block, origin_h, origin_w);
+    st.data.assign(data, data + static_cast<size_t>(count) * channels * (block + overlap) * (block + overlap));
+    save_block_stack(prefix, st);
+  });
+}
+
+int ref_io_load_block_stack(const char* prefix, float* data, size_t cap, int32_t* idx, size_t idx_cap, int* meta) {
+  return guarded([&] {
+    BlockStack st = load_block_stack(prefix);
+    meta[0] = static_cast<int>(st.count()), meta[1] = st.channels, meta[2] = st.block, meta[3] = st.overlap;
+    meta[4] = st.origin.block_size, meta[5] = st.origin.h, meta[6] = st.origin.w;
+    if (data && cap >= st.data.size()) std::memcpy(data, st.data.data(), st.data.size() * sizeof(float));
+    if (idx && idx_cap >= 3 * st.count())
+      for (size_t g = 0; g < st.count(); ++g) {
+        idx[3 * g] = st.origin.indices[g].n;
+        idx[3 * g + 1] = st.origin.indices[g].r;
+        idx[3 * g + 2] = st.origin.indices[g].c;
+      }
+  });
+}
+
+}  // extern "C"
+#endif  // SIGE_REF_IO

@@ -307,6 +307,66 @@ def make_edit_fixture(kind: str, n: int, c: int, h: int, w: int, seed: int):
     return o, e
 
 
+# ------------------------------------------------ on-disk formats (io.hpp) --
+
+def save_tensor(path: str, t: torch.Tensor) -> None:
+    """io.hpp:14 — SIGT v1 file of a 4-D float32 tensor (host copy taken)."""
+    t = t.detach().to("cpu", torch.float32).contiguous()
+    if t.dim() != 4:
+        raise ConfigError("save_tensor: expected a 4-D tensor")
+    _check(_lib().sige_save_tensor(str(path).encode(), t.data_ptr(), *t.shape))
+
+
+def load_tensor(path: str) -> torch.Tensor:
+    """io.hpp:15 — host float32 (n, c, h, w) tensor."""
+    dims = (C.c_int * 4)()
+    _check(_lib().sige_load_tensor(str(path).encode(), None, 0, dims))
+    t = torch.empty(tuple(dims), dtype=torch.float32)
+    _check(_lib().sige_load_tensor(str(path).encode(), t.data_ptr(), t.numel(), dims))
+    return t
+
+
+def save_mask_pbm(path: str, mask: torch.Tensor) -> None:
+    """io.hpp:18 — plain PBM (P1) of an (h, w) uint8 mask."""
+    m = mask.detach().to("cpu", torch.uint8).contiguous()
+    _check(_lib().sige_save_mask_pbm(str(path).encode(), m.data_ptr(), *m.shape))
+
+
+def load_mask_pbm(path: str) -> torch.Tensor:
+    """io.hpp:19 — host (h, w) uint8 mask."""
+    h, w = C.c_int(0), C.c_int(0)
+    _check(_lib().sige_load_mask_pbm(str(path).encode(), None, 0, C.byref(h), C.byref(w)))
+    m = torch.empty((h.value, w.value), dtype=torch.uint8)
+    _check(_lib().sige_load_mask_pbm(str(path).encode(), m.data_ptr(), m.numel(), C.byref(h), C.byref(w)))
+    return m
+
+
+def save_block_stack(prefix: str, blocks: torch.Tensor, idx: torch.Tensor, block: int, overlap: int,
+                     origin_hw: tuple[int, int], origin_block: int | None = None) -> None:
+    """io.hpp:33 — <prefix>.sigt + <prefix>.json (sige_blocks_v1)."""
+    b = blocks.detach().to("cpu", torch.float32).contiguous()
+    i = idx.detach().to("cpu", torch.int32).contiguous()
+    g = int(i.shape[0])
+    ch = int(b.shape[1]) if b.dim() == 4 else 0
+    _check(_lib().sige_save_block_stack(str(prefix).encode(), b.data_ptr(), g, ch, block, overlap,
+                                        block if origin_block is None else origin_block, origin_hw[0],
+                                        origin_hw[1], i.data_ptr()))
+
+
+def load_block_stack(prefix: str) -> dict:
+    """io.hpp:34 — {blocks (G, C, bh, bh), idx (G, 3), block, overlap, origin_block, origin_hw}."""
+    meta = (C.c_int * 7)()
+    _check(_lib().sige_load_block_stack(str(prefix).encode(), None, 0, None, 0, meta))
+    g, ch, block, overlap = meta[0], meta[1], meta[2], meta[3]
+    bh = block + overlap
+    blocks = torch.empty((g, ch, bh, bh), dtype=torch.float32)
+    idx = torch.empty((g, 3), dtype=torch.int32)
+    _check(_lib().sige_load_block_stack(str(prefix).encode(), blocks.data_ptr(), blocks.numel(), idx.data_ptr(),
+                                        idx.numel(), meta))
+    return {"blocks": blocks, "idx": idx, "block": block, "overlap": overlap, "origin_block": meta[4],
+            "origin_hw": (meta[5], meta[6])}
+
+
 class Model:
     """A model description (graph.hpp:63-71): a named synthetic model or a
     ModelDesc pointer supplied by the caller (kept alive by ``owner``)."""

@@ -192,6 +192,12 @@ SYMBOLS = {
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),
+    "sige_save_tensor": (_i, [C.c_char_p, _vp, _i, _i, _i, _i]),
+    "sige_load_tensor": (_i, [C.c_char_p, _vp, C.c_size_t, C.POINTER(_i)]),
+    "sige_save_mask_pbm": (_i, [C.c_char_p, _vp, _i, _i]),
+    "sige_load_mask_pbm": (_i, [C.c_char_p, _vp, C.c_size_t, C.POINTER(_i), C.POINTER(_i)]),
+    "sige_save_block_stack": (_i, [C.c_char_p, _vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "sige_load_block_stack": (_i, [C.c_char_p, _vp, C.c_size_t, _vp, C.c_size_t, C.POINTER(_i)]),
     "sige_model_build": (_i, [C.c_char_p, C.POINTER(C.POINTER(ModelDesc))]),
     "sige_model_free": (None, [C.POINTER(ModelDesc)]),
     "sige_model_required_dilation": (_i, [C.POINTER(ModelDesc), C.POINTER(_i)]),

@@ -16,6 +16,17 @@
 
 using namespace sige_b200;
 
+namespace sige_b200 {  // io.cpp
+void io_write_sigt(const std::string& path, const uint32_t d[4], const float* data);
+void io_read_sigt(const std::string& path, uint32_t d[4], float* out, size_t cap);
+void io_save_mask_pbm(const std::string& path, const uint8_t* m, int h, int w);
+void io_load_mask_pbm(const std::string& path, int* h, int* w, uint8_t* out, size_t cap);
+void io_save_block_stack(const std::string& prefix, const float* data, int count, int channels, int block,
+                         int overlap, int origin_block, int origin_h, int origin_w, const int32_t* idx);
+void io_load_block_stack(const std::string& prefix, int meta[7], float* data, size_t cap, int32_t* idx,
+                         size_t idx_cap);
+}  // namespace sige_b200
+
 struct sige_engine {
   Engine* impl;
 };
@@ -449,5 +460,70 @@ int sige_model_required_dilation(const sige_model_desc* model, int* out) {
 }
 
 uint64_t sige_model_weight_hash(const sige_model_desc* model) { return model_weight_hash(model); }
+
+// ---- on-disk exchange formats (io.cpp) ----
+
+int sige_save_tensor(const char* path, const float* host, int n, int c, int h, int w) {
+  return guarded([&] {
+    need(path, "save_tensor");
+    if (n < 0 || c < 0 || h < 0 || w < 0) throw ConfigError("save_tensor: negative dimension");
+    if (static_cast<size_t>(n) * c * h * w) need(host, "save_tensor");
+    const uint32_t d[4] = {static_cast<uint32_t>(n), static_cast<uint32_t>(c), static_cast<uint32_t>(h),
+                           static_cast<uint32_t>(w)};
+    io_write_sigt(path, d, host);
+  });
+}
+
+int sige_load_tensor(const char* path, float* host, size_t cap, int* dims) {
+  return guarded([&] {
+    need(path, "load_tensor");
+    need(dims, "load_tensor");
+    uint32_t d[4];
+    io_read_sigt(path, d, nullptr, 0);
+    for (uint32_t v : d)
+      if (v == 0) throw ConfigError(std::string(path) + ": zero dimension");
+    if (host) io_read_sigt(path, d, host, cap);
+    for (int i = 0; i < 4; ++i) dims[i] = static_cast<int>(d[i]);
+  });
+}
+
+int sige_save_mask_pbm(const char* path, const uint8_t* mask, int h, int w) {
+  return guarded([&] {
+    need(path, "save_mask_pbm");
+    need(mask, "save_mask_pbm");
+    io_save_mask_pbm(path, mask, h, w);
+  });
+}
+
+int sige_load_mask_pbm(const char* path, uint8_t* mask, size_t cap, int* h, int* w) {
+  return guarded([&] {
+    need(path, "load_mask_pbm");
+    need(h, "load_mask_pbm");
+    need(w, "load_mask_pbm");
+    io_load_mask_pbm(path, h, w, mask, cap);
+  });
+}
+
+int sige_save_block_stack(const char* prefix, const float* host, int count, int channels, int block, int overlap,
+                          int origin_block, int origin_h, int origin_w, const int32_t* idx) {
+  return guarded([&] {
+    need(prefix, "save_block_stack");
+    if (count < 0 || channels < 0 || block < 1 || overlap < 0)
+      throw ConfigError("save_block_stack: bad block stack geometry");
+    if (count) {
+      need(host, "save_block_stack");
+      need(idx, "save_block_stack");
+    }
+    io_save_block_stack(prefix, host, count, channels, block, overlap, origin_block, origin_h, origin_w, idx);
+  });
+}
+
+int sige_load_block_stack(const char* prefix, float* host, size_t cap, int32_t* idx, size_t idx_cap, int* meta) {
+  return guarded([&] {
+    need(prefix, "load_block_stack");
+    need(meta, "load_block_stack");
+    io_load_block_stack(prefix, meta, host, cap, idx, idx_cap);
+  });
+}
 
 }  // extern "C"
