@@ -48,6 +48,9 @@ uint64_t sige_kernel_launch_count(void);
 
 /* ---- shared descriptors -------------------------------------------------- */
 enum { SIGE_ACT_NONE = 0, SIGE_ACT_RELU = 1, SIGE_ACT_SILU = 2 }; /* eltwise.hpp:12 */
+/* LeakyReLU(0.2) of GauGAN's SPADE blocks: only sige_gather_spade takes it
+ * (the reference's Epilogue has no such step). */
+enum { SIGE_ACT_LEAKY_RELU = 3 };
 enum { SIGE_EPI_SCALE_SHIFT = 0, SIGE_EPI_ACTIVATION = 1 };      /* eltwise.hpp:31-34 */
 #define SIGE_MAX_EPI_STEPS 4
 
@@ -331,6 +334,26 @@ void sige_model_free(sige_model_desc* model);
 int sige_model_required_dilation(const sige_model_desc* model, int* out);
 /* model_weight_hash (models.hpp:17, models.cpp:185-207). */
 uint64_t sige_model_weight_hash(const sige_model_desc* model);
+
+/* ---- SPADE ops (BASELINE config 3, GauGAN SPADE ResBlocks) -----------------
+ * Not in the reference API (per-pixel gamma/beta exceed Epilogue's
+ * per-channel params; no label-map resample); restated in
+ * oracle/sige_oracle.c (orc_gather_spade, orc_resize_nearest), parity bit-exact.
+ *
+ * gather with SPADE modulation: for every in-canvas cell of each window
+ * (geometry and validation exactly as sige_gather), v = x, then the `norm`
+ * chain (the folded, param-free norm as scale-shift steps: p = a*v, v = p + b),
+ * then v = v * (1 + gamma) + beta with gamma/beta the per-pixel modulation
+ * maps (n, c, h, w) at the same cell (two roundings each), then `act`
+ * (SIGE_ACT_*). Out-of-canvas cells stay +0. */
+int sige_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                      const int32_t* idx, int count, int block, int idx_h, int idx_w, int k, int stride,
+                      const sige_epilogue* norm, int act, float* out, sige_stream_t s);
+/* Nearest resample of a (segmentation / label) map by integer factors per
+ * axis (down: sample (y*f, x*f); up: replicate), = torch nearest for integer
+ * ratios. Non-integer ratios fail with "resize_nearest: non-integer scale". */
+int sige_resize_nearest(const float* in, int n, int c, int h, int w, int out_h, int out_w, float* out,
+                        sige_stream_t s);
 
 /* ---- on-disk exchange formats (io.hpp:12-36, io.cpp) ----------------------
  * Host buffers, host files. Same byte layouts and ConfigError messages as the

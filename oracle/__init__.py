@@ -222,6 +222,33 @@ class _Impl:
         self._check(self.fn("gather")(_ptr(x), n, c, h, w, _ptr(idx), len(idx), b, ih, iw, k, s, C.byref(e), _ptr(out)))
         return out
 
+    def gather_spade(self, x, gamma, beta, idx, b, ih, iw, k, s, norm=None, act=0):
+        """SPADE modulation gather — oracle only (orc_gather_spade; no reference function)."""
+        x, gamma, beta = (np.ascontiguousarray(a, np.float32) for a in (x, gamma, beta))
+        idx = np.ascontiguousarray(idx, np.int32)
+        n, c, h, w = x.shape
+        win = s * b + k - s
+        out = np.zeros((len(idx), c, win, win), np.float32)
+        keep = []
+        e = epilogue_struct(norm or [], keep)
+        f = self.lib.orc_gather_spade
+        f.restype = _i
+        f.argtypes = [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(Epilogue), _i, _vp]
+        self._check(f(_ptr(x), _ptr(gamma), _ptr(beta), n, c, h, w, _ptr(idx), len(idx), b, ih, iw, k, s, C.byref(e),
+                      act, _ptr(out)))
+        return out
+
+    def resize_nearest(self, x, oh, ow):
+        """Nearest integer-factor resample — oracle only (orc_resize_nearest)."""
+        x = np.ascontiguousarray(x, np.float32)
+        n, c, h, w = x.shape
+        out = np.zeros((n, c, oh, ow), np.float32)
+        f = self.lib.orc_resize_nearest
+        f.restype = _i
+        f.argtypes = [_vp, _i, _i, _i, _i, _i, _i, _vp]
+        self._check(f(_ptr(x), n, c, h, w, oh, ow, _ptr(out)))
+        return out
+
     def scatter(self, blocks, idx, base):
         blocks = np.ascontiguousarray(blocks, np.float32)
         idx = np.ascontiguousarray(idx, np.int32)

@@ -322,6 +322,7 @@ int orc_mask_to_block_indices(const uint8_t* m, int h, int w, int b, int batch, 
  * Relu x>0?x:0, Silu x/(1+expf(-x)). eltwise.cpp:23-36, 110-150. */
 static float act1(float v, int kind) {
   if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;
+  if (kind == SIGE_ACT_LEAKY_RELU) return v > 0.0f ? v : 0.2f * v;
   if (kind == SIGE_ACT_SILU) return v / (1.0f + expf(-v));
   return v;
 }
@@ -394,6 +395,63 @@ int orc_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, i
       }
     }
   }
+  return 0;
+}
+
+/* SPADE modulation gather (config 3; NOT a reference function — restated
+ * from GauGAN's SPADE block, x_norm * (1 + gamma) + beta, over gather()'s
+ * window geometry, kernels.cpp:39-86). Order: norm chain, m = 1 + gamma,
+ * v = v * m, v = v + beta, act. Out-of-canvas cells stay +0. */
+int orc_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                     const int32_t* idx, int count, int b, int ih, int iw, int k, int s,
+                     const sige_epilogue* norm, int act, float* out) {
+  if (k != 1 && k != 3) return fail("gather: kernel size must be 1 or 3");
+  if (s != 1 && s != 2) return fail("gather: stride must be 1 or 2");
+  int oh = conv_out_dim(h, k, s), ow = conv_out_dim(w, k, s);
+  if (ih != oh || iw != ow)
+    return fail("gather: index set lives at %dx%d but conv output of (%d, %d, %d, %d) is %dx%d", ih,
+                iw, n, c, h, w, oh, ow);
+  int win = s * b + k - s, pad = (k - 1) / 2;
+  size_t wsz = (size_t)win * win;
+  memset(out, 0, (size_t)count * c * wsz * sizeof(float));
+  for (int i = 0; i < count; ++i) {
+    int bn = idx[3 * i], y0 = idx[3 * i + 1] * s - pad, x0 = idx[3 * i + 2] * s - pad;
+    for (int ch = 0; ch < c; ++ch) {
+      size_t plane = ((size_t)bn * c + ch) * h * w;
+      float* dst = out + ((size_t)i * c + ch) * wsz;
+      for (int wy = 0; wy < win; ++wy) {
+        int sy = y0 + wy;
+        if (sy < 0 || sy >= h) continue;
+        for (int wx = 0; wx < win; ++wx) {
+          int sx = x0 + wx;
+          if (sx < 0 || sx >= w) continue;
+          size_t at = plane + (size_t)sy * w + sx;
+          float v = x[at];
+          TRY(epi_value(norm, &v, ch, c, bn));
+          float m = 1.0f + gamma[at];
+          v = v * m;
+          v = v + beta[at];
+          dst[(size_t)wy * win + wx] = act1(v, act);
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* Nearest resample by integer factors (config 3 label maps; not a reference
+ * function): down samples (y*f, x*f), up replicates (y/u, x/u). */
+int orc_resize_nearest(const float* in, int n, int c, int h, int w, int oh, int ow, float* out) {
+  if (oh < 1 || ow < 1 || !((h % oh == 0) || (oh % h == 0)) || !((w % ow == 0) || (ow % w == 0)))
+    return fail("resize_nearest: non-integer scale");
+  for (int p = 0; p < n * c; ++p)
+    for (int y = 0; y < oh; ++y) {
+      int sy = oh <= h ? y * (h / oh) : y / (oh / h);
+      for (int x = 0; x < ow; ++x) {
+        int sx = ow <= w ? x * (w / ow) : x / (ow / w);
+        out[((size_t)p * oh + y) * ow + x] = in[((size_t)p * h + sy) * w + sx];
+      }
+    }
   return 0;
 }
 

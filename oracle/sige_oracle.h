@@ -95,6 +95,12 @@ int orc_dense_forward(const sige_model_desc* m, const float* in, int n, int c, i
 int orc_dense_forward_reused_stats(const sige_model_desc* m, const float* in, int n, int c,
                                    int h, int w, orc_cache* cache, int step, float* out);
 
+/* SPADE ops (config 3): restatements, not reference functions. */
+int orc_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                     const int32_t* idx, int count, int b, int ih, int iw, int k, int s,
+                     const sige_epilogue* norm, int act, float* out);
+int orc_resize_nearest(const float* in, int n, int c, int h, int w, int oh, int ow, float* out);
+
 #ifdef __cplusplus
 }
 #endif

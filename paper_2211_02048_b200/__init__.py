@@ -171,6 +171,40 @@ def gather(x: torch.Tensor, idx: torch.Tensor, block_size: int, k: int, stride: 
     return out
 
 
+ACT_LEAKY_RELU = 3  # SPADE blocks only (include/sige_b200.h)
+
+
+def gather_spade(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, idx: torch.Tensor, block_size: int,
+                 k: int, stride: int, norm: Epilogue | None = None, act: int = 0,
+                 idx_hw: tuple[int, int] | None = None) -> torch.Tensor:
+    """SPADE modulation gather (config 3; not a reference function, restated in
+    orc_gather_spade): window cells -> norm chain -> v * (1 + gamma) + beta -> act."""
+    x = _dev(x, torch.float32, "gather_spade")
+    gamma = _dev(gamma, torch.float32, "gather_spade")
+    beta = _dev(beta, torch.float32, "gather_spade")
+    if gamma.shape != x.shape or beta.shape != x.shape:
+        raise ConfigError("gather_spade: gamma/beta must have the shape of x")
+    idx = _dev(idx, torch.int32, "gather_spade")
+    n, c, h, w = x.shape
+    ih, iw = idx_hw or (_conv_out(h, k, stride), _conv_out(w, k, stride))
+    win = stride * block_size + k - stride
+    out = torch.empty((idx.shape[0], c, max(win, 1), max(win, 1)), dtype=torch.float32, device=x.device)
+    e = _epi(norm)
+    _check(_lib().sige_gather_spade(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), n, c, h, w, idx.data_ptr(),
+                                    idx.shape[0], block_size, ih, iw, k, stride, C.byref(e), act, out.data_ptr(),
+                                    _stream()))
+    return out
+
+
+def resize_nearest(x: torch.Tensor, out_h: int, out_w: int) -> torch.Tensor:
+    """Nearest resample by integer factors (config 3 label maps)."""
+    x = _dev(x, torch.float32, "resize_nearest")
+    n, c, h, w = x.shape
+    out = torch.empty((n, c, out_h, out_w), dtype=torch.float32, device=x.device)
+    _check(_lib().sige_resize_nearest(x.data_ptr(), n, c, h, w, out_h, out_w, out.data_ptr(), _stream()))
+    return out
+
+
 def scatter_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> None:
     b = _dev(blocks, torch.float32, "scatter")
     i = _dev(idx, torch.int32, "scatter")

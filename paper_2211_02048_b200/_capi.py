@@ -192,6 +192,8 @@ SYMBOLS = {
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),
+    "sige_gather_spade": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(Epilogue), _i, _vp, _vp]),
+    "sige_resize_nearest": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     "sige_save_tensor": (_i, [C.c_char_p, _vp, _i, _i, _i, _i]),
     "sige_load_tensor": (_i, [C.c_char_p, _vp, C.c_size_t, C.POINTER(_i)]),
     "sige_save_mask_pbm": (_i, [C.c_char_p, _vp, _i, _i]),

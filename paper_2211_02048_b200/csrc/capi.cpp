@@ -145,6 +145,26 @@ int sige_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, 
   });
 }
 
+int sige_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                      const int32_t* idx, int count, int block, int idx_h, int idx_w, int k, int stride,
+                      const sige_epilogue* norm, int act, float* out, sige_stream_t s) {
+  return guarded([&] {
+    if (count) {
+      need(x, "gather_spade");
+      need(gamma, "gather_spade");
+      need(beta, "gather_spade");
+    }
+    DevEpilogue e = make_dev_epilogue(norm, c, n);
+    op_gather_spade(x, gamma, beta, n, c, h, w, idx, count, block, idx_h, idx_w, k, stride, e, act, out,
+                    as_stream(s));
+  });
+}
+
+int sige_resize_nearest(const float* in, int n, int c, int h, int w, int out_h, int out_w, float* out,
+                        sige_stream_t s) {
+  return guarded([&] { op_resize_nearest(in, n, c, h, w, out_h, out_w, out, as_stream(s)); });
+}
+
 namespace {
 void check_scatter_res(int idx_h, int idx_w, int n, int c, int h, int w, const char* op) {
   if (idx_h != h || idx_w != w)

@@ -347,6 +347,55 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
   }
 }
 
+// SPADE modulation gather (config 3; restated in orc_gather_spade): gather's
+// per-tile walk (above) with v -> norm chain -> v * (1 + gamma) + beta -> act
+// on in-canvas cells, each operation rounded separately (bit-exact to the
+// restatement).
+__device__ __forceinline__ float spade_act(float v, int act, int fma_expf) {
+  if (act == SIGE_ACT_LEAKY_RELU) return v > 0.0f ? v : __fmul_rn(0.2f, v);
+  return dev_act(v, act, fma_expf);
+}
+
+__global__ void k_gather_spade(const float* __restrict__ x, const float* __restrict__ gamma,
+                               const float* __restrict__ beta, int c, int h, int w,
+                               const int32_t* __restrict__ idx, int count, int win, int stride, int pad,
+                               DevEpilogue epi, int act, float* __restrict__ out) {
+  const int wsz = win * win, slab = c * wsz;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1) * stride - pad,
+              ox = __ldg(idx + 3 * i + 2) * stride - pad;
+    float* o = out + static_cast<size_t>(i) * slab;
+    for (int q = threadIdx.x; q < slab; q += blockDim.x) {
+      const int ch = q / wsz, cell = q - ch * wsz, wy = cell / win, wx = cell - wy * win;
+      const int sy = oy + wy, sx = ox + wx;
+      float v = 0.0f;
+      if (sy >= 0 && sy < h && sx >= 0 && sx < w) {
+        const size_t at = ((static_cast<size_t>(n) * c + ch) * h + sy) * w + sx;
+        v = __ldg(x + at);
+        if (epi.num_steps) v = dev_epi(epi, v, ch, c, n);
+        v = __fmul_rn(v, __fadd_rn(1.0f, __ldg(gamma + at)));
+        v = __fadd_rn(v, __ldg(beta + at));
+        v = spade_act(v, act, epi.fma_expf);
+      }
+      o[q] = v;
+    }
+  }
+}
+
+__global__ void k_resize_nearest(const float* __restrict__ in, long long planes, int h, int w, int oh, int ow,
+                                 float* __restrict__ out) {
+  const long long total = planes * oh * ow;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int x = static_cast<int>(e % ow);
+    const long long r = e / ow;
+    const int y = static_cast<int>(r % oh);
+    const long long p = r / oh;
+    const int sy = oh <= h ? y * (h / oh) : y / (oh / h), sx = ow <= w ? x * (w / ow) : x / (ow / w);
+    out[e] = __ldg(in + (p * h + sy) * w + sx);
+  }
+}
+
 __global__ void k_map_fill(sige_scatter_entry* map, long long hw) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < hw;
        p += (long long)gridDim.x * blockDim.x) {
@@ -590,6 +639,34 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
   k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
       blocks, count, c, b, idx, base, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0);
   after_launch("k_scatter");
+}
+
+void op_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                     const int32_t* idx, int count, int b, int ih, int iw, int k, int s, const DevEpilogue& epi,
+                     int act, float* out, cudaStream_t st) {
+  if (k != 1 && k != 3) throw ConfigError("gather: kernel size must be 1 or 3");
+  if (s != 1 && s != 2) throw ConfigError("gather: stride must be 1 or 2");
+  if (act < SIGE_ACT_NONE || act > SIGE_ACT_LEAKY_RELU) throw ConfigError("gather_spade: unknown activation");
+  int oh = conv_out_dim(h, k, s), ow = conv_out_dim(w, k, s);
+  if (ih != oh || iw != ow)
+    throw ConfigError("gather: index set lives at " + std::to_string(ih) + "x" + std::to_string(iw) +
+                      " but conv output of (" + std::to_string(n) + ", " + std::to_string(c) + ", " +
+                      std::to_string(h) + ", " + std::to_string(w) + ") is " + std::to_string(oh) +
+                      "x" + std::to_string(ow));
+  if (count == 0) return;
+  const int win = s * b + k - s;
+  k_gather_spade<<<std::min(count, sm_count() * 16), kThreads, 0, st>>>(x, gamma, beta, c, h, w, idx, count, win,
+                                                                       s, (k - 1) / 2, epi, act, out);
+  after_launch("k_gather_spade");
+}
+
+void op_resize_nearest(const float* in, int n, int c, int h, int w, int oh, int ow, float* out, cudaStream_t st) {
+  if (oh < 1 || ow < 1 || !((h % oh == 0) || (oh % h == 0)) || !((w % ow == 0) || (ow % w == 0)))
+    throw ConfigError("resize_nearest: non-integer scale");
+  const long long total = static_cast<long long>(n) * c * oh * ow;
+  if (total == 0) return;
+  k_resize_nearest<<<grid_for(total), kThreads, 0, st>>>(in, static_cast<long long>(n) * c, h, w, oh, ow, out);
+  after_launch("k_resize_nearest");
 }
 
 int op_build_scatter_map(const int32_t* idx, int count, int b, int h, int w,

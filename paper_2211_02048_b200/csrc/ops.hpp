@@ -37,4 +37,9 @@ void op_conv_cc(const float* in, long long in_stride, int ci, int ih, int iw, co
                 const float* bias, int co, int k, int s, int pad, float* out, long long out_stride,
                 int oh, int ow, int items, int math, cudaStream_t st);
 
+void op_gather_spade(const float* x, const float* gamma, const float* beta, int n, int c, int h, int w,
+                     const int32_t* idx, int count, int b, int ih, int iw, int k, int s, const DevEpilogue& epi,
+                     int act, float* out, cudaStream_t st);
+void op_resize_nearest(const float* in, int n, int c, int h, int w, int oh, int ow, float* out, cudaStream_t st);
+
 }  // namespace sige_b200
