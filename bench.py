@@ -509,6 +509,19 @@ def main_ours(args):
                                                         sms=max(1, sms // 4))
         except Exception as e:  # report, never hide
             line["batched_requests"] = {"error": str(e)}
+    # Tensor-pipe context at throughput-shaped work (same kernels): the whole
+    # dense pass, and the batched requests' aggregate (algorithmic FLOPs = the
+    # reference's MAC counts x 2, graph.cpp:712-714) — the single edit is
+    # latency-bound (80 dependent launches), these show what the kernel does
+    # when the GPU is given work.
+    ctx = {"dense_pass_tflops": round(2 * dense_macs / (dense_ms * 1e-3) / 1e12, 2)}
+    ctx["dense_pass_frac"] = round(ctx["dense_pass_tflops"] / bf16_peak, 4)
+    br = line.get("batched_requests", {})
+    if "ms_per_round" in br:
+        ctx["batched_requests_tflops"] = round(br["requests_per_gpu"] * 2 * macs / (br["ms_per_round"] * 1e-3) / 1e12, 2)
+        ctx["batched_requests_frac"] = round(ctx["batched_requests_tflops"] / bf16_peak, 4)
+    ctx["peak_tflops"] = bf16_peak
+    line["roofline_context"] = ctx
     if world == 1:
         try:
             line["ops_hbm"] = ops_roofline(sb, torch, hbm_peak)
