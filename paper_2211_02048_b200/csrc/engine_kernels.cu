@@ -116,6 +116,33 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
   const int ty = (h + b - 1) / b, tx = (w + b - 1) / b, tiles = ty * tx;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool down_y = h <= H, down_x = w <= W;
+  // The tile rectangle is separable (rows from the tile row, columns from the
+  // tile column): OR each tile row's full-resolution row range into one
+  // bit row first, so a tile tests 1-2 words instead of scanning ~20-40 rows
+  // (almost every tile of a small edit is inactive, the worst case of the scan).
+  uint32_t* rowor = sbits + H * wpr;
+  const bool sep = use_smem && ty * wpr <= 2 * H * wpr;
+  if (sep) {
+    for (int k = threadIdx.x; k < ty * wpr; k += blockDim.x) {
+      const int r = k / wpr, wd = k - r * wpr, R = r * b;
+      const int ly0 = max(0, R - ds), ly1 = min(h - 1, min(h, R + b) - 1 + ds);
+      int fy0, fy1;
+      if (down_y) {
+        const int f = H / h;
+        fy0 = ly0 * f;
+        fy1 = ly1 * f + f - 1;
+      } else {
+        const int u = h / H;
+        fy0 = ly0 / u;
+        fy1 = ly1 / u;
+      }
+      fy0 = max(0, fy0 - df);
+      fy1 = min(H - 1, fy1 + df);
+      uint32_t acc = 0;
+      for (int y = fy0; y <= fy1; ++y) acc |= bits[y * wpr + wd];
+      rowor[k] = acc;
+    }
+  }
   if (threadIdx.x == 0) base = 0;
   __syncthreads();
   for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
@@ -150,7 +177,7 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
       fy1 = min(H - 1, fy1 + df);
       fx0 = max(0, fx0 - df);
       fx1 = min(W - 1, fx1 + df);
-      on = rect_any(bits, wpr, fy0, fy1, fx0, fx1);
+      on = sep ? rect_any(rowor + (t / tx) * wpr, wpr, 0, 0, fx0, fx1) : rect_any(bits, wpr, fy0, fy1, fx0, fx1);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, on);
     if (lane == 0) warp_sums[wid] = __popc(bal);
@@ -585,7 +612,8 @@ void launch_mask_u8_to_bits(const uint8_t* mask, int h, int w, uint32_t* bits, i
 void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate_scale, int batch,
                  const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st) {
   if (num_entries == 0) return;
-  const size_t smem = sizeof(uint32_t) * H * ((W + 31) >> 5);
+  // full-resolution bits + the per-tile-row OR table (tile rows <= 2 H)
+  const size_t smem = sizeof(uint32_t) * 3 * H * ((W + 31) >> 5);
   const int use_smem = smem <= 96 * 1024 ? 1 : 0;
   static bool attr_set = false;
   if (use_smem && smem > 48 * 1024 && !attr_set) {
