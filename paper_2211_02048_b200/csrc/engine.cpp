@@ -177,6 +177,9 @@ Engine::~Engine() {
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   if (cap_stream_) cudaStreamDestroy(cap_stream_);
+  if (side_stream_) cudaStreamDestroy(side_stream_);
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+  if (join_ev_) cudaEventDestroy(join_ev_);
   for (void* p : allocations_) cudaFree(p);
 }
 
@@ -1188,6 +1191,22 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
 // every compiled step, then the restore of the tiles this call dirtied.
 void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
                          const sige_run_config& cfg, cudaStream_t st) {
+  static const bool no_fork = std::getenv("SIGE_NO_FORK") != nullptr;  // A/B switch
+  const bool fork = in_twin_ && !no_fork;
+  if (fork) {
+    // The fp16 input twin depends on the edited input only: it runs on a side
+    // branch (a parallel graph node when captured) beside the mask and the
+    // IndexPlan instead of between the plan and the first conv.
+    if (!side_stream_) {
+      SIGE_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+      SIGE_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+      SIGE_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+    }
+    SIGE_CUDA(cudaEventRecord(fork_ev_, st));
+    SIGE_CUDA(cudaStreamWaitEvent(side_stream_, fork_ev_, 0));
+    launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, side_stream_);
+    SIGE_CUDA(cudaEventRecord(join_ev_, side_stream_));
+  }
   SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
   if (P.stats_used) SIGE_CUDA(cudaMemsetAsync(P.stats, 0, P.stats_used * sizeof(double), st));
   if (mask) {
@@ -1199,7 +1218,10 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
   }
   launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
               static_cast<int>(P.entries.size()), st);
-  if (in_twin_) launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, st);
+  if (fork)
+    SIGE_CUDA(cudaStreamWaitEvent(st, join_ev_, 0));
+  else if (in_twin_)
+    launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, st);
   for (auto& f : P.steps) f(st);
   if (!P.restores.empty())
     launch_restore(P.restores_dev, static_cast<int>(P.restores.size()),

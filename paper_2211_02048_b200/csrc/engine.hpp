@@ -142,6 +142,9 @@ class Engine {
   bool use_graphs_ = true;
   int sm_budget_ = 0;  // 0 = every SM
   cudaStream_t cap_stream_ = nullptr;
+  // fork/join for work off the launch chain (the input twin)
+  cudaStream_t side_stream_ = nullptr;
+  cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
 
   std::string name_;
