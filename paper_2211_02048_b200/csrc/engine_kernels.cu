@@ -456,11 +456,25 @@ __global__ void k_restore(const RestoreJob* __restrict__ jobs, int max_tiles) {
       const int n = j.idx[3 * g], y0 = j.idx[3 * g + 1], x0 = j.idx[3 * g + 2];
       const int rows = min(j.b, j.h - y0), cells = min(j.b, j.w - x0);
       const int vrow = cells * j.c * esz / 16;
-      for (int q = threadIdx.x; q < rows * vrow_full; q += blockDim.x) {
-        const int r = q / vrow_full, v = q - r * vrow_full;
-        if (r >= rows || v >= vrow) continue;
-        const size_t off = (((static_cast<size_t>(n) * j.h + y0 + r) * j.w + x0) * j.c) * esz / 16 + v;
-        reinterpret_cast<uint4*>(j.dst)[off] = reinterpret_cast<const uint4*>(j.src)[off];
+      // 4 vectors in flight per thread (one dependent load->store per pass
+      // left the restore latency-bound)
+      constexpr int kR = 4;
+      for (int q0 = threadIdx.x; q0 < rows * vrow_full; q0 += blockDim.x * kR) {
+        uint4 val[kR];
+        size_t off[kR];
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const int q = q0 + u * blockDim.x;
+          const int r = q / vrow_full, v = q - r * vrow_full;
+          off[u] = ~size_t(0);
+          if (q < rows * vrow_full && v < vrow) {
+            off[u] = (((static_cast<size_t>(n) * j.h + y0 + r) * j.w + x0) * j.c) * esz / 16 + v;
+            val[u] = reinterpret_cast<const uint4*>(j.src)[off[u]];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kR; ++u)
+          if (off[u] != ~size_t(0)) reinterpret_cast<uint4*>(j.dst)[off[u]] = val[u];
       }
     }
     return;
