@@ -164,10 +164,10 @@ __global__ void k_blockify(const uint8_t* __restrict__ m, int h, int w, int b, i
 // side walked in (channel, row, tile, column) order — the index set is
 // row-major (mask.cpp:103-136), so a chunk's tiles are mostly horizontal
 // neighbours and a warp's b-wide tile rows merge into full-line stores.
-// (The same staging for gather measured slower than the per-tile walk below:
-// 114-250 us vs 100 us at the ops_hbm workload, profiles/r1_ops_hbm_iter.txt.) Non-adjacent
-// tiles stay correct, only less coalesced. Tiles larger than the staging
-// buffer fall back to a direct walk (staged = false).
+// Non-adjacent tiles stay correct, only less coalesced. Tiles larger than the
+// staging buffer fall back to a direct walk (staged = false). (The same
+// staging for gather measured slower than gather's per-tile walk below:
+// 114-250 us vs 100 us at the ops_hbm workload, profiles/r1_ops_hbm_iter.txt.)
 constexpr int kChunkCols = 256;  // image-side columns (tiles x tile width) per chunk
 constexpr int kMaxChunkTiles = 256;
 constexpr int kStageFloats = 8192;  // 32 KB staging buffer per CTA
@@ -201,7 +201,7 @@ __device__ __forceinline__ void load_origins(int (*s_org)[3], const int32_t* __r
   __syncthreads();
 }
 
-// Column walk shared by both kernels: the image side of an item is a grid of
+// Column walk of the scatter: the image side of an item is a grid of
 // rows (channel, tile row) x cols (tile, tile column). A thread owns one
 // column (one division per column and item) and a strided set of channels,
 // and walks each channel's tile rows with plain pointer arithmetic — no
@@ -218,11 +218,11 @@ struct ColWalk {
   }
 };
 
-// Contiguous per-tile runs between shared memory and a block stack
-// (tile t's run of `run` floats at stack + t * slab), 16-byte vectors when the
-// geometry keeps them aligned.
-template <bool kToStack>
-__device__ __forceinline__ void stack_runs(float* stack, size_t slab, float* sbuf, int tc, int run, bool vec) {
+// Contiguous per-tile runs of a block stack (tile t's `run` floats at
+// stack + t * slab) into shared memory (sbuf + t * run), 16-byte vectors when
+// the geometry keeps them aligned.
+__device__ __forceinline__ void stack_to_smem(const float* stack, size_t slab, float* sbuf, int tc, int run,
+                                              bool vec) {
   const int v = vec ? 4 : 1, rv = run / v;
   const int tpp = rv >= static_cast<int>(blockDim.x) ? 1 : static_cast<int>(blockDim.x) / rv;
   int t = tpp > 1 ? static_cast<int>(threadIdx.x) / rv : 0;
@@ -230,20 +230,13 @@ __device__ __forceinline__ void stack_runs(float* stack, size_t slab, float* sbu
   const int jstep = tpp > 1 ? rv : static_cast<int>(blockDim.x);
   if (t >= tpp) return;
   for (; t < tc; t += tpp) {
-    float* g = stack + t * slab;
+    const float* g = stack + t * slab;
     float* sm = sbuf + t * run;
     for (int j = j0; j < rv; j += jstep) {
-      if (vec) {
-        if (kToStack)
-          reinterpret_cast<float4*>(g)[j] = reinterpret_cast<const float4*>(sm)[j];
-        else
-          reinterpret_cast<float4*>(sm)[j] = __ldg(reinterpret_cast<const float4*>(g) + j);
-      } else {
-        if (kToStack)
-          g[j] = sm[j];
-        else
-          sm[j] = __ldg(g + j);
-      }
+      if (vec)
+        reinterpret_cast<float4*>(sm)[j] = __ldg(reinterpret_cast<const float4*>(g) + j);
+      else
+        sm[j] = __ldg(g + j);
     }
   }
 }
@@ -320,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
     const float* sb = blocks + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * bsz;
     const int run = ncl * bsz;
     if (staged) {
-      stack_runs<false>(const_cast<float*>(sb), slab, s_buf, tc, run, (bsz & 3) == 0);
+      stack_to_smem(sb, slab, s_buf, tc, run, (bsz & 3) == 0);
       __syncthreads();
     }
     // image side: rows (channel, tile row), cols (tile, tile column)
