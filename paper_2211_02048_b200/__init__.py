@@ -465,7 +465,7 @@ class Engine:
         return n.value, c.value, h.value, w.value
 
     def precompute(self, original: torch.Tensor, step: int = 0) -> None:
-        o = _dev(original, torch.float32, "precompute")
+        o = self._check_input(original, "precompute")
         _check(_lib().sige_engine_precompute(self.h, o.data_ptr(), step, _stream()))
 
     def put_tensor(self, key: str, host_nchw, step: int = 0) -> None:
@@ -488,12 +488,62 @@ class Engine:
         _check(_lib().sige_engine_get_norm(self.h, step, key.encode(), sc.data_ptr(), sh.data_ptr(), count))
         return sc, sh
 
+    def _in_shape(self):
+        c, h, w = self.model.in_shape
+        return (self.batch, c, h, w)
+
+    def _check_input(self, x: torch.Tensor, name: str, device: bool = True) -> torch.Tensor:
+        """check_inputs / dense_walk (graph.cpp:348-352,606-614): the edited
+        input must be (batch, in_channels, H, W) float32."""
+        if not isinstance(x, torch.Tensor):
+            raise ConfigError(f"{name}: expected a tensor")
+        if device and not x.is_cuda:
+            raise ConfigError(f"{name}: expected a CUDA tensor")
+        if not device and x.is_cuda:
+            raise ConfigError(f"{name}: expected a host tensor")
+        if x.dtype != torch.float32:
+            raise ConfigError(f"{name}: expected torch.float32, got {x.dtype}")
+        want = self._in_shape()
+        if x.dim() != 4:
+            raise ConfigError(f"{name}: expected a 4-D (n, c, h, w) tensor")
+        if x.shape[1] != want[1]:
+            if name in ("precompute", "dense_forward"):  # dense_walk (graph.cpp:348-352)
+                raise ConfigError(f"forward: input has {x.shape[1]} channels, model expects {want[1]}")
+            raise ConfigError("forward: input channel mismatch")  # check_inputs (graph.cpp:606-609)
+        if tuple(x.shape) != want:
+            raise ConfigError(f"{name}: input is {tuple(x.shape)}, engine expects {want}")
+        return x.contiguous()
+
+    def _check_mask(self, m: torch.Tensor | None, name: str, device: bool = True) -> torch.Tensor | None:
+        if m is None:
+            return None
+        if not isinstance(m, torch.Tensor) or m.is_cuda != device:
+            raise ConfigError(f"{name}: mask must be a {'CUDA' if device else 'host'} tensor")
+        if m.dtype != torch.uint8:
+            raise ConfigError(f"{name}: mask must be torch.uint8, got {m.dtype}")
+        _, _, h, w = self._in_shape()
+        if m.dim() != 2 or tuple(m.shape) != (h, w):
+            mh, mw = (tuple(m.shape) + (0, 0))[:2]
+            raise ConfigError(f"forward: mask is {mh}x{mw} but input is {h}x{w}")
+        return m.contiguous()
+
+    def _check_out(self, out: torch.Tensor | None, like: torch.Tensor, name: str) -> torch.Tensor:
+        shape = self.output_shape()
+        if out is None:
+            return torch.empty(shape, dtype=torch.float32, device=like.device)
+        if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != shape
+                or out.device != like.device or not out.is_contiguous()):
+            raise ConfigError(f"{name}: out must be a contiguous float32 tensor of shape {shape} on {like.device}")
+        return out
+
     def sparse_forward(self, edited: torch.Tensor, mask: torch.Tensor | None = None,
                        config: RunConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
-        e = _dev(edited, torch.float32, "sparse_forward")
-        m = _dev(mask, torch.uint8, "sparse_forward") if mask is not None else None
-        if out is None:
-            out = torch.empty(self.output_shape(), dtype=torch.float32, device=e.device)
+        """sparse_forward (graph.hpp:224-226) on device buffers."""
+        e = self._check_input(edited, "sparse_forward")
+        m = self._check_mask(mask, "sparse_forward")
+        if m is not None and m.device != e.device:
+            raise ConfigError("sparse_forward: mask and input on different devices")
+        out = self._check_out(out, e, "sparse_forward")
         cfg = config or default_config()
         _check(_lib().sige_engine_sparse_forward(self.h, e.data_ptr(), m.data_ptr() if m is not None else None,
                                                  C.byref(cfg), out.data_ptr(), _stream()))
@@ -501,16 +551,22 @@ class Engine:
 
     def sparse_forward_host(self, edited_host: torch.Tensor, mask_host: torch.Tensor | None = None,
                             config: RunConfig | None = None, out_host: torch.Tensor | None = None) -> torch.Tensor:
-        e = edited_host.contiguous()
+        """The host-buffer entry point (H2D, sparse_forward, D2H, synchronise)."""
+        e = self._check_input(edited_host, "sparse_forward_host", device=False)
+        m = self._check_mask(mask_host, "sparse_forward_host", device=False)  # kept alive across the call
+        shape = self.output_shape()
         if out_host is None:
-            out_host = torch.empty(self.output_shape(), dtype=torch.float32)
+            out_host = torch.empty(shape, dtype=torch.float32)
+        elif (out_host.is_cuda or out_host.dtype != torch.float32 or tuple(out_host.shape) != shape
+              or not out_host.is_contiguous()):
+            raise ConfigError(f"sparse_forward_host: out_host must be a contiguous host float32 tensor of shape {shape}")
         cfg = config or default_config()
-        mp = mask_host.contiguous().data_ptr() if mask_host is not None else None
-        _check(_lib().sige_engine_sparse_forward_host(self.h, e.data_ptr(), mp, C.byref(cfg), out_host.data_ptr(), _stream()))
+        _check(_lib().sige_engine_sparse_forward_host(self.h, e.data_ptr(), m.data_ptr() if m is not None else None,
+                                                      C.byref(cfg), out_host.data_ptr(), _stream()))
         return out_host
 
     def dense_forward(self, x: torch.Tensor, reused_stats: bool = False, step: int = 0) -> torch.Tensor:
-        x = _dev(x, torch.float32, "dense_forward")
+        x = self._check_input(x, "dense_forward")
         out = torch.empty(self.output_shape(), dtype=torch.float32, device=x.device)
         _check(_lib().sige_engine_dense_forward(self.h, x.data_ptr(), int(reused_stats), step, out.data_ptr(), _stream()))
         return out

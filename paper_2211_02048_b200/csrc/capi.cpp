@@ -27,8 +27,23 @@ void io_load_block_stack(const std::string& prefix, int meta[7], float* data, si
                          size_t idx_cap);
 }  // namespace sige_b200
 
+// Device staging of the host-buffer entry point, owned by the engine handle
+// (freed in sige_engine_destroy).
+struct HostStage {
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  uint8_t* d_mask = nullptr;
+  size_t in_n = 0, out_n = 0, mask_n = 0;
+  ~HostStage() {
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_mask);
+  }
+};
+
 struct sige_engine {
   Engine* impl;
+  HostStage stage;
 };
 
 namespace {
@@ -75,6 +90,15 @@ uint64_t sige_kernel_launch_count(void) { return g_launches.load(); }
 // Developer instrumentation, not part of the reference-facing ABI: per-launch
 // [start, end] globaltimer of k_conv_tc launches when SIGE_TC_GTL=1.
 int sige_debug_conv_timeline(unsigned long long* out, int cap) { return sige_b200::debug_conv_timeline(out, cap); }
+// Device glibc expf (mode 0) / exact SiLU (mode 1) of the float bit patterns
+// first .. first+count-1, with the libm build the host dispatches to.
+int sige_debug_expf_sweep(uint32_t first, long long count, int mode, float* out, sige_stream_t s) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) throw ConfigError("expf_sweep: mode must be 0 (expf) or 1 (silu)");
+    op_expf_sweep(first, count, mode, out, as_stream(s));
+  });
+}
+int sige_debug_host_expf_is_fma(void) { return sige_b200::host_expf_is_fma() ? 1 : 0; }
 
 void sige_run_config_default(sige_run_config* c) {  // graph.hpp:87-101
   c->step = 0;
@@ -317,7 +341,7 @@ int sige_engine_create(const sige_model_desc* model, int batch, int math_mode, s
 
 void sige_engine_destroy(sige_engine* eng) {
   if (!eng) return;
-  delete eng->impl;
+  delete eng->impl;  // synchronises the device before freeing
   delete eng;
 }
 
@@ -363,22 +387,6 @@ int sige_engine_sparse_forward(sige_engine* eng, const float* edited, const uint
   });
 }
 
-namespace {
-struct HostStage {  // per-engine pinned/device staging for the host-buffer API
-  float* d_in = nullptr;
-  float* d_out = nullptr;
-  uint8_t* d_mask = nullptr;
-  size_t in_n = 0, out_n = 0, mask_n = 0;
-};
-thread_local std::vector<std::pair<const sige_engine*, HostStage>> g_stage;
-HostStage& stage_for(const sige_engine* e) {
-  for (auto& kv : g_stage)
-    if (kv.first == e) return kv.second;
-  g_stage.push_back({e, HostStage{}});
-  return g_stage.back().second;
-}
-}  // namespace
-
 int sige_engine_sparse_forward_host(sige_engine* eng, const float* edited_host,
                                     const uint8_t* mask_host, const sige_run_config* cfg,
                                     float* out_host, sige_stream_t s) {
@@ -391,7 +399,7 @@ int sige_engine_sparse_forward_host(sige_engine* eng, const float* edited_host,
     const size_t in_n = static_cast<size_t>(E.batch()) * E.in_channels() * E.in_h() * E.in_w();
     const size_t out_n = static_cast<size_t>(n) * c * h * w;
     const size_t mask_n = static_cast<size_t>(E.in_h()) * E.in_w();
-    HostStage& S = stage_for(eng);
+    HostStage& S = eng->stage;
     if (S.in_n < in_n) {
       cudaFree(S.d_in);
       SIGE_CUDA(cudaMalloc(&S.d_in, in_n * sizeof(float)));

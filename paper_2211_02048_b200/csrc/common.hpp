@@ -42,6 +42,16 @@ inline void after_launch(const char* name) {
   if (e != cudaSuccess) throw_cuda(e, name, __FILE__, __LINE__);
 }
 
+// True the first time it is called for the current device (per flag word):
+// function attributes such as the dynamic shared-memory limit are per device
+// context, so an engine on a second GPU must set them again.
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = 1ull << dev;
+  return (done.fetch_or(bit) & bit) == 0;
+}
+
 inline cudaStream_t as_stream(sige_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }

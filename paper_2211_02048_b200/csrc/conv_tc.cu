@@ -2075,13 +2075,13 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   else
     fn = f16 ? SIGE_TC_PICK(true, 3, 2) : SIGE_TC_PICK(false, 3, 2);
 #undef SIGE_TC_PICK
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
+  static std::atomic<uint64_t> attr_done{0};
+  if (first_on_device(attr_done)) {
     for (KernelFn f : {k_conv_tc<true, 1, 1, true>, k_conv_tc<false, 1, 1, true>, k_conv_tc<true, 3, 1, true>,
                        k_conv_tc<false, 3, 1, true>, k_conv_tc<true, 3, 2, true>, k_conv_tc<false, 3, 2, true>,
                        k_conv_tc<true, 1, 1, false>, k_conv_tc<true, 3, 1, false>, k_conv_tc<true, 3, 2, false>})
       SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
-  });
+  }
   static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
   auto launch = [&](size_t smem) {
     cudaLaunchConfig_t cfg{};

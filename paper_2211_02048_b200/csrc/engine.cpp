@@ -96,7 +96,9 @@ struct Program {
   bool ran = false;
   double* stats = nullptr;  // GroupNorm statistics arena (fused dense-fallback ResBlocks), zeroed per call
   size_t stats_len = 0, stats_used = 0;
-  std::map<std::tuple<const void*, const void*, const void*>, std::pair<cudaGraphExec_t, int>> graphs;
+  // captured calls keyed by (edited, mask, out, threshold bits): without a
+  // mask the threshold is baked into the captured k_mask_bits launch
+  std::map<std::tuple<const void*, const void*, const void*, uint32_t>, std::pair<cudaGraphExec_t, int>> graphs;
   ~Program() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
   }
@@ -1153,8 +1155,10 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
   // final copy, restore) is captured once per (input, mask, output) binding
   // into a CUDA graph on an internal stream and replayed with one launch.
   if (use_graphs_ && !profiling_ && P.ran) {
+    uint32_t thr_bits = 0;
+    if (!mask) std::memcpy(&thr_bits, &cfg.mask_threshold, sizeof(thr_bits));
     auto key = std::make_tuple(static_cast<const void*>(edited), static_cast<const void*>(mask),
-                               static_cast<const void*>(out));
+                               static_cast<const void*>(out), thr_bits);
     auto it = P.graphs.find(key);
     if (it == P.graphs.end()) {
       if (!cap_stream_) SIGE_CUDA(cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking));

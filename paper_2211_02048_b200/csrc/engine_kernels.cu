@@ -629,11 +629,9 @@ void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate
   // full-resolution bits + the per-tile-row OR table (tile rows <= 2 H)
   const size_t smem = sizeof(uint32_t) * 3 * H * ((W + 31) >> 5);
   const int use_smem = smem <= 96 * 1024 ? 1 : 0;
-  static bool attr_set = false;
-  if (use_smem && smem > 48 * 1024 && !attr_set) {
+  static std::atomic<uint64_t> attr_done{0};
+  if (use_smem && smem > 48 * 1024 && first_on_device(attr_done))
     SIGE_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr_set = true;
-  }
   k_plan<<<num_entries, 1024, use_smem ? smem : 0, st>>>(bits, H, W, dilate_full, dilate_scale,
                                                          batch, entries_dev, use_smem);
   after_launch("k_plan");

@@ -730,4 +730,23 @@ void op_conv_cc(const float* in, long long in_stride, int ci, int ih, int iw, co
   after_launch("k_conv_cc");
 }
 
+// Device expf / SiLU over a contiguous range of float bit patterns (the GPU
+// leg of the exhaustive libm sweep, tests/test_gpu_expf.py): out[i] =
+// f(bits(first + i)) with f = glibc expf (mode 0) or the reference SiLU
+// x / (1 + expf(-x)) (mode 1, eltwise.cpp:31-34) exactly as every exact-mode
+// epilogue evaluates it.
+__global__ void k_expf_sweep(uint32_t first, long long count, int mode, int fma, float* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float x = __uint_as_float(first + static_cast<uint32_t>(i));
+    out[i] = mode == 0 ? glibc_expf(x, fma != 0) : dev_act(x, SIGE_ACT_SILU, fma, 0);
+  }
+}
+
+void op_expf_sweep(uint32_t first, long long count, int mode, float* out, cudaStream_t st) {
+  if (count <= 0) return;
+  k_expf_sweep<<<grid_for(count), kThreads, 0, st>>>(first, count, mode, host_expf_is_fma() ? 1 : 0, out);
+  after_launch("k_expf_sweep");
+}
+
 }  // namespace sige_b200

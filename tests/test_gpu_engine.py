@@ -148,3 +148,64 @@ def test_graph_replay_identical(orc, math):
     for a, b in zip(outs[False], outs[True]):
         assert np.array_equal(a, b)
     assert np.array_equal(outs[True][0], outs[True][4])
+
+
+def test_graph_replay_follows_threshold(orc):
+    """Without a mask the threshold is part of the captured call: alternating
+    thresholds on the same buffers with graphs on must give the same bits as
+    direct launches (compute_difference_mask's strict '>' at each threshold,
+    mask.cpp:14-32)."""
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 41)
+    outs = {}
+    for graphs in (False, True):
+        eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+        eng.set_graphs(graphs)
+        eng.precompute(torch.from_numpy(orig).cuda())
+        x = torch.from_numpy(edited).cuda()
+        out = torch.empty(eng.output_shape(), device="cuda")
+        res = []
+        for thr in (1e-3, 1e-3, 0.3, 1e-3, 0.3, 0.3, 10.0):
+            eng.sparse_forward(x, config=sb.default_config(dilate_full=25, mask_threshold=thr), out=out)
+            res.append(out.cpu().numpy().copy())
+        outs[graphs] = res
+    for a, b in zip(outs[False], outs[True]):
+        assert np.array_equal(a, b)
+    assert not np.array_equal(outs[True][0], outs[True][2])  # 0.3 drops part of the edit
+    om = orc.model("mini_unet_gn")
+    ocache = om.precompute(orig)
+    for i, thr in ((2, 0.3), (6, 10.0)):
+        want, _ = om.sparse_forward(ocache, edited, orc.difference_mask(orig, edited, thr),
+                                    sb.default_config(dilate_full=25))
+        assert np.array_equal(outs[True][i], want)
+
+
+def test_engine_rejects_bad_buffers(orc):
+    """Shape / dtype / device of the edited input, the mask and a caller's out
+    are checked before any device access (check_inputs, graph.cpp:606-614)."""
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 2)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    x = torch.from_numpy(edited).cuda()
+    with pytest.raises(sb.ConfigError, match="forward: input channel mismatch"):
+        eng.sparse_forward(torch.zeros((1, 4, 64, 64), device="cuda"))
+    with pytest.raises(sb.ConfigError, match="engine expects"):
+        eng.sparse_forward(torch.zeros((1, 3, 32, 64), device="cuda"))
+    with pytest.raises(sb.ConfigError, match="float32"):
+        eng.sparse_forward(x.double())
+    with pytest.raises(sb.ConfigError, match="forward: mask is 32x64 but input is 64x64"):
+        eng.sparse_forward(x, torch.ones((32, 64), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(sb.ConfigError, match="uint8"):
+        eng.sparse_forward(x, torch.ones((64, 64), dtype=torch.bool, device="cuda"))
+    with pytest.raises(sb.ConfigError, match="out must be"):
+        eng.sparse_forward(x, out=torch.empty((1, 3, 64, 32), device="cuda"))
+    with pytest.raises(sb.ConfigError, match="out must be"):
+        eng.sparse_forward(x, out=torch.empty(eng.output_shape(), device="cuda").transpose(2, 3))
+    with pytest.raises(sb.ConfigError, match="host tensor"):
+        eng.sparse_forward_host(x)
+    with pytest.raises(sb.ConfigError, match="forward: input has 4 channels, model expects 3"):
+        eng.dense_forward(torch.zeros((1, 4, 64, 64), device="cuda"))
+    # a non-contiguous host mask is copied and kept alive across the call
+    m = torch.from_numpy(orc.difference_mask(orig, edited)).t().contiguous().t()
+    got = eng.sparse_forward_host(torch.from_numpy(edited), m, config=sb.default_config(dilate_full=25))
+    want = eng.sparse_forward(x, m.cuda(), config=sb.default_config(dilate_full=25)).cpu()
+    assert torch.equal(got, want)
