@@ -133,6 +133,10 @@ typedef struct sige_run_config {
   int min_sparse_res;
   int sparse;
   int norm_precompute;
+  /* Ablation toggles of the reference's schedule (graph.cpp:571-582). Their
+   * output is identical by the reference's own tests (test_graph.cpp:215-250);
+   * the device executor always runs the fused schedule, so any value gives the
+   * same result (tests/test_gpu_engine.py). */
   int elem_fusion;
   int scatter_fusion;
   uint32_t seed;
@@ -309,6 +313,16 @@ int sige_engine_set_graphs(sige_engine* eng, int enable);
 int sige_engine_set_sm_budget(sige_engine* eng, int sms);
 int sige_engine_profile_read(sige_engine* eng, double* rows, int cap, int* nrows,
                              sige_stream_t stream);
+/* Graph timeline (measurement; no reference counterpart): with it on, every
+ * tensor-core conv launch of a call stamps %globaltimer at its first CTA's
+ * start, its dependency-wait exit and its last CTA's end — inside replayed
+ * CUDA graphs, so PDL overlap is kept (captured graphs are re-captured when
+ * the switch changes). sige_engine_timeline_read synchronises the device and
+ * returns up to `cap` rows {start_ns, end_ns, wait_ns, algorithmic flops,
+ * sparse flag} of the last call's launches (times relative to the first
+ * start), then resets the stamps. */
+int sige_engine_set_timeline(sige_engine* eng, int enable);
+int sige_engine_timeline_read(sige_engine* eng, double* rows, int cap, int* nrows);
 /* Newline-separated cache listing for `step`: "T <key> <n> <c> <h> <w>" for
  * tensors (reference NCHW shape) and "N <key> <count>" for folded norms.
  * Returns the needed buffer size in *needed. */

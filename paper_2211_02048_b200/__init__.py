@@ -597,6 +597,17 @@ class Engine:
         _check(_lib().sige_engine_profile_read(self.h, rows.data_ptr(), cap, C.byref(n), _stream()))
         return rows[: n.value].clone()
 
+    def set_timeline(self, on: bool) -> None:
+        """Device %globaltimer stamps of every tensor-core conv launch (inside replayed graphs)."""
+        _check(_lib().sige_engine_set_timeline(self.h, int(on)))
+
+    def timeline_read(self, cap: int = 1024):
+        """[(start_ns, end_ns, wait_ns, flops, sparse)] of the last call's conv launches, then reset."""
+        rows = torch.zeros((cap, 5), dtype=torch.float64)
+        n = C.c_int(0)
+        _check(_lib().sige_engine_timeline_read(self.h, rows.data_ptr(), cap, C.byref(n)))
+        return rows[: min(n.value, cap)].clone()
+
     def cache_entries(self, step: int = 0):
         """[("T", key, (n, c, h, w)) | ("N", key, count)] of the device cache."""
         need = C.c_size_t(0)

@@ -4,6 +4,7 @@
 // keeps the message in a thread-local for sige_last_error().
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -291,10 +292,89 @@ int sige_apply_epilogue_on_blocks(float* blocks, int count, int channels, int bh
   });
 }
 
+namespace {
+void check_math_mode(int m, const char* op) {
+  if (m != SIGE_MATH_EXACT && m != SIGE_MATH_FP32_FMA && m != SIGE_MATH_TF32 && m != SIGE_MATH_F16)
+    throw ConfigError(std::string(op) + ": unknown math mode " + std::to_string(m));
+}
+
+// RAII device scratch of an op-level call (freed after the stream drains).
+struct Scratch {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  void* get(size_t bytes) {
+    void* p = nullptr;
+    SIGE_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    ptrs.push_back(p);
+    return p;
+  }
+  ~Scratch() {
+    cudaStreamSynchronize(st);
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+// Op-level conv on the tcgen05 tensor cores (SIGE_MATH_F16 / SIGE_MATH_TF32):
+// the NCHW fp32 source `x` (n, c, h, w) is convolved over the output tile list
+// `tiles` (origins at output resolution) with padding `pad` by the engine's
+// fused kernel (launch_conv_tc) into an NHWC scratch, then written to `out`
+// (NCHW, n x c_out x oh x ow). The weights are packed per call.
+void op_conv_tc(const float* x, int n, int c, int h, int w, const sige_conv_desc& cv, bool with_bias,
+                int math, int pad, const std::vector<int32_t>& tiles_host, int bh, int bw, int oh, int ow,
+                float* out, cudaStream_t st) {
+  Scratch S(st);
+  const bool f16 = math == SIGE_MATH_F16;
+  ConvW cw;
+  cw.c_in = cv.c_in;
+  cw.c_out = cv.c_out;
+  cw.k = cv.k;
+  cw.stride = cv.stride;
+  cw.w = cv.weight;
+  cw.bias = with_bias ? cv.bias : nullptr;
+  pack_weights_tc(cv.weight, cv.c_out, cv.c_in, cv.k, f16 ? 1 : 0, &cw, st);
+  S.ptrs.push_back(const_cast<void*>(cw.w_tc));
+  Src src;
+  src.ptr = x;
+  src.layout = kNCHW;
+  src.n = n;
+  src.c = c;
+  src.h = h;
+  src.w = w;
+  src.epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+  Tiles t;
+  int32_t* idx = static_cast<int32_t*>(S.get(tiles_host.size() * sizeof(int32_t)));
+  SIGE_CUDA(cudaMemcpyAsync(idx, tiles_host.data(), tiles_host.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  t.idx = idx;
+  t.count = static_cast<int>(tiles_host.size() / 3);
+  t.capacity = t.count;
+  t.bh = bh;
+  t.bw = bw;
+  float* tmp = static_cast<float*>(S.get(static_cast<size_t>(n) * oh * ow * cv.c_out * sizeof(float)));
+  Dst d;
+  d.ptr = tmp;
+  d.n = n;
+  d.c = cv.c_out;
+  d.h = oh;
+  d.w = ow;
+  d.mode = kStore;
+  launch_conv_tc(src, t, cw, d, f16 ? 1 : 0, st, 0, nullptr, 0, pad);
+  Src r;
+  r.ptr = tmp;
+  r.layout = kNHWC;
+  r.n = n;
+  r.c = cv.c_out;
+  r.h = oh;
+  r.w = ow;
+  launch_materialize(r, out, kNCHW, st);
+}
+}  // namespace
+
 int sige_conv_on_blocks(const float* blocks, int count, int window, const sige_conv_desc* conv,
                         int with_bias, int math_mode, float* out, int block, sige_stream_t s) {
   return guarded([&] {
     need(conv, "conv_on_blocks");
+    check_math_mode(math_mode, "conv_on_blocks");
     const sige_conv_desc& cv = *conv;
     if (cv.k != 1 && cv.k != 3) throw ConfigError("conv: kernel size must be 1 or 3, got " + std::to_string(cv.k));
     if (cv.stride != 1 && cv.stride != 2)
@@ -304,8 +384,16 @@ int sige_conv_on_blocks(const float* blocks, int count, int window, const sige_c
       throw ConfigError("conv_on_blocks: window " + std::to_string(window) + " with k=" +
                         std::to_string(cv.k) + " s=" + std::to_string(cv.stride) + " yields " +
                         std::to_string(b_out) + ", expected block " + std::to_string(block));
-    if (math_mode == SIGE_MATH_TF32)
-      throw ConfigError("conv_on_blocks: SIGE_MATH_TF32 runs through the engine (fused path)");
+    if (count == 0) return;
+    if (math_mode == SIGE_MATH_TF32 || math_mode == SIGE_MATH_F16) {
+      // one tile per block: the block stack is an NCHW batch of count windows,
+      // each convolved without padding (the gather carried the halo)
+      std::vector<int32_t> tiles(static_cast<size_t>(count) * 3, 0);
+      for (int g = 0; g < count; ++g) tiles[3 * g] = g;
+      op_conv_tc(blocks, count, cv.c_in, window, window, cv, with_bias != 0, math_mode, 0, tiles, block, block,
+                 block, block, out, as_stream(s));
+      return;
+    }
     op_conv_cc(blocks, static_cast<long long>(cv.c_in) * window * window, cv.c_in, window, window,
                cv.weight, with_bias ? cv.bias : nullptr, cv.c_out, cv.k, cv.stride, 0, out,
                static_cast<long long>(cv.c_out) * block * block, block, block, count, math_mode,
@@ -317,13 +405,29 @@ int sige_conv2d(const float* x, int n, int c, int h, int w, const sige_conv_desc
                 int math_mode, float* out, sige_stream_t s) {
   return guarded([&] {
     need(conv, "conv2d");
+    check_math_mode(math_mode, "conv2d");
     const sige_conv_desc& cv = *conv;
     if (c != cv.c_in)
       throw ConfigError("conv2d: input has " + std::to_string(c) + " channels, layer expects " +
                         std::to_string(cv.c_in));
-    if (math_mode == SIGE_MATH_TF32)
-      throw ConfigError("conv2d: SIGE_MATH_TF32 runs through the engine (fused path)");
     int oh = conv_out_dim(h, cv.k, cv.stride), ow = conv_out_dim(w, cv.k, cv.stride);
+    if (math_mode == SIGE_MATH_TF32 || math_mode == SIGE_MATH_F16) {
+      if (cv.k != 1 && cv.k != 3) throw ConfigError("conv: kernel size must be 1 or 3, got " + std::to_string(cv.k));
+      if (cv.stride != 1 && cv.stride != 2)
+        throw ConfigError("conv: stride must be 1 or 2, got " + std::to_string(cv.stride));
+      if (n == 0 || oh <= 0 || ow <= 0) return;
+      // output tiles as the engine's dense pass lays them out (one M=128 MMA each)
+      const int bw = std::min(ow, 16);
+      const int P = cv.stride == 1 ? bw + cv.k - 1 : bw + 1;
+      const int bh = std::max(1, std::min(oh, (128 - bw) / P + 1));
+      std::vector<int32_t> tiles;
+      for (int i = 0; i < n; ++i)
+        for (int r = 0; r < oh; r += bh)
+          for (int q = 0; q < ow; q += bw) tiles.insert(tiles.end(), {i, r, q});
+      op_conv_tc(x, n, c, h, w, cv, with_bias != 0, math_mode, (cv.k - 1) / 2, tiles, bh, bw, oh, ow, out,
+                 as_stream(s));
+      return;
+    }
     op_conv_cc(x, static_cast<long long>(c) * h * w, c, h, w, cv.weight, with_bias ? cv.bias : nullptr,
                cv.c_out, cv.k, cv.stride, (cv.k - 1) / 2, out,
                static_cast<long long>(cv.c_out) * oh * ow, oh, ow, n, math_mode, as_stream(s));
@@ -449,6 +553,14 @@ int sige_engine_set_profiling(sige_engine* eng, int enable) {
 
 int sige_engine_set_sm_budget(sige_engine* eng, int sms) {
   return guarded([&] { eng->impl->set_sm_budget(sms); });
+}
+
+int sige_engine_set_timeline(sige_engine* eng, int enable) {
+  return guarded([&] { eng->impl->set_timeline(enable != 0); });
+}
+
+int sige_engine_timeline_read(sige_engine* eng, double* rows, int cap, int* nrows) {
+  return guarded([&] { *nrows = eng->impl->timeline_read(rows, cap); });
 }
 
 int sige_engine_set_graphs(sige_engine* eng, int enable) {

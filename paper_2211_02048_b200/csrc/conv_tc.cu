@@ -836,9 +836,9 @@ __device__ __forceinline__ const float* aux_ptr(const Dst& d, size_t pix, int n,
 
 // dry: the warm-up pass — same instruction stream, no memory access.
 __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v,
-                                      float* written, const EpiOps& ops, bool dry = false) {
+                                      float* written, const EpiOps& ops, bool dry = false, int lim = 16) {
   const Dst& d = p.dst;
-  const int cnt = min(16, p.c_out - oc0);
+  const int cnt = min(lim, p.c_out - oc0);
   if (cnt <= 0) return;
   if (cnt < 16 || (d.c & 3) != 0 || !addend_vectorizable(d)) {
     if (dry) return;
@@ -949,12 +949,12 @@ __device__ __forceinline__ void gn_flush(const Dst& d, int n, int n0, bool unifo
 }
 
 __device__ __forceinline__ void gn_accumulate(const Dst& d, int c_out, int oc0, int n, bool valid, const float* w,
-                                              bool dry = false) {
+                                              bool dry = false, int lim16 = 16) {
   const int cpg = d.c / d.gn_groups;
   const int n0 = __shfl_sync(0xffffffffu, n, 0);
   const bool uniform_n = __all_sync(0xffffffffu, !valid || n == n0);
   if (!__any_sync(0xffffffffu, valid)) return;
-  const int lim = min(16, c_out - oc0);
+  const int lim = min(lim16, c_out - oc0);
   // One (runtime, uniform) pass per group touched; each pass sums the 16
   // values under a mask so w is only ever indexed at compile time.
   for (int lo = 0; lo < lim;) {
@@ -1758,6 +1758,13 @@ int tps_for(int n_tile, int ntaps) {
   return 1;
 }
 
+// A split of an N tile over ks CTAs: every CTA owns nt / ks output columns,
+// a multiple of 16 (the epilogue's block). Narrower owners (4 / 8 columns,
+// e.g. 16 slices x 8 splits = 128 CTAs for an 8x8 512-channel layer) were
+// measured 2-2.5x slower in the edit's launch chain than 32 CTAs with 16-column
+// owners (profiles/r2_splitk_plans.txt) and are not planned.
+bool split_ok(int nt, int ks) { return nt % (16 * ks) == 0; }
+
 // (N tile, split-K) for a launch whose tile count is known on the host (the
 // dense pass / dense-fallback layers): minimise rounds over the SMs x the
 // per-CTA chain — max(MMA issue at ~max(47, 40 + N/4) cycles per MMA, weight
@@ -1770,7 +1777,7 @@ void plan_static(int items_m, int n_pad, int nchunks, int ntaps, int sms, long l
     if (ks > nchunks) break;
     for (int c = 16; c <= kMaxNTile; c <<= 1) {
       const int nt = std::min(c, n_pad);
-      if (n_pad % nt != 0 || nt % (16 * ks) != 0) continue;
+      if (n_pad % nt != 0 || !split_ok(nt, ks)) continue;
       if (ks > 1 && static_cast<long long>(ks - 1) * 128 * (nt / ks) * 4 > red_cap) continue;
       const long long ctas = static_cast<long long>(items_m) * (n_pad / nt) * ks;
       const long long rounds = (ctas + sms - 1) / sms;
@@ -1871,7 +1878,8 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
 }
 
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st, int sm_budget) {
+                    cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad) {
+  static_assert(kGtlLaunchesDev == kTimelineSlots, "timeline layout");
   const int sms_all = sm_count();
   const int sms_use = sm_budget > 0 ? std::min(sm_budget, sms_all) : sms_all;
   if (!cw.w_tc) throw ConfigError("conv (tensor core): weights were not packed for this path");
@@ -1904,7 +1912,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.c_out = cw.c_out;
   p.k = cw.k;
   p.s = cw.stride;
-  p.pad = (cw.k - 1) / 2;
+  p.pad = pad >= 0 ? pad : (cw.k - 1) / 2;
   p.n_pad = cw.n_pad;
   p.nchunks = cw.k_pad / (f16 ? 64 : 32);
   p.ntaps = cw.k * cw.k;
@@ -2136,7 +2144,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
       plan_static(items_m, p.n_pad, p.nchunks, p.ntaps, sms_use, no_splitk ? -1 : red_cap, &nt_plan, &ks_plan);
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
       SIGE_CUDA(cudaStreamIsCapturing(st, &cap));
-      const bool tunable = !no_tune && force_ks == 0 && cap == cudaStreamCaptureStatusNone &&
+      const bool tunable = !no_tune && force_ks == 0 && !std::getenv("SIGE_FORCE_PLAN") && cap == cudaStreamCaptureStatusNone &&
                            (dst.mode == kStore || dst.mode == kResMain || dst.mode == kAddSrc);
       if (tunable) {
         double* const gn_saved = p.dst.gn_stats;
@@ -2149,7 +2157,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
           if (ks > p.nchunks || (ks > 1 && no_splitk)) break;
           for (int c = 16; c <= kMaxNTile; c <<= 1) {
             const int nt = std::min(c, p.n_pad);
-            if (p.n_pad % nt != 0 || nt % (16 * ks) != 0) continue;
+            if (p.n_pad % nt != 0 || !split_ok(nt, ks)) continue;
             if (ks > 1 && static_cast<long long>(ks - 1) * 128 * (nt / ks) * 4 > red_cap) continue;
             const size_t sm = configure(nt, ks);
             float ms_best = 1e30f;
@@ -2177,6 +2185,17 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
         plans[key] = {nt_plan, ks_plan};
       }
     }
+    // Test hook: SIGE_FORCE_PLAN="nt:ks" pins (N tile, split) wherever that plan is legal.
+    static const char* force_plan = std::getenv("SIGE_FORCE_PLAN");
+    if (force_plan) {
+      int fnt = 0, fks = 0;
+      if (std::sscanf(force_plan, "%d:%d", &fnt, &fks) == 2 && fnt >= 16 && fnt <= kMaxNTile && fks >= 1 &&
+          fks <= 8 && (fks & (fks - 1)) == 0 && fks <= p.nchunks && p.n_pad % fnt == 0 && split_ok(fnt, fks) &&
+          static_cast<long long>(fks - 1) * 128 * (fnt / fks) * 4 <= red_cap) {
+        nt_plan = fnt;
+        ks_plan = fks;
+      }
+    }
     // Test hook: force a split (largest power of two <= the request that the geometry allows).
     for (int f = force_ks; f > 1 && ks_plan == 1; f >>= 1) {
       const int ntf = std::min(p.n_pad, kMaxNTile);
@@ -2198,7 +2217,10 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.dbg = dbg;
   static const bool no_warm = std::getenv("SIGE_NO_WARM") != nullptr;
   p.warm = no_warm ? 0 : 1;
-  if (g_gtl_on) {
+  if (gtl) {  // the engine's graph timeline
+    p.gtl = gtl;
+    p.gtl_idx = gtl_idx % kTimelineSlots;
+  } else if (g_gtl_on) {
     if (!g_gtl_buf) {
       SIGE_CUDA(cudaMalloc(&g_gtl_buf, 3 * kGtlLaunches * 8));
       gtl_reset();

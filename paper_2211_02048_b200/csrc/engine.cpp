@@ -420,7 +420,22 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     }
     SIGE_CUDA(cudaEventRecord(rec.a, st));
   }
-  if (tensor_cores())
+  if (tensor_cores() && timeline_) {
+    const int idx = tl_next_++;
+    if (idx < kTimelineSlots) {
+      TlMeta m{};
+      m.count_dev = t.count_dev;
+      m.count = t.count;
+      // algorithmic FLOPs (graph.cpp:712-714): 2 C_out C_in k^2 b^2 per tile,
+      // exact output pixels for the static (dense) launches
+      m.flops_per_tile = t.count_dev ? 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * t.bh * t.bw
+                                     : 2.0 * cw.c_out * cw.c_in * cw.k * cw.k * dst.h * dst.w * dst.n /
+                                           std::max(1, t.count);
+      m.sparse = t.count_dev ? 1 : 0;
+      tl_meta_.push_back(m);
+    }
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, tl_buf_, idx);
+  } else if (tensor_cores())
     launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
@@ -440,6 +455,59 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
 }
 
 void Engine::set_profiling(bool on) { profiling_ = on; }
+
+void Engine::timeline_reset() {
+  std::vector<unsigned long long> init(3 * kTimelineSlots, ~0ull);  // [start, end] pairs, then wait exits
+  for (int i = 0; i < kTimelineSlots; ++i) init[2 * i + 1] = 0;
+  SIGE_CUDA(cudaMemcpy(tl_buf_, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+}
+
+void Engine::drop_graphs() {
+  SIGE_CUDA(cudaDeviceSynchronize());
+  for (auto& kv : programs_) {
+    for (auto& g : kv.second->graphs) cudaGraphExecDestroy(g.second.first);
+    kv.second->graphs.clear();
+  }
+}
+
+void Engine::set_timeline(bool on) {
+  if (on == timeline_) return;
+  if (on && !tl_buf_) {
+    tl_buf_ = static_cast<unsigned long long*>(alloc(3 * kTimelineSlots * sizeof(unsigned long long)));
+    timeline_reset();
+  }
+  drop_graphs();  // captured launches carry (or lack) the stamp buffer
+  timeline_ = on;
+}
+
+int Engine::timeline_read(double* rows, int cap) {
+  if (!tl_buf_) return 0;
+  SIGE_CUDA(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(3 * kTimelineSlots);
+  SIGE_CUDA(cudaMemcpy(h.data(), tl_buf_, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  int n = 0;
+  unsigned long long t0 = ~0ull;
+  for (size_t i = 0; i < tl_meta_.size(); ++i)
+    if (h[2 * i + 1]) t0 = std::min(t0, h[2 * i]);
+  for (size_t i = 0; i < tl_meta_.size(); ++i) {
+    const TlMeta& m = tl_meta_[i];
+    if (!h[2 * i + 1]) continue;  // not launched (or no CTA ran)
+    int32_t cnt = m.count;
+    if (m.count_dev) SIGE_CUDA(cudaMemcpy(&cnt, m.count_dev, sizeof cnt, cudaMemcpyDeviceToHost));
+    if (n < cap && rows) {
+      double* r = rows + 5 * n;
+      r[0] = static_cast<double>(h[2 * i] - t0);
+      r[1] = static_cast<double>(h[2 * i + 1] - t0);
+      const unsigned long long w = h[2 * kTimelineSlots + i];
+      r[2] = w == ~0ull ? r[0] : static_cast<double>(w - t0);
+      r[3] = m.flops_per_tile * cnt;
+      r[4] = m.sparse;
+    }
+    ++n;
+  }
+  timeline_reset();
+  return n;
+}
 
 int Engine::profile_read(double* rows, int cap, cudaStream_t st) {
   SIGE_CUDA(cudaStreamSynchronize(st));
@@ -639,6 +707,8 @@ void Engine::precompute(const float* original, int step, cudaStream_t st) {
 }
 
 void Engine::dense_forward(const float* input, bool reused, int step, float* out, cudaStream_t st) {
+  tl_next_ = 0;
+  tl_meta_.clear();
   dense_walk(input_src(input, st, true), step, false, reused, out, st);
 }
 
@@ -1195,6 +1265,8 @@ void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige
 // every compiled step, then the restore of the tiles this call dirtied.
 void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
                          const sige_run_config& cfg, cudaStream_t st) {
+  tl_next_ = 0;
+  tl_meta_.clear();
   static const bool no_fork = std::getenv("SIGE_NO_FORK") != nullptr;  // A/B switch
   const bool fork = in_twin_ && !no_fork;
   if (fork) {

@@ -82,6 +82,11 @@ class Engine {
   size_t cache_bytes() const;
   void set_profiling(bool on);
   void set_graphs(bool on);
+  // Graph timeline of the conv launches (device stamps inside replayed
+  // graphs): on/off, and read rows [start_ns, end_ns, wait_ns, flops, sparse]
+  // (times relative to the first launch's start) of the last call, then reset.
+  void set_timeline(bool on);
+  int timeline_read(double* rows, int cap);
   void set_sm_budget(int sms);
   int profile_read(double* rows, int cap, cudaStream_t st);
   std::string cache_entries(int step) const;
@@ -171,6 +176,21 @@ class Engine {
   };
   bool profiling_ = false;
   mutable std::vector<ProfRec> prof_;
+  // Graph timeline (set_timeline): every tensor-core conv launch of a call
+  // stamps [start, end, dependency-wait exit] with %globaltimer into tl_buf_,
+  // indexed by launch order within the call; valid inside replayed graphs.
+  struct TlMeta {
+    const int32_t* count_dev;
+    int count;
+    double flops_per_tile;
+    int sparse;
+  };
+  bool timeline_ = false;
+  unsigned long long* tl_buf_ = nullptr;
+  mutable int tl_next_ = 0;
+  mutable std::vector<TlMeta> tl_meta_;
+  void timeline_reset();
+  void drop_graphs();
   mutable std::vector<cudaEvent_t> ev_pool_;
   // per-call bindings read by program steps
   const float* cur_in_ = nullptr;

@@ -131,8 +131,15 @@ void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, cons
                        int math, cudaStream_t st);
 // Same contract on tcgen05 tensor cores (kind::tf32, fp32 TMEM accumulators).
 // conv_tc.cu.
+// gtl (optional): device stamp buffer of the engine's graph timeline — this
+// launch records [first CTA start, last CTA end] at gtl[2 idx], gtl[2 idx + 1]
+// and its first dependency-wait exit at gtl[2 kTimelineSlots + idx] (globaltimer).
+constexpr int kTimelineSlots = 1024;
+// pad >= 0 overrides the conv padding (k - 1) / 2 (op-level conv_on_blocks:
+// the gathered window already carries the halo, kernels.cpp:391-421).
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st, int sm_budget = 0);
+                    cudaStream_t st, int sm_budget = 0, unsigned long long* gtl = nullptr, int gtl_idx = 0,
+                    int pad = -1);
 // Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
 // k_pad and the TMA descriptors of `cw`).
 // Developer instrumentation (SIGE_TC_GTL=1): per-launch conv spans, read + reset.

@@ -165,17 +165,19 @@ def test_graph_replay_follows_threshold(orc):
         out = torch.empty(eng.output_shape(), device="cuda")
         res = []
         for thr in (1e-3, 1e-3, 0.3, 1e-3, 0.3, 0.3, 10.0):
-            eng.sparse_forward(x, config=sb.default_config(dilate_full=25, mask_threshold=thr), out=out)
+            eng.sparse_forward(x, config=sb.default_config(dilate_full=1, min_sparse_res=1, mask_threshold=thr), out=out)
             res.append(out.cpu().numpy().copy())
         outs[graphs] = res
     for a, b in zip(outs[False], outs[True]):
         assert np.array_equal(a, b)
+    m_lo, m_hi = orc.difference_mask(orig, edited, 1e-3), orc.difference_mask(orig, edited, 0.3)
+    assert m_hi.sum() < m_lo.sum()
     assert not np.array_equal(outs[True][0], outs[True][2])  # 0.3 drops part of the edit
     om = orc.model("mini_unet_gn")
     ocache = om.precompute(orig)
     for i, thr in ((2, 0.3), (6, 10.0)):
         want, _ = om.sparse_forward(ocache, edited, orc.difference_mask(orig, edited, thr),
-                                    sb.default_config(dilate_full=25))
+                                    sb.default_config(dilate_full=1, min_sparse_res=1))
         assert np.array_equal(outs[True][i], want)
 
 
@@ -209,3 +211,26 @@ def test_engine_rejects_bad_buffers(orc):
     got = eng.sparse_forward_host(torch.from_numpy(edited), m, config=sb.default_config(dilate_full=25))
     want = eng.sparse_forward(x, m.cuda(), config=sb.default_config(dilate_full=25)).cpu()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("math", [sb.MATH_EXACT, sb.MATH_F16])
+def test_fusion_toggles_do_not_change_the_output(orc, math):
+    """RunConfig.elem_fusion / scatter_fusion (graph.cpp:571-582) select the
+    reference's ablation schedule, whose output is identical by the reference's
+    own tests (test_graph.cpp:215-250, 'fusion toggles do not change the output
+    at all'); the device executor always runs the fused schedule, so every
+    toggle combination gives the same bits (and, exact mode, the oracle's)."""
+    om = orc.model("mini_unet_gn")
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 19)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=math)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    x = torch.from_numpy(edited).cuda()
+    outs = []
+    for bits in range(4):
+        cfg = sb.default_config(dilate_full=om.required_dilation(), elem_fusion=bits & 1, scatter_fusion=(bits >> 1) & 1)
+        outs.append(eng.sparse_forward(x, config=cfg).cpu().numpy())
+        if math == sb.MATH_EXACT:
+            want, _ = om.sparse_forward(om.precompute(orig), edited, orc.difference_mask(orig, edited), cfg)
+            assert np.array_equal(outs[-1], want)
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))

@@ -320,3 +320,44 @@ def test_gather_scatter_long_runs_chunk_and_slice_edges(orc, b):
     tb = cu(base)
     sb.scatter_add_inplace(cu(blocks), cu(idx), tb)
     assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
+
+
+@pytest.mark.parametrize("math", [sb.MATH_TF32, sb.MATH_F16], ids=["tf32", "f16"])
+def test_conv_tensor_core_op_level(orc, math):
+    """conv_on_blocks / conv2d (kernels.cpp:391-421, conv.cpp:83-102) on the
+    tcgen05 path: integer data is exact in any summation order (bit-exact vs the
+    oracle), real data within the north-star 1e-2 normalised max error."""
+    rng = np.random.default_rng(151)
+    for k, s, cin, cout, b, hw in [(3, 1, 64, 96, 6, 20), (1, 1, 128, 64, 4, 16), (3, 2, 32, 40, 6, 26),
+                                  (3, 1, 3, 16, 6, 14)]:
+        oh = (hw + 2 * ((k - 1) // 2) - k) // s + 1
+        for integer in (True, False):
+            if integer:
+                x = rng.integers(-2, 3, (2, cin, hw, hw)).astype(np.float32)
+                wt = rng.integers(-2, 3, (cout, cin, k, k)).astype(np.float32)
+                bias = rng.integers(-3, 4, cout).astype(np.float32)
+            else:
+                x = rng.uniform(-1, 1, (2, cin, hw, hw)).astype(np.float32)
+                wt = rng.uniform(-0.2, 0.2, (cout, cin, k, k)).astype(np.float32)
+                bias = rng.uniform(-0.1, 0.1, cout).astype(np.float32)
+            m = (rng.random((oh, oh)) < 0.3).astype(np.uint8)
+            idx, _ = orc.mask_to_block_indices(m, b, 2)
+            g = orc.gather(x, idx, b, oh, oh, k, s)
+            want_b = orc.conv_on_blocks(g, wt, bias, k, s, b)
+            want_d = orc.conv2d(x, wt, bias, k, s)
+            got_b = host(sb.conv_on_blocks(cu(g), cu(wt), cu(bias), s, b, math=math))
+            got_d = host(sb.conv2d(cu(x), cu(wt), cu(bias), s, math=math))
+            if integer:
+                assert bits_equal(got_b, want_b) and bits_equal(got_d, want_d), (k, s, cin, cout)
+            else:
+                for got, want in ((got_b, want_b), (got_d, want_d)):
+                    assert np.abs(got - want).max() <= 1e-2 * np.abs(want).max(), (k, s, cin, cout)
+
+
+def test_conv_rejects_unknown_math_mode():
+    g = cu(np.zeros((1, 2, 8, 8), np.float32))
+    w = cu(np.zeros((2, 2, 3, 3), np.float32))
+    with pytest.raises(sb.ConfigError, match="conv_on_blocks: unknown math mode 7"):
+        sb.conv_on_blocks(g, w, None, 1, 6, math=7)
+    with pytest.raises(sb.ConfigError, match="conv2d: unknown math mode -1"):
+        sb.conv2d(g, w, None, math=-1)
