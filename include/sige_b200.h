@@ -208,6 +208,21 @@ int sige_scatter_add_inplace(const float* blocks, int count, int channels, int b
 int sige_build_scatter_map(const int32_t* idx, int count, int block, int h, int w,
                            sige_scatter_entry* map_out, int* blocks_per_sample_host,
                            sige_stream_t stream);
+/* BlockIndexSet::content_hash (mask.cpp:91-101) of a device index set
+ * (fnv1a64 over block, h, w, then every {n, r, c}); synchronises the stream. */
+int sige_block_index_hash(const int32_t* idx, int count, int block, int h, int w, uint64_t* hash_out,
+                          sige_stream_t stream);
+/* ScatterMapCache::instance().get/size/clear (kernels.hpp:80-91,
+ * kernels.cpp:171-202): a process-wide, mutex-protected memo of DEVICE scatter
+ * maps keyed by the index set's content hash. get() builds the map on a miss
+ * and returns the cache-owned map (h x w entries), blocks-per-sample and the
+ * key; the map stays valid until sige_scatter_map_cache_clear(), which waits
+ * for the device before freeing. */
+int sige_scatter_map_cache_get(const int32_t* idx, int count, int block, int h, int w,
+                               const sige_scatter_entry** map_out, int* blocks_per_sample,
+                               uint64_t* key_out, sige_stream_t stream);
+size_t sige_scatter_map_cache_size(void);
+void sige_scatter_map_cache_clear(void);
 /* scatter_gather (kernels.hpp:98-100, kernels.cpp:204-275). */
 int sige_scatter_gather(const float* blocks, int count, int block, const float* original_out,
                         int n, int c, int h, int w, const sige_scatter_entry* map,

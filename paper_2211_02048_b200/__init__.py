@@ -35,7 +35,7 @@ __all__ = [
     "gather", "scatter", "scatter_inplace", "scatter_add_inplace", "build_scatter_map",
     "scatter_gather", "scatter_with_block_residual", "scatter_with_block_residual_unfused",
     "add_blocks", "subtract_blocks", "apply_epilogue_on_blocks", "conv_on_blocks", "conv2d",
-    "make_edit_fixture", "kernel_launch_count",
+    "make_edit_fixture", "kernel_launch_count", "ScatterMapCache", "block_index_hash",
 ]
 
 
@@ -234,6 +234,54 @@ def build_scatter_map(idx: torch.Tensor, block_size: int, h: int, w: int):
     bps = C.c_int(0)
     _check(_lib().sige_build_scatter_map(i.data_ptr(), i.shape[0], block_size, h, w, m.data_ptr(), C.byref(bps), _stream()))
     return m, bps.value
+
+
+def block_index_hash(idx: torch.Tensor, block_size: int, h: int, w: int) -> int:
+    """BlockIndexSet::content_hash (mask.cpp:91-101) of a device index set."""
+    i = _dev(idx, torch.int32, "content_hash")
+    out = C.c_uint64(0)
+    _check(_lib().sige_block_index_hash(i.data_ptr(), i.shape[0], block_size, h, w, C.byref(out), _stream()))
+    return out.value
+
+
+class DeviceScatterMap:
+    """A cache-owned device scatter map (valid until ScatterMapCache.clear());
+    unpacks like build_scatter_map's (map, blocks_per_sample)."""
+
+    def __init__(self, ptr: int, bps: int, key: int, h: int, w: int):
+        self.ptr, self.bps, self.key, self.h, self.w = ptr, bps, key, h, w
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def __iter__(self):
+        return iter((self, self.bps))
+
+
+class ScatterMapCache:
+    """ScatterMapCache (kernels.hpp:80-91): process-wide memo of device scatter
+    maps keyed by the index set's content hash."""
+
+    _inst = None
+
+    @classmethod
+    def instance(cls) -> "ScatterMapCache":
+        if cls._inst is None:
+            cls._inst = cls()
+        return cls._inst
+
+    def get(self, idx: torch.Tensor, block_size: int, h: int, w: int) -> DeviceScatterMap:
+        i = _dev(idx, torch.int32, "ScatterMapCache::get")
+        p, bps, key = C.c_void_p(), C.c_int(0), C.c_uint64(0)
+        _check(_lib().sige_scatter_map_cache_get(i.data_ptr(), i.shape[0], block_size, h, w, C.byref(p),
+                                                 C.byref(bps), C.byref(key), _stream()))
+        return DeviceScatterMap(p.value, bps.value, key.value, h, w)
+
+    def size(self) -> int:
+        return int(_lib().sige_scatter_map_cache_size())
+
+    def clear(self) -> None:
+        _lib().sige_scatter_map_cache_clear()
 
 
 def scatter_gather(blocks: torch.Tensor, original_out: torch.Tensor, scatter_map, consumer_idx: torch.Tensor,

@@ -191,6 +191,10 @@ SYMBOLS = {
     "sige_engine_set_sm_budget": (_i, [_vp, _i]),
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_set_timeline": (_i, [_vp, _i]),
+    "sige_block_index_hash": (_i, [_vp, _i, _i, _i, _i, C.POINTER(_u64), _vp]),
+    "sige_scatter_map_cache_get": (_i, [_vp, _i, _i, _i, _i, C.POINTER(_vp), C.POINTER(_i), C.POINTER(_u64), _vp]),
+    "sige_scatter_map_cache_size": (_sz, []),
+    "sige_scatter_map_cache_clear": (None, []),
     "sige_engine_timeline_read": (_i, [_vp, _vp, _i, C.POINTER(_i)]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),

@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -91,6 +93,7 @@ uint64_t sige_kernel_launch_count(void) { return g_launches.load(); }
 // Developer instrumentation, not part of the reference-facing ABI: per-launch
 // [start, end] globaltimer of k_conv_tc launches when SIGE_TC_GTL=1.
 int sige_debug_conv_timeline(unsigned long long* out, int cap) { return sige_b200::debug_conv_timeline(out, cap); }
+int sige_debug_conv_marks(unsigned long long* out, int cap) { return sige_b200::debug_conv_marks(out, cap); }
 // Device glibc expf (mode 0) / exact SiLU (mode 1) of the float bit patterns
 // first .. first+count-1, with the libm build the host dispatches to.
 int sige_debug_expf_sweep(uint32_t first, long long count, int mode, float* out, sige_stream_t s) {
@@ -227,6 +230,78 @@ int sige_build_scatter_map(const int32_t* idx, int count, int block, int h, int 
     DevBuf<int> scratch(2);
     *bps = op_build_scatter_map(idx, count, block, h, w, map_out, scratch.p, as_stream(s));
   });
+}
+
+namespace {
+// BlockIndexSet::content_hash (mask.cpp:91-101) of a device index set.
+uint64_t index_set_hash(const int32_t* idx, int count, int block, int h, int w, cudaStream_t st) {
+  std::vector<int32_t> host(static_cast<size_t>(count) * 3);
+  if (count) {
+    SIGE_CUDA(cudaMemcpyAsync(host.data(), idx, host.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SIGE_CUDA(cudaStreamSynchronize(st));
+  }
+  uint64_t hs = fnv1a64(&block, sizeof(block));
+  hs = fnv1a64(&h, sizeof(h), hs);
+  hs = fnv1a64(&w, sizeof(w), hs);
+  for (int i = 0; i < count; ++i)
+    for (int j = 0; j < 3; ++j) hs = fnv1a64(&host[3 * i + j], sizeof(int32_t), hs);
+  return hs;
+}
+
+// ScatterMapCache (kernels.hpp:80-91, kernels.cpp:171-202) on the device: one
+// scatter map per index-set content hash, built once and kept until clear().
+struct MapEntry {
+  sige_scatter_entry* map = nullptr;
+  int bps = 0;
+};
+std::mutex g_map_mu;
+std::unordered_map<uint64_t, MapEntry> g_maps;
+}  // namespace
+
+int sige_block_index_hash(const int32_t* idx, int count, int block, int h, int w, uint64_t* out, sige_stream_t s) {
+  return guarded([&] {
+    need(out, "content_hash");
+    *out = index_set_hash(idx, count, block, h, w, as_stream(s));
+  });
+}
+
+int sige_scatter_map_cache_get(const int32_t* idx, int count, int block, int h, int w,
+                               const sige_scatter_entry** map_out, int* bps, uint64_t* key_out, sige_stream_t s) {
+  return guarded([&] {
+    need(map_out, "ScatterMapCache::get");
+    need(bps, "ScatterMapCache::get");
+    cudaStream_t st = as_stream(s);
+    const uint64_t key = index_set_hash(idx, count, block, h, w, st);
+    if (key_out) *key_out = key;
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it == g_maps.end()) {
+      MapEntry e;
+      SIGE_CUDA(cudaMalloc(&e.map, std::max<size_t>(static_cast<size_t>(h) * w, 1) * sizeof(sige_scatter_entry)));
+      try {
+        DevBuf<int> scratch(2);
+        e.bps = op_build_scatter_map(idx, count, block, h, w, e.map, scratch.p, st);
+      } catch (...) {
+        cudaFree(e.map);
+        throw;
+      }
+      it = g_maps.emplace(key, e).first;
+    }
+    *map_out = it->second.map;
+    *bps = it->second.bps;
+  });
+}
+
+size_t sige_scatter_map_cache_size(void) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  return g_maps.size();
+}
+
+void sige_scatter_map_cache_clear(void) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  cudaDeviceSynchronize();  // maps may still be read by queued scatter_gather launches
+  for (auto& kv : g_maps) cudaFree(kv.second.map);
+  g_maps.clear();
 }
 
 int sige_scatter_gather(const float* blocks, int count, int block, const float* original_out, int n,

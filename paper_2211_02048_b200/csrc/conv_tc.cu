@@ -121,6 +121,9 @@ struct TcParams {
   int warm;                // epilogue warm-up pass (SIGE_NO_WARM=1 disables)
   unsigned long long* gtl;  // SIGE_TC_GTL: per-launch [first CTA start, last CTA end] (graph-safe)
   int gtl_idx;
+  const char* pf_ptr;       // next conv's packed weights (L2 prefetch), or nullptr
+  long long pf_bytes;
+  unsigned long long* gtl_marks;  // SIGE_TC_GTL: CTA 0's phase marks per launch (64 slots), or nullptr
 };
 
 // ------------------------------------------------------------- PTX ------
@@ -129,6 +132,10 @@ __device__ __forceinline__ void tl_mark(const TcParams& p, int idx) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.tl[blockIdx.x * 64 + idx] = t;
+  } else if (p.gtl_marks && blockIdx.x == 0) {  // graph-safe phase marks of CTA 0 (SIGE_TC_GTL)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.gtl_marks[p.gtl_idx * 64 + idx] = t;
   }
 }
 __device__ __forceinline__ void tl_cta(const TcParams& p, int base) {
@@ -1004,6 +1011,18 @@ __device__ __forceinline__ int nt_index(int nt) {
   return nt <= 16 ? 0 : nt <= 32 ? 1 : nt <= 64 ? 2 : nt <= 128 ? 3 : 4;
 }
 
+// This CTA's slice of the next conv's packed weights into L2 (one elected
+// thread; the next layer's weight TMA then streams from L2).
+__device__ __forceinline__ void prefetch_next_weights(const TcParams& p) {
+  if (!p.pf_ptr) return;
+  const long long per = ((p.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15LL;
+  const long long lo = per * blockIdx.x, hi = min(p.pf_bytes, lo + per);
+  for (long long o = lo; o < hi; o += 32768)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_ptr + o),
+                 "r"(static_cast<uint32_t>(min(32768LL, hi - o)))
+                 : "memory");
+}
+
 // MMA-issue state shared by the unrolled chunk bodies (uniform across the warp).
 struct MmaCtx {
   uint32_t a0, b0, kstep16, row16, tap_b16, plane16, bstage16, P, nb, idesc, tmem_d;
@@ -1466,6 +1485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (valid || dry) out16(p, pix, n, y, x, oc, v, wv, ops, dry);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid || dry, wv, dry);
           if (dry) break;
+          if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 40 + min(cb >> 4, 3));
           if (more) {
             tmem_wait_regs(rnext);
 #pragma unroll
@@ -1680,6 +1700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
       uint32_t b_iter = 0, bslot = 0, bphase = 0;
       const uint32_t b0 = smem_u32(bbuf);
+      if (cid >= n_items) prefetch_next_weights(p);  // no items of its own
       const uint32_t stage_bytes = b_stage;
       for (int item = cid; item < n_items; item += ncl) {
         const int ni = item - static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices) * n_slices;
@@ -1693,7 +1714,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mbar_expect_tx(&bar_bfull[st], stage_bytes);
             tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, ch * p.ntaps + tg * tps, &bar_bfull[st]);
-            if (b_iter == 0) tl_mark(p, 10);
+            if (b_iter == 0) {
+              tl_mark(p, 10);
+              if (item == cid) prefetch_next_weights(p);  // behind this CTA's own first stage
+            }
           }
         if (item == cid) tl_mark(p, 11);
       }
@@ -1815,12 +1839,22 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 constexpr int kGtlLaunches = 1024;
 static const bool g_gtl_on = std::getenv("SIGE_TC_GTL") != nullptr;
 static unsigned long long* g_gtl_buf = nullptr;  // allocated at the first instrumented launch
+static unsigned long long* g_gtl_marks = nullptr;  // [launch][64] phase marks of CTA 0
 static void gtl_reset() {
   std::vector<unsigned long long> init(3 * kGtlLaunches, ~0ull);  // [start, end] pairs, then wait-done
   for (int i = 0; i < kGtlLaunches; ++i) init[2 * i + 1] = 0;
   SIGE_CUDA(cudaMemcpy(g_gtl_buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+  SIGE_CUDA(cudaMemset(g_gtl_marks, 0, 64 * kGtlLaunches * 8));
 }
 static int g_gtl_next = 0;
+
+int debug_conv_marks(unsigned long long* out, int cap) {
+  if (!g_gtl_marks) return 0;
+  SIGE_CUDA(cudaDeviceSynchronize());
+  const int n = std::min(cap, kGtlLaunches);
+  SIGE_CUDA(cudaMemcpy(out, g_gtl_marks, static_cast<size_t>(n) * 64 * 8, cudaMemcpyDeviceToHost));
+  return n;
+}
 
 int debug_conv_timeline(unsigned long long* out, int cap) {
   if (!g_gtl_buf) return 0;
@@ -1855,6 +1889,7 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
   after_launch("k_pack_tc");
   SIGE_CUDA(cudaStreamSynchronize(st));
   cw->w_tc = out;
+  cw->w_tc_bytes = total * esize;
   // One 3-D tensor map per N-slice width: dims (128-byte K row, n, (chunk, tap)),
   // box (row, n_tile, taps_per_stage), 128-byte swizzle — a ring stage is one
   // TMA of whole 128-byte rows (the MMA reads it through SWIZZLE_128B descriptors).
@@ -1878,7 +1913,8 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
 }
 
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad) {
+                    cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad,
+                    const void* pf_ptr, size_t pf_bytes) {
   static_assert(kGtlLaunchesDev == kTimelineSlots, "timeline layout");
   const int sms_all = sm_count();
   const int sms_use = sm_budget > 0 ? std::min(sm_budget, sms_all) : sms_all;
@@ -1913,6 +1949,12 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   p.k = cw.k;
   p.s = cw.stride;
   p.pad = pad >= 0 ? pad : (cw.k - 1) / 2;
+  // Opt-in (SIGE_L2_PREFETCH=1): measured 2.5 % slower per edit on config 2
+  // (profiles/r2_l2_prefetch_ab.txt) — the next layer's own weight TMA is
+  // already issued in its PDL prologue, before the dependency wait.
+  static const bool pf_on = std::getenv("SIGE_L2_PREFETCH") != nullptr;
+  p.pf_ptr = pf_on ? static_cast<const char*>(pf_ptr) : nullptr;
+  p.pf_bytes = pf_on ? static_cast<long long>(pf_bytes) & ~15LL : 0;
   p.n_pad = cw.n_pad;
   p.nchunks = cw.k_pad / (f16 ? 64 : 32);
   p.ntaps = cw.k * cw.k;
@@ -2223,9 +2265,11 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
   } else if (g_gtl_on) {
     if (!g_gtl_buf) {
       SIGE_CUDA(cudaMalloc(&g_gtl_buf, 3 * kGtlLaunches * 8));
+      SIGE_CUDA(cudaMalloc(&g_gtl_marks, 64 * kGtlLaunches * 8));
       gtl_reset();
     }
     p.gtl = g_gtl_buf;
+    p.gtl_marks = g_gtl_marks;
     p.gtl_idx = g_gtl_next++ % kGtlLaunches;
     std::fprintf(stderr, "[gtl %d] %dx%d c%d->%d k%d s%d count %d T%d Mt%d nt %d ks %d tma %d xform %d up %d\n",
                  p.gtl_idx, tiles.bh, tiles.bw, cw.c_in, cw.c_out, cw.k, cw.stride, tiles.count, p.T, p.Mt,

@@ -89,6 +89,7 @@ struct Program {
   RestoreJob* restores_dev = nullptr;
   long long restore_max = 0;
   std::vector<TraceInfo> trace;
+  std::vector<WRef> wseq;  // packed weights of the tensor-core convs in launch order
   uint32_t* bits = nullptr;
   int32_t* any = nullptr;
   int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
@@ -420,6 +421,16 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     }
     SIGE_CUDA(cudaEventRecord(rec.a, st));
   }
+  const void* pf = nullptr;
+  size_t pf_bytes = 0;
+  if (tensor_cores() && seq_) {
+    const size_t i = seq_next_++;
+    if (seq_->size() == i) seq_->push_back({cw.w_tc, cw.w_tc_bytes});  // first run records the chain
+    if (i + 1 < seq_->size()) {
+      pf = (*seq_)[i + 1].p;
+      pf_bytes = (*seq_)[i + 1].bytes;
+    }
+  }
   if (tensor_cores() && timeline_) {
     const int idx = tl_next_++;
     if (idx < kTimelineSlots) {
@@ -434,9 +445,10 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
       m.sparse = t.count_dev ? 1 : 0;
       tl_meta_.push_back(m);
     }
-    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, tl_buf_, idx);
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, tl_buf_, idx, -1, pf,
+                   pf_bytes);
   } else if (tensor_cores())
-    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_);
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, nullptr, 0, -1, pf, pf_bytes);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
   if (profiling_) {
@@ -1267,6 +1279,12 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
                          const sige_run_config& cfg, cudaStream_t st) {
   tl_next_ = 0;
   tl_meta_.clear();
+  seq_ = &P.wseq;
+  seq_next_ = 0;
+  struct SeqReset {  // the sequence belongs to this call only
+    Engine* e;
+    ~SeqReset() { e->seq_ = nullptr; }
+  } seq_reset{this};
   static const bool no_fork = std::getenv("SIGE_NO_FORK") != nullptr;  // A/B switch
   const bool fork = in_twin_ && !no_fork;
   if (fork) {

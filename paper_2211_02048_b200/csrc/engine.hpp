@@ -60,6 +60,12 @@ struct TraceInfo {
 
 struct Program;
 
+// A packed weight tensor (L2 prefetch target).
+struct WRef {
+  const void* p;
+  size_t bytes;
+};
+
 class Engine {
  public:
   Engine(const sige_model_desc* model, int batch, int math);
@@ -185,6 +191,11 @@ class Engine {
     double flops_per_tile;
     int sparse;
   };
+  // Weight L2 prefetch along the launch chain: the packed weights of every
+  // tensor-core conv in call order (recorded by the first run of a program),
+  // so conv i prefetches conv i+1's weights while it runs.
+  std::vector<WRef>* seq_ = nullptr;  // the running call's sequence (nullptr: none)
+  mutable size_t seq_next_ = 0;
   bool timeline_ = false;
   unsigned long long* tl_buf_ = nullptr;
   mutable int tl_next_ = 0;

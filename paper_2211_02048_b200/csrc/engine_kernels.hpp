@@ -120,6 +120,7 @@ struct ConvW {
   const float* w = nullptr;     // (c_out, c_in, k, k) reference layout
   const float* bias = nullptr;  // c_out or nullptr
   const void* w_tc = nullptr;   // tcgen05 packing [chunk][tap][n_pad][128 B K row] (conv_tc.cu)
+  size_t w_tc_bytes = 0;        // bytes of the packing
   int n_pad = 0;                // c_out rounded up for the tensor-core N dimension
   int k_pad = 0;                // channels rounded up per tap for the K dimension
   TcMaps maps{};
@@ -139,11 +140,17 @@ constexpr int kTimelineSlots = 1024;
 // the gathered window already carries the halo, kernels.cpp:391-421).
 void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
                     cudaStream_t st, int sm_budget = 0, unsigned long long* gtl = nullptr, int gtl_idx = 0,
-                    int pad = -1);
+                    int pad = -1, const void* pf_ptr = nullptr, size_t pf_bytes = 0);
+// pf_ptr / pf_bytes: the packed weights of the NEXT conv of the launch chain;
+// the launch's CTAs prefetch them into L2 (cp.async.bulk.prefetch.L2, one
+// slice per CTA) while this layer runs, so the next layer's weight stream
+// starts from L2 instead of HBM.
 // Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
 // k_pad and the TMA descriptors of `cw`).
 // Developer instrumentation (SIGE_TC_GTL=1): per-launch conv spans, read + reset.
 int debug_conv_timeline(unsigned long long* out, int cap);
+// CTA 0's phase marks (64 globaltimer slots per launch, 0 = not reached).
+int debug_conv_marks(unsigned long long* out, int cap);
 void pack_weights_tc(const float* w_dev_ref, int c_out, int c_in, int k, int f16, ConvW* cw,
                      cudaStream_t st);
 

@@ -155,7 +155,10 @@ def test_graph_replay_follows_threshold(orc):
     thresholds on the same buffers with graphs on must give the same bits as
     direct launches (compute_difference_mask's strict '>' at each threshold,
     mask.cpp:14-32)."""
-    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 41)
+    orig, _ = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 41)
+    edited = orig.copy()
+    edited[:, :, 5:11, 5:11] += 0.1  # below the 0.3 threshold
+    edited[:, :, 40:46, 30:36] -= 1.0  # above it
     outs = {}
     for graphs in (False, True):
         eng = sb.Engine(sb.Model("mini_unet_gn"), math=sb.MATH_EXACT)

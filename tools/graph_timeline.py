@@ -16,6 +16,8 @@ from paper_2211_02048_b200 import _capi  # noqa: E402
 lib = sb._lib()
 lib.sige_debug_conv_timeline.restype = C.c_int
 lib.sige_debug_conv_timeline.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+lib.sige_debug_conv_marks.restype = C.c_int
+lib.sige_debug_conv_marks.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 
 m = sb.Model("ddim_stack")
 c, h, w = m.in_shape
@@ -37,6 +39,8 @@ a.record()
 eng.sparse_forward(ed, config=cfg, out=out)
 b.record()
 torch.cuda.synchronize()
+marks = (C.c_ulonglong * (64 * 1024))()
+lib.sige_debug_conv_marks(marks, 1024)
 n = lib.sige_debug_conv_timeline(buf, 1024)
 rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2], i) for i in range(n) if buf[3 * i + 1]]
 t0 = rows[0][0]
@@ -52,5 +56,26 @@ for i, (s, en, wd, gi) in enumerate(rows):
     print(f"{i:3d} {(s - t0) / 1e3:9.2f} {(wd - t0) / 1e3:9.2f} {(en - t0) / 1e3:9.2f} {work:8.2f} {hand:8.2f}"
           f"  [gtl {gi}]")
     prev_end = en
+print()
+print("CTA 0 phases (us): wait->A landed (22-49), MMAs (9-22), acc ready (5-9), epilogue (47-5), "
+      "teardown (13-47); reduce-scatter (52-53) when split")
+
+
+def mk(gi, k):
+    v = marks[gi * 64 + k]
+    return v if v else None
+
+
+acc = {}
+for i, (s_, en, wd, gi) in enumerate(rows):
+    m = {k: mk(gi, k) for k in (49, 22, 9, 5, 47, 13, 52, 53)}
+    def d(a, b):
+        return (m[a] - m[b]) / 1e3 if m[a] and m[b] else float("nan")
+    ph = [d(22, 49), d(9, 22), d(5, 9), d(47, 5), d(13, 47), d(52, 53)]
+    print(f"{i:3d} " + " ".join(f"{v:6.2f}" for v in ph) + f"  [gtl {gi}]")
+    for j, v in enumerate(ph):
+        if v == v:
+            acc[j] = acc.get(j, 0.0) + v
+print("sums " + " ".join(f"{acc.get(j, 0.0):7.1f}" for j in range(6)))
 print(f"sum work {tot_work:.1f} us, sum handoff (incl. non-conv kernels) {tot_hand:.1f} us, "
       f"first->last {(rows[-1][1] - t0) / 1e3:.1f} us")
