@@ -271,6 +271,20 @@ void sige_engine_destroy(sige_engine* eng);
  * pass over `original` (device NCHW) that fills the cache for `step`. */
 int sige_engine_precompute(sige_engine* eng, const float* original, int step,
                            sige_stream_t stream);
+/* ActivationCache lifecycle (graph.hpp:116-176). drop_step erases one step's
+ * entries and frees their device memory (ActivationCache::drop_step,
+ * graph.cpp:271-274); refresh_step replaces a step from a new original
+ * (graph.cpp:437-444). The cache carries the structure hash of the model it
+ * was built for (precompute sets the engine's own; a cache imported with
+ * put_tensor/put_norm declares its producer's with set_cache_model_hash), and
+ * sparse_forward fails with the reference's check_cache_model ConfigError
+ * when it differs from the engine model's (graph.cpp:596-603). */
+int sige_engine_drop_step(sige_engine* eng, int step);
+int sige_engine_refresh_step(sige_engine* eng, const float* original, int step, sige_stream_t stream);
+int sige_engine_cache_model_hash(const sige_engine* eng, uint64_t* cache_hash, uint64_t* model_hash);
+int sige_engine_set_cache_model_hash(sige_engine* eng, uint64_t cache_hash);
+/* ModelSpec::structure_hash (graph.cpp:89-127). */
+uint64_t sige_model_structure_hash(const sige_model_desc* model);
 /* Upload one cache entry (host NCHW tensor or n*C folded norm) from a CPU
  * precompute, for parity runs. key follows graph.cpp:356-410 ("L3.conv1.out",
  * "L0.norm", "final", ...). For norms pass scale and shift (n*C each). */
@@ -290,6 +304,16 @@ int sige_engine_get_norm(sige_engine* eng, int step, const char* key, float* hos
  * out is device NCHW of the model output shape. No host synchronisation. */
 int sige_engine_sparse_forward(sige_engine* eng, const float* edited, const uint8_t* mask,
                                const sige_run_config* cfg, float* out, sige_stream_t stream);
+/* Grouped independent requests (config 5; no reference counterpart — the
+ * reference runs one request per call, graph.hpp:224-226): every batch sample
+ * of the engine is its own request, with its own original (precompute), edited
+ * input and difference mask (`masks`: batch x H x W u8, or NULL to compute
+ * each sample's mask against its cached original with cfg->mask_threshold).
+ * Per-sample IndexPlans are concatenated n-major into each layer's tile list,
+ * so one launch per layer serves all requests; sample n's output equals a
+ * batch-1 sparse_forward of request n (empty mask -> its cached final). */
+int sige_engine_sparse_forward_grouped(sige_engine* eng, const float* edited, const uint8_t* masks,
+                                       const sige_run_config* cfg, float* out, sige_stream_t stream);
 /* Same through HOST buffers: H2D of edited (and mask when non-NULL), run,
  * D2H of the output, stream synchronised on return. */
 int sige_engine_sparse_forward_host(sige_engine* eng, const float* edited_host,

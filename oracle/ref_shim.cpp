@@ -515,6 +515,7 @@ void* ref_model_from_desc(const sige_model_desc* d) {
 void ref_model_free(void* m) { delete static_cast<ModelSpec*>(m); }
 
 uint64_t ref_model_weight_hash(void* m) { return model_weight_hash(*static_cast<ModelSpec*>(m)); }
+uint64_t ref_model_structure_hash(void* m) { return static_cast<ModelSpec*>(m)->structure_hash(); }
 
 int ref_model_required_dilation(void* m) { return required_dilation(*static_cast<ModelSpec*>(m)); }
 

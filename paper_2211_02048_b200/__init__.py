@@ -483,6 +483,10 @@ class Model:
     def weight_hash(self) -> int:
         return int(_lib().sige_model_weight_hash(self.desc))
 
+    def structure_hash(self) -> int:
+        """ModelSpec::structure_hash (graph.cpp:89-127)."""
+        return int(_lib().sige_model_structure_hash(self.desc))
+
     def required_dilation(self) -> int:
         v = C.c_int(0)
         _check(_lib().sige_model_required_dilation(self.desc, C.byref(v)))
@@ -515,6 +519,25 @@ class Engine:
     def precompute(self, original: torch.Tensor, step: int = 0) -> None:
         o = self._check_input(original, "precompute")
         _check(_lib().sige_engine_precompute(self.h, o.data_ptr(), step, _stream()))
+
+    def drop_step(self, step: int) -> None:
+        """ActivationCache::drop_step (graph.cpp:271-274): erase (and free) one step's entries."""
+        _check(_lib().sige_engine_drop_step(self.h, step))
+
+    def refresh_step(self, original: torch.Tensor, step: int) -> None:
+        """refresh_step (graph.cpp:437-444): replace one step's entries from a new original."""
+        o = self._check_input(original, "precompute")
+        _check(_lib().sige_engine_refresh_step(self.h, o.data_ptr(), step, _stream()))
+
+    def cache_model_hash(self) -> tuple[int, int]:
+        """(hash of the model the cache was built for, hash of the engine's model)."""
+        c, m = C.c_uint64(0), C.c_uint64(0)
+        _check(_lib().sige_engine_cache_model_hash(self.h, C.byref(c), C.byref(m)))
+        return c.value, m.value
+
+    def set_cache_model_hash(self, h: int) -> None:
+        """Declare the producer model of an imported cache (ActivationCache::set_model_hash)."""
+        _check(_lib().sige_engine_set_cache_model_hash(self.h, C.c_uint64(h)))
 
     def put_tensor(self, key: str, host_nchw, step: int = 0) -> None:
         t = torch.as_tensor(host_nchw, dtype=torch.float32).contiguous().cpu()
@@ -595,6 +618,25 @@ class Engine:
         cfg = config or default_config()
         _check(_lib().sige_engine_sparse_forward(self.h, e.data_ptr(), m.data_ptr() if m is not None else None,
                                                  C.byref(cfg), out.data_ptr(), _stream()))
+        return out
+
+    def sparse_forward_grouped(self, edited: torch.Tensor, masks: torch.Tensor | None = None,
+                               config: RunConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Independent requests, one per batch sample (own original, edit and
+        mask; masks: (batch, H, W) uint8 or None), served by one launch per layer."""
+        e = self._check_input(edited, "sparse_forward_grouped")
+        m = None
+        if masks is not None:
+            _, _, h, w = self._in_shape()
+            if (not isinstance(masks, torch.Tensor) or not masks.is_cuda or masks.dtype != torch.uint8
+                    or tuple(masks.shape) != (self.batch, h, w)):
+                raise ConfigError(f"sparse_forward_grouped: masks must be a CUDA uint8 tensor of shape "
+                                  f"{(self.batch, h, w)}")
+            m = masks.contiguous()
+        out = self._check_out(out, e, "sparse_forward_grouped")
+        cfg = config or default_config()
+        _check(_lib().sige_engine_sparse_forward_grouped(self.h, e.data_ptr(), m.data_ptr() if m is not None else None,
+                                                         C.byref(cfg), out.data_ptr(), _stream()))
         return out
 
     def sparse_forward_host(self, edited_host: torch.Tensor, mask_host: torch.Tensor | None = None,

@@ -181,6 +181,7 @@ SYMBOLS = {
     "sige_engine_get_norm": (_i, [_vp, _i, C.c_char_p, _vp, _vp, _sz]),
     "sige_engine_sparse_forward": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, _vp]),
     "sige_engine_sparse_forward_host": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, _vp]),
+    "sige_engine_sparse_forward_grouped": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, _vp]),
     "sige_engine_dense_forward": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sige_engine_output_shape": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "sige_engine_last_launch_count": (_i, [_vp]),
@@ -191,6 +192,11 @@ SYMBOLS = {
     "sige_engine_set_sm_budget": (_i, [_vp, _i]),
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_set_timeline": (_i, [_vp, _i]),
+    "sige_engine_drop_step": (_i, [_vp, _i]),
+    "sige_engine_refresh_step": (_i, [_vp, _vp, _i, _vp]),
+    "sige_engine_cache_model_hash": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
+    "sige_engine_set_cache_model_hash": (_i, [_vp, _u64]),
+    "sige_model_structure_hash": (_u64, [_vp]),
     "sige_block_index_hash": (_i, [_vp, _i, _i, _i, _i, C.POINTER(_u64), _vp]),
     "sige_scatter_map_cache_get": (_i, [_vp, _i, _i, _i, _i, C.POINTER(_vp), C.POINTER(_i), C.POINTER(_u64), _vp]),
     "sige_scatter_map_cache_size": (_sz, []),

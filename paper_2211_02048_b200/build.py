@@ -70,6 +70,12 @@ def build(verbose: bool = False) -> pathlib.Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
+        # a shared library links with unresolved symbols; ours must have none
+        u = subprocess.run(["nm", "-D", "--undefined-only", str(LIB)], capture_output=True, text=True)
+        missing = [ln.split()[-1] for ln in u.stdout.splitlines() if "sige_b200" in ln]
+        if missing:
+            LIB.unlink()
+            raise RuntimeError(f"link left library symbols unresolved: {missing}")
     return LIB
 
 

@@ -532,6 +532,40 @@ int sige_engine_precompute(sige_engine* eng, const float* original, int step, si
   });
 }
 
+int sige_engine_drop_step(sige_engine* eng, int step) {
+  return guarded([&] {
+    need(eng, "engine");
+    eng->impl->drop_step(step);
+  });
+}
+
+int sige_engine_refresh_step(sige_engine* eng, const float* original, int step, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    need(original, "refresh_step");
+    eng->impl->refresh_step(original, step, as_stream(s));
+  });
+}
+
+int sige_engine_cache_model_hash(const sige_engine* eng, uint64_t* cache_hash, uint64_t* model_hash) {
+  return guarded([&] {
+    need(eng, "engine");
+    if (cache_hash) *cache_hash = eng->impl->cache_model_hash();
+    if (model_hash) *model_hash = eng->impl->structure_hash();
+  });
+}
+
+int sige_engine_set_cache_model_hash(sige_engine* eng, uint64_t cache_hash) {
+  return guarded([&] {
+    need(eng, "engine");
+    eng->impl->set_cache_model_hash(cache_hash);
+  });
+}
+
+uint64_t sige_model_structure_hash(const sige_model_desc* model) {
+  return model ? sige_b200::model_structure_hash(model) : 0;
+}
+
 int sige_engine_put_tensor(sige_engine* eng, int step, const char* key, const float* host,
                            size_t numel) {
   return guarded([&] { eng->impl->put_tensor(step, key, host, numel); });
@@ -563,6 +597,21 @@ int sige_engine_sparse_forward(sige_engine* eng, const float* edited, const uint
     else
       sige_run_config_default(&c);
     eng->impl->sparse_forward(edited, mask, c, out, as_stream(s));
+  });
+}
+
+int sige_engine_sparse_forward_grouped(sige_engine* eng, const float* edited, const uint8_t* masks,
+                                       const sige_run_config* cfg, float* out, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    need(edited, "sparse_forward");
+    need(out, "sparse_forward");
+    sige_run_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      sige_run_config_default(&c);
+    eng->impl->sparse_forward(edited, masks, c, out, as_stream(s), true);
   });
 }
 

@@ -95,6 +95,7 @@ struct Program {
   int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
   int launches = 0;
   bool ran = false;
+  bool grouped = false;  // per-sample masks (independent requests)
   double* stats = nullptr;  // GroupNorm statistics arena (fused dense-fallback ResBlocks), zeroed per call
   size_t stats_len = 0, stats_used = 0;
   // captured calls keyed by (edited, mask, out, threshold bits): without a
@@ -114,6 +115,7 @@ Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), m
     throw ConfigError("engine: unknown math mode " + std::to_string(math));
   shapes_ = walk_shapes(m);
   name_ = m->name ? m->name : "";
+  structure_hash_ = cache_model_hash_ = model_structure_hash(m);
   in_c_ = m->in_channels;
   in_h_ = m->in_h;
   in_w_ = m->in_w;
@@ -712,6 +714,7 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
 }
 
 void Engine::precompute(const float* original, int step, cudaStream_t st) {
+  cache_model_hash_ = structure_hash_;  // precompute (graph.cpp:426-435)
   invalidate_programs();
   DevTensor& in = cache_slot(step, "input", in_c_, in_h_, in_w_, kNCHW);
   SIGE_CUDA(cudaMemcpyAsync(in.p, original, in.numel() * sizeof(float), cudaMemcpyDeviceToDevice, st));
@@ -853,7 +856,8 @@ struct ProgramBuilder {
     e.count = static_cast<int32_t*>(E.alloc(sizeof(int32_t)));
     SIGE_CUDA(cudaMemset(e.count, 0, sizeof(int32_t)));
     const int grid_tiles = ((h + b - 1) / b) * ((w + b - 1) / b);
-    e.bm = static_cast<uint32_t*>(E.alloc(static_cast<size_t>((grid_tiles + 31) / 32) * sizeof(uint32_t)));
+    e.bm = static_cast<uint32_t*>(
+        E.alloc(static_cast<size_t>((grid_tiles + 31) / 32) * (P.grouped ? E.batch_ : 1) * sizeof(uint32_t)));
     P.entries.push_back(e);
     return memo[key] = static_cast<int>(P.entries.size()) - 1;
   }
@@ -1130,6 +1134,13 @@ struct ProgramBuilder {
             if (fuse_join) {
               d2.join_bm = P.entries[es].bm;
               d2.main_bm = P.entries[em].bm;
+              if (P.grouped) {  // one activity bitmap per request
+                const auto words = [](const PlanEntryDev& e) {
+                  return (((e.h + e.b - 1) / e.b) * ((e.w + e.b - 1) / e.b) + 31) / 32;
+                };
+                d2.join_bm_words = words(P.entries[es]);
+                d2.main_bm_words = words(P.entries[em]);
+              }
               d2.join_b = P.entries[es].b;
               d2.main_b = P.entries[em].b;
               d2.join_tiles = ts;
@@ -1180,23 +1191,26 @@ struct ProgramBuilder {
     // short-circuit, graph.cpp:665-668), full NCHW copy.
     const float* cfp = cfin.p;
     int32_t* anyp = P.any;
-    add([eng, result, result_is_input, cfp, anyp, bind](cudaStream_t st) {
-      launch_finalize(bind(result, result_is_input), cfp, anyp, eng->cur_out_, st);
+    const int per_sample = P.grouped ? 1 : 0;
+    add([eng, result, result_is_input, cfp, anyp, bind, per_sample](cudaStream_t st) {
+      launch_finalize(bind(result, result_is_input), cfp, anyp, eng->cur_out_, st, per_sample);
     });
   }
 };
 
-Program& Engine::program(const sige_run_config& cfg) {
-  const std::string key = config_key(cfg);
+Program& Engine::program(const sige_run_config& cfg, bool grouped) {
+  const std::string key = config_key(cfg) + (grouped ? "|grouped" : "");
   auto it = programs_.find(key);
   if (it != programs_.end()) return *it->second;
   auto P = std::make_unique<Program>();
+  P->grouped = grouped;
+  const int masks = grouped ? batch_ : 1;
   P->full_h = in_h_;
   P->full_w = in_w_;
   P->dilate_full = cfg.dilate_full;
   P->dilate_scale = cfg.dilate_scale;
-  P->bits = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * in_h_ * ((in_w_ + 31) / 32)));
-  P->any = static_cast<int32_t*>(alloc(sizeof(int32_t)));
+  P->bits = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * in_h_ * ((in_w_ + 31) / 32) * masks));
+  P->any = static_cast<int32_t*>(alloc(sizeof(int32_t) * masks));
   P->stats_len = std::max<size_t>(stats_len(), 1);
   P->stats = static_cast<double*>(alloc(P->stats_len * sizeof(double)));
   ProgramBuilder b{*this, *P, cfg, {}};
@@ -1217,19 +1231,22 @@ Program& Engine::program(const sige_run_config& cfg) {
 }
 
 void Engine::sparse_forward(const float* edited, const uint8_t* mask, const sige_run_config& cfg,
-                            float* out, cudaStream_t st) {
+                            float* out, cudaStream_t st, bool grouped) {
   // RunConfig::validate (graph.cpp:220-227)
   if (cfg.mask_threshold < 0.0f) throw ConfigError("config: threshold must be >= 0");
   if (cfg.dilate_full < 0 || cfg.dilate_scale < 0) throw ConfigError("config: dilation radii must be >= 0");
   if (cfg.block3 < 1 || cfg.block1 < 1) throw ConfigError("config: block sizes must be >= 1");
   if (cfg.step < 0) throw ConfigError("config: step must be >= 0");
+  if (cfg.sparse && cache_model_hash_ != structure_hash_)  // check_cache_model (graph.cpp:596-603)
+    throw ConfigError("cache was precomputed for a different model than '" + name_ + "' (cache hash " +
+                      std::to_string(cache_model_hash_) + ", model hash " + std::to_string(structure_hash_) + ")");
   const uint64_t before = g_launches.load();
   if (!cfg.sparse) {  // graph.cpp:626-663: plain dense forward
     dense_forward(edited, false, cfg.step, out, st);
     last_launches_ = static_cast<int>(g_launches.load() - before);
     return;
   }
-  Program& P = program(cfg);
+  Program& P = program(cfg, grouped && batch_ > 1);
   cur_in_ = edited;
   cur_out_ = out;
   last_program_ = &P;
@@ -1301,17 +1318,18 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
     launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, side_stream_);
     SIGE_CUDA(cudaEventRecord(join_ev_, side_stream_));
   }
-  SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
+  const int masks = P.grouped ? batch_ : 1;
+  SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t) * masks, st));
   if (P.stats_used) SIGE_CUDA(cudaMemsetAsync(P.stats, 0, P.stats_used * sizeof(double), st));
   if (mask) {
-    launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st);
+    launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st, masks);
   } else {
     const DevTensor& orig = cache_tensor(cfg.step, "input");
     launch_mask_bits(orig.p, edited, batch_, in_c_, in_h_, in_w_, cfg.mask_threshold, P.bits,
-                     nullptr, P.any, st);
+                     nullptr, P.any, st, P.grouped ? 1 : 0);
   }
   launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
-              static_cast<int>(P.entries.size()), st);
+              static_cast<int>(P.entries.size()), st, P.grouped ? 1 : 0);
   if (fork)
     SIGE_CUDA(cudaStreamWaitEvent(st, join_ev_, 0));
   else if (in_twin_)
@@ -1323,6 +1341,41 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
 }
 
 void Engine::set_graphs(bool on) { use_graphs_ = on; }
+
+void Engine::release(void* p) {
+  if (!p) return;
+  auto it = std::find(allocations_.begin(), allocations_.end(), p);
+  if (it == allocations_.end()) return;
+  cudaFree(p);
+  allocations_.erase(it);
+}
+
+void Engine::drop_step(int step) {  // ActivationCache::drop_step (graph.cpp:271-274)
+  invalidate_programs();            // programs and captured graphs point into the dropped entries
+  for (auto it = cache_.begin(); it != cache_.end();) {
+    if (it->first.first != step) {
+      ++it;
+      continue;
+    }
+    release(it->second.p);  // the step's device memory goes back (multi-step caches)
+    release(it->second.h16);
+    it = cache_.erase(it);
+  }
+  for (auto it = norms_.begin(); it != norms_.end();) {
+    if (it->first.first != step) {
+      ++it;
+      continue;
+    }
+    release(it->second.scale);
+    release(it->second.shift);
+    it = norms_.erase(it);
+  }
+}
+
+void Engine::refresh_step(const float* original, int step, cudaStream_t st) {  // graph.cpp:437-444
+  drop_step(step);
+  precompute(original, step, st);
+}
 
 void Engine::set_sm_budget(int sms) {
   if (sms < 0) throw ConfigError("engine: SM budget must be >= 0");
@@ -1336,9 +1389,11 @@ int Engine::trace(uint64_t* rows, int cap, cudaStream_t st) {
   std::vector<int32_t> counts(P.entries.size());
   for (size_t i = 0; i < P.entries.size(); ++i)
     SIGE_CUDA(cudaMemcpyAsync(&counts[i], P.entries[i].count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  int32_t any = 0;
-  SIGE_CUDA(cudaMemcpyAsync(&any, P.any, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> anys(P.grouped ? batch_ : 1, 0);
+  SIGE_CUDA(cudaMemcpyAsync(anys.data(), P.any, sizeof(int32_t) * anys.size(), cudaMemcpyDeviceToHost, st));
   SIGE_CUDA(cudaStreamSynchronize(st));
+  bool any = false;
+  for (int32_t a : anys) any = any || a != 0;
   if (!any) return 0;  // short-circuit: no trace rows (graph.cpp:665-668)
   int n = 0;
   for (const TraceInfo& t : P.trace) {

@@ -74,12 +74,26 @@ class Engine {
   Engine& operator=(const Engine&) = delete;
 
   void precompute(const float* original_nchw, int step, cudaStream_t st);
+  // ActivationCache lifecycle (graph.hpp:116-176): drop_step erases one
+  // step's entries (graph.cpp:271-274); refresh_step replaces them from a new
+  // original (graph.cpp:437-444); the cache's model hash guards sparse_forward
+  // against a cache built for another model (check_cache_model, graph.cpp:596-603).
+  void drop_step(int step);
+  void refresh_step(const float* original_nchw, int step, cudaStream_t st);
+  uint64_t structure_hash() const { return structure_hash_; }
+  uint64_t cache_model_hash() const { return cache_model_hash_; }
+  void set_cache_model_hash(uint64_t h) { cache_model_hash_ = h; }
   void put_tensor(int step, const std::string& key, const float* host_nchw, size_t numel);
   void put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np);
   void get_tensor(int step, const std::string& key, float* host_nchw, size_t numel);
   void get_norm(int step, const std::string& key, float* sc, float* sh, size_t np);
+  // grouped: every batch sample is an independent request with its own
+  // difference mask (mask: batch x H x W when given) — per-sample IndexPlans
+  // concatenated n-major into each layer's tile list, one launch per layer for
+  // all requests; each sample's output equals a batch-1 sparse_forward of that
+  // request (graph.cpp:619-901). Otherwise one mask is shared by the batch.
   void sparse_forward(const float* edited, const uint8_t* mask, const sige_run_config& cfg,
-                      float* out, cudaStream_t st);
+                      float* out, cudaStream_t st, bool grouped = false);
   void dense_forward(const float* in, bool reused_stats, int step, float* out, cudaStream_t st);
 
   void output_shape(int* n, int* c, int* h, int* w) const;
@@ -147,7 +161,7 @@ class Engine {
   void drop_act(int step);
   void dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
                   cudaStream_t st);
-  Program& program(const sige_run_config& cfg);
+  Program& program(const sige_run_config& cfg, bool grouped);
   void run_program(Program& P, const float* edited, const uint8_t* mask, const sige_run_config& cfg,
                    cudaStream_t st);
   bool use_graphs_ = true;
@@ -159,6 +173,8 @@ class Engine {
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
 
   std::string name_;
+  uint64_t structure_hash_ = 0;     // of the engine's model
+  uint64_t cache_model_hash_ = 0;   // of the model the cache was built for
   int batch_, math_, in_c_, in_h_, in_w_;
   int out_c_ = 0, out_h_ = 0, out_w_ = 0;
   std::vector<LayerDev> layers_;
@@ -207,6 +223,7 @@ class Engine {
   const float* cur_in_ = nullptr;
   float* cur_out_ = nullptr;
   void* alloc(size_t bytes);
+  void release(void* p);  // frees an alloc() block early (dropped cache entries)
 };
 
 }  // namespace sige_b200

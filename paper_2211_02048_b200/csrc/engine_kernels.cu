@@ -23,11 +23,18 @@ inline int grid_cap(long long n, int threads) {
 // compute_difference_mask (mask.cpp:14-32) straight into a row-major bit mask
 // (ceil(W/32) words per row). grid.y splits the N*C planes; set bits are
 // merged with atomicOr, so the result is order-independent.
+// Grouped requests (per-sample masks): grid.z = sample, each with its own
+// planes, bit mask (h x wpr words) and any flag.
 __global__ void k_mask_bits(const float* __restrict__ o, const float* __restrict__ e, int planes,
                             int ppy, int h, int w, float thr, uint32_t* __restrict__ bits,
                             uint8_t* __restrict__ mask_u8, int32_t* __restrict__ any) {
   const long long hw = static_cast<long long>(h) * w;
   const int wpr = (w + 31) >> 5;
+  o += static_cast<long long>(blockIdx.z) * planes * hw;
+  e += static_cast<long long>(blockIdx.z) * planes * hw;
+  bits += static_cast<long long>(blockIdx.z) * h * wpr;
+  any += blockIdx.z;
+  if (mask_u8) mask_u8 += blockIdx.z * hw;
   const int p0 = blockIdx.y * ppy, p1 = min(planes, p0 + ppy);
   const bool vec = (w & 3) == 0;
   const long long nq = vec ? hw >> 2 : hw;
@@ -61,6 +68,9 @@ __global__ void k_mask_bits(const float* __restrict__ o, const float* __restrict
 __global__ void k_mask_u8_to_bits(const uint8_t* __restrict__ m, int h, int w, uint32_t* bits,
                                   int32_t* __restrict__ any) {
   const int wpr = (w + 31) >> 5;
+  m += static_cast<long long>(blockIdx.z) * h * w;  // grouped: one mask per sample
+  bits += static_cast<long long>(blockIdx.z) * h * wpr;
+  any += blockIdx.z;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)h * wpr;
        q += (long long)gridDim.x * blockDim.x) {
     int y = static_cast<int>(q / wpr), wd = static_cast<int>(q % wpr);
@@ -100,18 +110,27 @@ __device__ __forceinline__ bool rect_any(const uint32_t* bits, int wpr, int y0, 
 // dilate_full, clipped — composition of dilate_mask (mask.cpp:55-80),
 // downsample_mask (mask.cpp:34-53) / replicate_mask (graph.cpp:485-500) and
 // the "any pixel in tile" test of mask_to_block_indices (mask.cpp:113-127).
-__global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df, int ds, int batch,
-                       const PlanEntryDev* __restrict__ entries, int use_smem) {
+// per_sample (grouped requests): one pass per sample over its own bit mask,
+// tiles appended n-major ((n, r, c) order) and one activity bitmap per sample;
+// otherwise one pass over the shared mask, replicated for every sample
+// (mask_to_block_indices, mask.cpp:129-134).
+__global__ void k_plan(const uint32_t* __restrict__ gbits_all, int H, int W, int df, int ds, int batch,
+                       const PlanEntryDev* __restrict__ entries, int use_smem, int per_sample) {
   extern __shared__ uint32_t sbits[];
   __shared__ int warp_sums[32];
   __shared__ int base;
   const int wpr = (W + 31) >> 5;
+  const PlanEntryDev e = entries[blockIdx.x];
+  if (threadIdx.x == 0) base = 0;
+  const int passes = per_sample ? batch : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+  const uint32_t* gbits = gbits_all + static_cast<long long>(pass) * H * wpr;
   const uint32_t* bits = gbits;
+  __syncthreads();  // previous pass done with the shared bits
   if (use_smem) {
     for (int i = threadIdx.x; i < H * wpr; i += blockDim.x) sbits[i] = gbits[i];
     bits = sbits;
   }
-  const PlanEntryDev e = entries[blockIdx.x];
   const int h = e.h, w = e.w, b = e.b;
   const int ty = (h + b - 1) / b, tx = (w + b - 1) / b, tiles = ty * tx;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -143,8 +162,8 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
       rowor[k] = acc;
     }
   }
-  if (threadIdx.x == 0) base = 0;
   __syncthreads();
+  uint32_t* bm = e.bm ? e.bm + static_cast<long long>(pass) * ((tiles + 31) >> 5) : nullptr;
   for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
     const int t = t0 + threadIdx.x;
     bool on = false;
@@ -181,7 +200,7 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
     }
     const unsigned bal = __ballot_sync(0xffffffffu, on);
     if (lane == 0) warp_sums[wid] = __popc(bal);
-    if (e.bm && lane == 0 && t0 + wid * 32 < tiles) e.bm[(t0 + wid * 32) >> 5] = bal;  // tile activity bitmap
+    if (bm && lane == 0 && t0 + wid * 32 < tiles) bm[(t0 + wid * 32) >> 5] = bal;  // tile activity bitmap
     __syncthreads();
     if (wid == 0) {
       int v = lane < nw ? warp_sums[lane] : 0;
@@ -195,7 +214,7 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
     __syncthreads();
     const int slot = base + (wid ? warp_sums[wid - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
     if (on && slot < e.capacity) {
-      e.idx[3 * slot] = 0;
+      e.idx[3 * slot] = pass;
       e.idx[3 * slot + 1] = R;
       e.idx[3 * slot + 2] = Cc;
     }
@@ -203,6 +222,11 @@ __global__ void k_plan(const uint32_t* __restrict__ gbits, int H, int W, int df,
     __syncthreads();
     if (threadIdx.x == 0) base += chunk_total;
     __syncthreads();
+  }
+  }  // passes
+  if (per_sample) {
+    if (threadIdx.x == 0) *e.count = min(base, e.capacity);
+    return;
   }
   const int per = base;
   for (int n = 1; n < batch; ++n)
@@ -523,12 +547,13 @@ __global__ void k_materialize_act(Src s, void* __restrict__ dst, int half) {
 }
 
 __global__ void k_finalize(Src r, const float* __restrict__ cached, const int32_t* __restrict__ any,
-                           float* __restrict__ out) {
+                           float* __restrict__ out, int per_sample) {
   pdl_enter();
-  const bool use = *any != 0;
   const long long total = static_cast<long long>(r.n) * r.c * r.h * r.w;
+  const long long per_n = static_cast<long long>(r.c) * r.h * r.w;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
+    const bool use = any[per_sample ? q / per_n : 0] != 0;  // empty mask -> cached final (graph.cpp:665-668)
     if (!use) {
       out[q] = cached[q];
       continue;
@@ -601,30 +626,32 @@ __global__ void k_nhwc_to_nchw(const float* __restrict__ in, float* __restrict__
 }  // namespace
 
 void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
-                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st) {
+                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st, int per_sample) {
   const int wpr = (w + 31) >> 5;
-  SIGE_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * h * wpr, st));
-  if (mask_u8) SIGE_CUDA(cudaMemsetAsync(mask_u8, 0, static_cast<size_t>(h) * w, st));
+  const int masks = per_sample ? n : 1;
+  SIGE_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * h * wpr * masks, st));
+  if (mask_u8) SIGE_CUDA(cudaMemsetAsync(mask_u8, 0, static_cast<size_t>(h) * w * masks, st));
   const long long hw = static_cast<long long>(h) * w;
   const long long nq = (w & 3) == 0 ? hw / 4 : hw;
-  const int planes = n * c;
+  const int planes = per_sample ? c : n * c;
   const int gx = static_cast<int>(std::min<long long>((nq + 255) / 256, 4096));
-  int gy = std::min(planes, std::max(1, sm_count() * 8 / gx));
+  int gy = std::min(planes, std::max(1, sm_count() * 8 / (gx * masks)));
   const int ppy = (planes + gy - 1) / gy;
   gy = (planes + ppy - 1) / ppy;
-  k_mask_bits<<<dim3(gx, gy), 256, 0, st>>>(orig, edited, planes, ppy, h, w, thr, bits, mask_u8, any);
+  k_mask_bits<<<dim3(gx, gy, masks), 256, 0, st>>>(orig, edited, planes, ppy, h, w, thr, bits, mask_u8, any);
   after_launch("k_mask_bits");
 }
 
 void launch_mask_u8_to_bits(const uint8_t* mask, int h, int w, uint32_t* bits, int32_t* any,
-                            cudaStream_t st) {
+                            cudaStream_t st, int masks) {
   const int wpr = (w + 31) >> 5;
-  k_mask_u8_to_bits<<<grid_cap(static_cast<long long>(h) * wpr, 256), 256, 0, st>>>(mask, h, w, bits, any);
+  k_mask_u8_to_bits<<<dim3(grid_cap(static_cast<long long>(h) * wpr, 256), 1, masks), 256, 0, st>>>(mask, h, w, bits,
+                                                                                                    any);
   after_launch("k_mask_u8_to_bits");
 }
 
 void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate_scale, int batch,
-                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st) {
+                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st, int per_sample) {
   if (num_entries == 0) return;
   // full-resolution bits + the per-tile-row OR table (tile rows <= 2 H)
   const size_t smem = sizeof(uint32_t) * 3 * H * ((W + 31) >> 5);
@@ -633,7 +660,7 @@ void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate
   if (use_smem && smem > 48 * 1024 && first_on_device(attr_done))
     SIGE_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   k_plan<<<num_entries, 1024, use_smem ? smem : 0, st>>>(bits, H, W, dilate_full, dilate_scale,
-                                                         batch, entries_dev, use_smem);
+                                                         batch, entries_dev, use_smem, per_sample);
   after_launch("k_plan");
 }
 
@@ -725,9 +752,9 @@ void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_elems_per_
 }
 
 void launch_finalize(const Src& result, const float* cached_final, const int32_t* any, float* out,
-                     cudaStream_t st) {
+                     cudaStream_t st, int per_sample) {
   const long long total = static_cast<long long>(result.n) * result.c * result.h * result.w;
-  launch_pdl(k_finalize, dim3(grid_cap(total, 256)), dim3(256), st, result, cached_final, any, out);
+  launch_pdl(k_finalize, dim3(grid_cap(total, 256)), dim3(256), st, result, cached_final, any, out, per_sample);
   after_launch("k_finalize");
 }
 

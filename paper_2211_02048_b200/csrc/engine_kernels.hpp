@@ -98,6 +98,7 @@ struct Dst {
   const uint32_t* join_bm = nullptr;
   const uint32_t* main_bm = nullptr;
   int join_b = 0, main_b = 0;
+  int join_bm_words = 0, main_bm_words = 0;  // words per sample (grouped requests), 0: one shared bitmap
   Src join_x;    // the block input x
   Tiles join_tiles;  // the shortcut tile list
   // Optional GroupNorm statistics of the written values: += (sum, sum of
@@ -164,15 +165,17 @@ struct PlanEntryDev {
   int32_t* idx;    // capacity triplets
   int32_t* count;  // device int
   int capacity;
-  uint32_t* bm;    // activity bitmap of the (h/b, w/b) tile grid, row-major (shared by the batch)
+  uint32_t* bm;    // activity bitmap of the (h/b, w/b) tile grid, row-major (one per sample when grouped)
 };
 // Both set *any = 1 when at least one pixel is set (the caller zeroes it).
+// per_sample / masks > 1 (grouped requests): one mask, bit mask and any flag
+// per sample (bits: masks x h x ceil(w/32) words).
 void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
-                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st);
+                      uint32_t* bits, uint8_t* mask_u8, int32_t* any, cudaStream_t st, int per_sample = 0);
 void launch_mask_u8_to_bits(const uint8_t* mask, int h, int w, uint32_t* bits, int32_t* any,
-                            cudaStream_t st);
+                            cudaStream_t st, int masks = 1);
 void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate_scale, int batch,
-                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st);
+                 const PlanEntryDev* entries_dev, int num_entries, cudaStream_t st, int per_sample = 0);
 
 // GroupNorm statistics + fold (norm.cpp:25-90) over a full NHWC tensor,
 // writing scale/shift (n*C). exact=1 follows the reference's sequential
@@ -210,7 +213,7 @@ void launch_restore(const RestoreJob* jobs_dev, int num_jobs, int max_tiles, cud
 // out (NCHW, full) = *any ? value of `result` : cached_final — the empty-mask
 // short-circuit of sparse_forward (graph.cpp:665-668) folded into the final copy.
 void launch_finalize(const Src& result, const float* cached_final, const int32_t* any, float* out,
-                     cudaStream_t st);
+                     cudaStream_t st, int per_sample = 0);
 // Elementwise a + b over n values (dense ResBlock sum in precompute).
 void launch_add(const float* a, const float* b, float* out, size_t n, cudaStream_t st);
 // Same, also writing out_h16 = fp16(out) when out_h16 != nullptr.

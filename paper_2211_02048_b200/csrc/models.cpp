@@ -310,6 +310,61 @@ uint64_t hnorm(const sige_norm_desc& n, uint64_t h) {
 }
 }  // namespace
 
+// ModelSpec::structure_hash (graph.cpp:89-127): name, input dims, then per
+// layer its kind, sparse policy and parameters (hash_conv / hash_norm,
+// graph.cpp:68-85) — the guard that ties an ActivationCache to its model.
+namespace {
+uint64_t sconv(const sige_conv_desc& c, uint64_t h) {
+  const int dims[4] = {c.c_in, c.c_out, c.k, c.stride};
+  h = fnv1a64(dims, sizeof(dims), h);
+  h = hv(c.weight, static_cast<size_t>(c.c_out) * c.c_in * c.k * c.k, h);
+  return hv(c.bias, c.bias ? c.c_out : 0, h);
+}
+uint64_t snorm(const sige_norm_desc& n, uint64_t h) {
+  const int meta[2] = {n.kind, n.groups};
+  h = fnv1a64(meta, sizeof(meta), h);
+  h = fnv1a64(&n.eps, sizeof(n.eps), h);
+  return hnorm(n, h);
+}
+}  // namespace
+
+uint64_t model_structure_hash(const sige_model_desc* d) {
+  uint64_t h = fnv1a64(d->name, std::strlen(d->name), kFnvSeed);
+  const int dims[3] = {d->in_channels, d->in_h, d->in_w};
+  h = fnv1a64(dims, sizeof(dims), h);
+  for (int i = 0; i < d->num_layers; ++i) {
+    const sige_layer_desc& L = d->layers[i];
+    h = fnv1a64(&L.kind, sizeof(L.kind), h);
+    const int pol[2] = {L.policy_sparse ? 1 : 0, L.min_resolution};
+    h = fnv1a64(pol, sizeof(pol), h);
+    switch (L.kind) {
+      case SIGE_LAYER_CONV:
+      case SIGE_LAYER_DOWNSAMPLE:
+        h = sconv(L.conv, h);
+        break;
+      case SIGE_LAYER_NORM:
+        h = snorm(L.norm, h);
+        break;
+      case SIGE_LAYER_ACTIVATION:
+        h = fnv1a64(&L.act, sizeof(L.act), h);
+        break;
+      case SIGE_LAYER_RESBLOCK: {
+        h = sconv(L.conv, h);
+        h = sconv(L.conv2, h);
+        h = snorm(L.norm, h);
+        h = fnv1a64(&L.act, sizeof(L.act), h);
+        const int has_sc = L.has_shortcut ? 1 : 0;
+        h = fnv1a64(&has_sc, sizeof(has_sc), h);
+        if (has_sc) h = sconv(L.shortcut, h);
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  return h;
+}
+
 uint64_t model_weight_hash(const sige_model_desc* d) {  // models.cpp:185-207
   uint64_t h = fnv1a64(d->name, std::strlen(d->name), kFnvSeed);
   for (int i = 0; i < d->num_layers; ++i) {

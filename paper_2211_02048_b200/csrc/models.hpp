@@ -18,6 +18,7 @@ void make_edit_fixture(const std::string& kind, int n, int c, int h, int w, uint
 sige_model_desc* build_model(const std::string& name);
 void free_model(sige_model_desc* d);
 uint64_t model_weight_hash(const sige_model_desc* d);
+uint64_t model_structure_hash(const sige_model_desc* d);  // ModelSpec::structure_hash (graph.cpp:89-127)
 
 struct LayerShape {
   int c_in, h_in, w_in, c_out, h_out, w_out;

@@ -50,6 +50,40 @@ def serve(n_requests: int, handler: Callable[[int], tuple[float, float]], world:
     return out
 
 
+def groups_for_rank(n_requests: int, world: int, rank: int, group: int) -> list[list[int]]:
+    """This rank's requests (i mod world) in consecutive groups of at most
+    `group`: each group is served by one grouped engine (one launch per layer
+    for all of its requests, Engine.sparse_forward_grouped)."""
+    if group < 1:
+        raise ValueError("group size must be >= 1")
+    mine = requests_for_rank(n_requests, world, rank)
+    return [mine[i:i + group] for i in range(0, len(mine), group)]
+
+
+def serve_grouped(n_requests: int, group_handler: Callable[[list[int]], Sequence[tuple[float, float]]], group: int,
+                  world: int | None = None, rank: int | None = None) -> list[RequestResult] | None:
+    """Like serve(), but the handler takes a whole group of this rank's requests
+    and returns one (ms, checksum) per request of the group."""
+    if world is None:
+        world = dist.get_world_size() if dist.is_initialized() else 1
+        rank = dist.get_rank() if dist.is_initialized() else 0
+    mine: list[RequestResult] = []
+    for ids in groups_for_rank(n_requests, world, rank, group):
+        res = list(group_handler(ids))
+        if len(res) != len(ids):
+            raise AssertionError(f"group handler returned {len(res)} results for {len(ids)} requests")
+        mine += [RequestResult(i, rank, ms, cs) for i, (ms, cs) in zip(ids, res)]
+    if world == 1 or not dist.is_initialized():
+        return mine
+    gathered: list = [None] * world if rank == 0 else None
+    dist.gather_object(mine, gathered, dst=0)
+    if rank != 0:
+        return None
+    out = [r for part in gathered for r in part]
+    out.sort(key=lambda r: r.request)
+    return out
+
+
 def max_over_ranks(value: float, device: torch.device | None = None) -> float:
     """Max of a per-rank timing over all ranks (multi-GPU numbers are the
     slowest rank's, never a wall-clock average)."""

@@ -86,3 +86,19 @@ def test_ddim_stack_structure():
             chans.add(L.conv2.c_out)
     assert convs == 80
     assert chans == {3, 128, 256, 512}
+
+
+def test_structure_hash_matches_reference(ref):
+    """ModelSpec::structure_hash (graph.cpp:89-127) — the cache/model guard key —
+    restated in models.cpp equals the reference's for every model (host only)."""
+    import ctypes as C
+
+    import paper_2211_02048_b200 as sb
+
+    ref.lib.ref_model_structure_hash.restype = C.c_uint64
+    ref.lib.ref_model_structure_hash.argtypes = [C.c_void_p]
+    for name in ("mini_unet_gn", "mini_unet_bn", "gaugan_stack_in", "conv3x3_128", "single_conv64", "ddim_stack",
+                 "ddim_stack_64x32"):
+        m = sb.Model(name)
+        rm = ref.model(name)
+        assert m.structure_hash() == ref.lib.ref_model_structure_hash(rm.h), name

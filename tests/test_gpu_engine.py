@@ -237,3 +237,43 @@ def test_fusion_toggles_do_not_change_the_output(orc, math):
             assert np.array_equal(outs[-1], want)
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+
+
+def test_cache_lifecycle_steps_and_model_guard(orc):
+    """Multi-step ActivationCache (graph.hpp:116-176): per-step precompute,
+    drop_step (graph.cpp:271-274) frees a step, refresh_step (graph.cpp:437-444)
+    replaces one from a new original, and a cache declared for another model
+    fails like check_cache_model (graph.cpp:596-603)."""
+    name = "mini_unet_gn"
+    om = orc.model(name)
+    a_orig, a_edit = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 61)
+    b_orig, b_edit = orc.make_edit_fixture("blob5", 1, 3, 64, 64, 62)
+    eng = sb.Engine(sb.Model(name), math=sb.MATH_EXACT)
+    eng.precompute(torch.from_numpy(a_orig).cuda(), step=0)
+    eng.precompute(torch.from_numpy(b_orig).cuda(), step=1)
+    bytes_two = eng.cache_bytes()
+
+    def run(edit, step):
+        cfg = sb.default_config(dilate_full=om.required_dilation(), step=step)
+        return eng.sparse_forward(torch.from_numpy(edit).cuda(), config=cfg).cpu().numpy()
+
+    def want(orig, edit):
+        cfg = sb.default_config(dilate_full=om.required_dilation())
+        return om.sparse_forward(om.precompute(orig), edit, orc.difference_mask(orig, edit), cfg)[0]
+
+    assert np.array_equal(run(a_edit, 0), want(a_orig, a_edit))
+    assert np.array_equal(run(b_edit, 1), want(b_orig, b_edit))
+    eng.drop_step(1)
+    assert eng.cache_bytes() < bytes_two
+    with pytest.raises(sb.ConfigError, match="precompute required: no cache entry for step 1"):
+        run(b_edit, 1)
+    assert np.array_equal(run(a_edit, 0), want(a_orig, a_edit))  # step 0 untouched
+    eng.refresh_step(torch.from_numpy(b_orig).cuda(), 0)  # step 0 now holds b's activations
+    assert np.array_equal(run(b_edit, 0), want(b_orig, b_edit))
+    cache_h, model_h = eng.cache_model_hash()
+    assert cache_h == model_h == sb.Model(name).structure_hash()
+    eng.set_cache_model_hash(sb.Model("mini_unet_bn").structure_hash())
+    with pytest.raises(sb.ConfigError, match="cache was precomputed for a different model than 'mini_unet_gn'"):
+        run(b_edit, 0)
+    eng.set_cache_model_hash(model_h)
+    assert np.array_equal(run(b_edit, 0), want(b_orig, b_edit))
