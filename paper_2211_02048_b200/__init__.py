@@ -205,25 +205,49 @@ def resize_nearest(x: torch.Tensor, out_h: int, out_w: int) -> torch.Tensor:
     return out
 
 
-def scatter_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> None:
+def _check_scatter(op: str, blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor, idx_hw) -> None:
+    """require_scatter_compatible (kernels.cpp:18-35): channels, index
+    resolution (when the caller states it) and every block's sample in range."""
+    n, c, h, w = base.shape
+    if blocks.dim() != 4 or blocks.shape[2] != blocks.shape[3]:
+        raise ConfigError(f"{op}: blocks must be overlap-free output tiles")
+    if blocks.shape[1] != c:
+        raise ConfigError(f"{op}: channel mismatch")
+    if idx_hw is not None and tuple(idx_hw) != (h, w):
+        raise ConfigError(f"{op}: index resolution {idx_hw[0]}x{idx_hw[1]} does not match tensor ({n}, {c}, {h}, {w})")
+    if idx.shape[0]:
+        lo, hi = int(idx[:, 0].min()), int(idx[:, 0].max())
+        if lo < 0 or hi >= n:
+            raise ConfigError(f"{op}: block sample out of range")
+
+
+def scatter_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor, idx_hw=None) -> None:
+    """kernels.hpp:54 — idx_hw: the index set's resolution (BlockIndexSet::h, w), checked when given."""
     b = _dev(blocks, torch.float32, "scatter")
     i = _dev(idx, torch.int32, "scatter")
     if not base.is_contiguous():
         raise ConfigError("scatter: base must be contiguous")
+    _check_scatter("scatter", b, i, base, idx_hw)
     _check(_lib().sige_scatter_inplace(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.data_ptr(), *base.shape, _stream()))
 
 
-def scatter(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> torch.Tensor:
+def scatter(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor, idx_hw=None) -> torch.Tensor:
+    """kernels.hpp:53."""
     out = torch.empty_like(_dev(base, torch.float32, "scatter"))
     b = _dev(blocks, torch.float32, "scatter")
     i = _dev(idx, torch.int32, "scatter")
+    _check_scatter("scatter", b, i, base, idx_hw)
     _check(_lib().sige_scatter(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.contiguous().data_ptr(), out.data_ptr(), *out.shape, _stream()))
     return out
 
 
-def scatter_add_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor) -> None:
+def scatter_add_inplace(blocks: torch.Tensor, idx: torch.Tensor, base: torch.Tensor, idx_hw=None) -> None:
+    """kernels.hpp:57."""
     b = _dev(blocks, torch.float32, "scatter_add")
     i = _dev(idx, torch.int32, "scatter_add")
+    if not base.is_contiguous():
+        raise ConfigError("scatter_add: base must be contiguous")
+    _check_scatter("scatter_add", b, i, base, idx_hw)
     _check(_lib().sige_scatter_add_inplace(b.data_ptr(), i.shape[0], b.shape[1], b.shape[2], i.data_ptr(), base.data_ptr(), *base.shape, _stream()))
 
 
@@ -308,6 +332,11 @@ def _residual(fn, main_blocks, main_idx, shortcut_blocks, shortcut_idx, precompu
     si = _dev(shortcut_idx, torch.int32, "block_residual")
     s = _dev(precomputed_sum, torch.float32, "block_residual")
     o = _dev(original_shortcut, torch.float32, "block_residual")
+    # require_join_compatible (kernels.cpp:276-287)
+    _check_scatter("block_residual(main)", mb, mi, s, None)
+    _check_scatter("block_residual(shortcut)", sb, si, s, None)
+    if s.shape != o.shape:
+        raise ConfigError("block_residual: shape mismatch")
     out = torch.empty_like(s)
     _check(fn(mb.data_ptr(), mi.shape[0], mb.shape[2], mi.data_ptr(), sb.data_ptr(), si.shape[0], sb.shape[2], si.data_ptr(),
               s.data_ptr(), o.data_ptr(), out.data_ptr(), *s.shape, _stream()))

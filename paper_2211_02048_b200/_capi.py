@@ -220,7 +220,10 @@ SYMBOLS = {
 
 
 def _declare(L: C.CDLL) -> None:
+    override = "SIGE_B200_LIB" in os.environ  # an older build may lack newer entry points
     for name, (res, args) in SYMBOLS.items():
+        if override and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args

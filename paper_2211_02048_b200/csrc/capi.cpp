@@ -193,15 +193,6 @@ int sige_resize_nearest(const float* in, int n, int c, int h, int w, int out_h, 
   return guarded([&] { op_resize_nearest(in, n, c, h, w, out_h, out_w, out, as_stream(s)); });
 }
 
-namespace {
-void check_scatter_res(int idx_h, int idx_w, int n, int c, int h, int w, const char* op) {
-  if (idx_h != h || idx_w != w)
-    throw ConfigError(std::string(op) + ": index resolution " + std::to_string(idx_h) + "x" +
-                      std::to_string(idx_w) + " does not match tensor (" + std::to_string(n) +
-                      ", " + std::to_string(c) + ", " + std::to_string(h) + ", " +
-                      std::to_string(w) + ")");
-}
-}  // namespace
 
 int sige_scatter_inplace(const float* blocks, int count, int channels, int block, const int32_t* idx,
                          float* base, int n, int c, int h, int w, sige_stream_t s) {
@@ -324,8 +315,8 @@ int sige_scatter_with_block_residual(const float* mb, int mcount, int mblock, co
   return guarded([&] {
     cudaStream_t st = as_stream(s);
     SIGE_CUDA(cudaMemcpyAsync(out, sum, sizeof(float) * n * c * h * w, cudaMemcpyDeviceToDevice, st));
-    op_residual_pass(mb, mcount, c, mblock, midx, orig_sc, out, h, w, false, st);
-    op_residual_pass(sb, scount, c, sblock, sidx, orig_sc, out, h, w, true, st);
+    op_residual_pass(mb, mcount, c, mblock, midx, orig_sc, out, n, h, w, false, st);
+    op_residual_pass(sb, scount, c, sblock, sidx, orig_sc, out, n, h, w, true, st);
   });
 }
 

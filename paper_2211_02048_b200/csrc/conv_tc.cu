@@ -127,6 +127,11 @@ struct TcParams {
 };
 
 // ------------------------------------------------------------- PTX ------
+// Phase marks (developer instrumentation): compiled in only with
+// -DSIGE_TC_MARKS (tools/build_variant.sh marks -DSIGE_TC_MARKS, used by
+// SIGE_TC_TIMELINE / tools/graph_timeline.py). The production build carries
+// none — the checks alone cost 3-4 % of the edit (profiles/r2_ab_variants.txt).
+#ifdef SIGE_TC_MARKS
 __device__ __forceinline__ void tl_mark(const TcParams& p, int idx) {
   if (p.tl && blockIdx.x < 8) {
     unsigned long long t;
@@ -145,6 +150,14 @@ __device__ __forceinline__ void tl_cta(const TcParams& p, int base) {
     p.tl[base + blockIdx.x] = t;
   }
 }
+__device__ __forceinline__ void tl_clock(const TcParams& p, int idx) {
+  if (p.tl && blockIdx.x < 8) p.tl[blockIdx.x * 64 + idx] = clock64();
+}
+#else
+__device__ __forceinline__ void tl_mark(const TcParams&, int) {}
+__device__ __forceinline__ void tl_cta(const TcParams&, int) {}
+__device__ __forceinline__ void tl_clock(const TcParams&, int) {}
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1034,11 +1047,7 @@ struct MmaCtx {
 };
 
 // All MMAs of one K chunk: K*K taps x 4 k-steps, one weight stage per TPS taps.
-// KS: k-steps issued per tap (of 4) — 1 for a chunk with <= 1/4 of its
-// channels real (the 3-channel input conv): the MMAs over zero padding (zero
-// weights) are skipped, which is exact. Compile-time: a runtime guard on
-// the issue path measured 40 % slower MMA phases.
-template <bool F16, int K, int S, int TPS, int KS>
+template <bool F16, int K, int S, int TPS>
 __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_chunk) {
   static_assert((K * K) % TPS == 0, "taps per stage must divide the tap count");
 #pragma unroll
@@ -1056,7 +1065,7 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
           abase + phase * c.plane16 + static_cast<uint32_t>(ky / S) * c.P + static_cast<uint32_t>(kx / S) * c.row16;
       const uint32_t boff = bbase + static_cast<uint32_t>(tt) * c.tap_b16;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) {  // KS MMAs of K = 32 bytes each
+      for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
         const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * c.kstep16) & 0x3FFFu);
         const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2) & 0x3FFFu);
         const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
@@ -1111,7 +1120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
     tl_cta(p, 1024);
-    if (p.tl && blockIdx.x < 8) p.tl[blockIdx.x * 64 + 60] = clock64();
+    tl_clock(p, 60);
   }
   for (int q = threadIdx.x; q < p.phases * p.T * p.Mt; q += blockDim.x) row_tab[q] = row_info(p, q);
 
@@ -1693,21 +1702,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (lane == 0 && it == 0 && ch < 8) tl_mark(p, 22 + ch);
         const uint32_t abase = c.a0 + aslot * astage16;
-        constexpr int kStepCh = (F16 ? 64 : 32) / 4;  // input channels per k-step
-        if (p.c_in - ch * 4 * kStepCh <= kStepCh) {     // one k-step of real channels
-          if (tps == 9)
-            mma_chunk<F16, K, S, (K == 3 ? 9 : 1), 1>(c, abase, ch == c_begin);
-          else if (tps == 3)
-            mma_chunk<F16, K, S, (K == 3 ? 3 : 1), 1>(c, abase, ch == c_begin);
-          else
-            mma_chunk<F16, K, S, 1, 1>(c, abase, ch == c_begin);
-        } else if (tps == 9) {
-          mma_chunk<F16, K, S, (K == 3 ? 9 : 1), 4>(c, abase, ch == c_begin);
-        } else if (tps == 3) {
-          mma_chunk<F16, K, S, (K == 3 ? 3 : 1), 4>(c, abase, ch == c_begin);
-        } else {
-          mma_chunk<F16, K, S, 1, 4>(c, abase, ch == c_begin);
-        }
+        // (Skipping the k-steps over zero padding of a tiny input — the
+        // 3-channel first conv — measured slower overall: a runtime guard on
+        // the issue path cost 40 % of the MMA phase, compile-time variants the
+        // instruction cache.)
+        if (tps == 9)
+          mma_chunk<F16, K, S, (K == 3 ? 9 : 1)>(c, abase, ch == c_begin);
+        else if (tps == 3)
+          mma_chunk<F16, K, S, (K == 3 ? 3 : 1)>(c, abase, ch == c_begin);
+        else
+          mma_chunk<F16, K, S, 1>(c, abase, ch == c_begin);
         if (elect_one()) umma_commit(&bar_afree[aslot]);
         if (++aslot == na) {
           aslot = 0;
@@ -1750,7 +1754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (threadIdx.x == 0) {
     tl_mark(p, 12);
-    if (p.tl && blockIdx.x < 8) p.tl[blockIdx.x * 64 + 61] = clock64();
+    tl_clock(p, 61);
   }
   tc_fence_before();
   __syncthreads();

@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <string>
@@ -132,8 +133,11 @@ class Engine {
   // fallback, dense_forward): conv1's epilogue accumulates the statistics,
   // conv2 folds them and applies norm + act to its staged window in shared
   // memory (no separate statistics / fold / activation kernels).
+  // (The folded table of n x C scale/shift pairs lives in shared memory:
+  // batches beyond 4096 / C channels take the separate fold + act path.)
   bool fused_gn(const LayerDev& L) const {
-    return math_ == SIGE_MATH_F16 && L.norm_kind != SIGE_NORM_BATCH;
+    return math_ == SIGE_MATH_F16 && L.norm_kind != SIGE_NORM_BATCH &&
+           static_cast<long long>(batch_) * std::max(L.channels, L.conv2.c_in) <= 4096;
   }
   double* dense_stats_ = nullptr;  // statistics arena of dense walks (zeroed per walk)
   // F16: fp16 channels-last copy of the current input (channels padded to 8),

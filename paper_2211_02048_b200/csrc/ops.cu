@@ -300,7 +300,7 @@ __global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
 // mode 0 writes, mode 1 adds.
 __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ blocks, int count, int c, int b,
                                                       const int32_t* __restrict__ idx, float* __restrict__ base,
-                                                      int h, int w, int T, int cpi, int staged, int mode) {
+                                                      int nsamp, int h, int w, int T, int cpi, int staged, int mode) {
   __shared__ int s_org[kMaxChunkTiles][3];
   __shared__ __align__(16) float s_buf[kStageFloats];
   const int bsz = b * b;
@@ -322,7 +322,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
     for (; cw.col < cols; cw.col += cw.col_step) {
       const int t = cw.col / b, dx = cw.col - t * b;
       const int y0 = s_org[t][1], xx = s_org[t][2] + dx;
-      const int dy_hi = xx < w ? min(b, h - y0) : 0;  // fringe clipping
+      // fringe clipping; an index outside the tensor (the wrappers reject it,
+      // require_scatter_compatible, kernels.cpp:18-35) never writes
+      const bool inside = s_org[t][0] >= 0 && s_org[t][0] < nsamp && y0 >= 0 && s_org[t][2] >= 0;
+      const int dy_hi = inside && xx < w ? min(b, h - y0) : 0;
       float* dpb = base + (static_cast<size_t>(s_org[t][0]) * c + c0) * plane + static_cast<size_t>(y0) * w + xx;
       const float* sp = staged ? s_buf + t * run + dx : sb + t * slab + dx;
       for (int cl = cw.group; cl < ncl; cl += cw.groups) {
@@ -470,7 +473,7 @@ __global__ void k_scatter_gather(const float* __restrict__ blocks, int pb, const
 // shortcut tiles out = out + (s - sc_orig).
 __global__ void k_residual(const float* __restrict__ blocks, int count, int c, int b,
                            const int32_t* __restrict__ idx, const float* __restrict__ orig_sc,
-                           float* __restrict__ out, int h, int w, int shortcut_pass) {
+                           float* __restrict__ out, int nsamp, int h, int w, int shortcut_pass) {
   long long bsz = (long long)b * b;
   long long total = (long long)count * c * bsz;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
@@ -479,9 +482,10 @@ __global__ void k_residual(const float* __restrict__ blocks, int count, int c, i
     int rem = static_cast<int>(q - i * c * bsz);
     int ch = rem / static_cast<int>(bsz);
     int cell = rem - ch * static_cast<int>(bsz);
-    int y = idx[3 * i + 1] + cell / b, xx = idx[3 * i + 2] + cell % b;
-    if (y >= h || xx >= w) continue;
-    size_t p = (((size_t)idx[3 * i] * c + ch) * h + y) * w + xx;
+    const int n = idx[3 * i], y0 = idx[3 * i + 1], x0 = idx[3 * i + 2];
+    int y = y0 + cell / b, xx = x0 + cell % b;
+    if (y >= h || xx >= w || n < 0 || n >= nsamp || y0 < 0 || x0 < 0) continue;  // never out of the tensor
+    size_t p = (((size_t)n * c + ch) * h + y) * w + xx;
     float v = blocks[q];
     out[p] = shortcut_pass ? __fadd_rn(out[p], __fsub_rn(v, orig_sc[p])) : __fadd_rn(v, orig_sc[p]);
   }
@@ -630,7 +634,7 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
   const ChunkPlan cp = chunk_plan(c, b);
   const long long items = static_cast<long long>((count + cp.T - 1) / cp.T) * ((c + cp.cpi - 1) / cp.cpi);
   k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
-      blocks, count, c, b, idx, base, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0);
+      blocks, count, c, b, idx, base, n, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0);
   after_launch("k_scatter");
 }
 
@@ -694,11 +698,11 @@ void op_scatter_gather(const float* blocks, int count, int pb, const float* orig
 }
 
 void op_residual_pass(const float* blocks, int count, int c, int b, const int32_t* idx,
-                      const float* orig_sc, float* out, int h, int w, bool shortcut_pass,
+                      const float* orig_sc, float* out, int n, int h, int w, bool shortcut_pass,
                       cudaStream_t st) {
   if (count == 0) return;
   k_residual<<<grid_for((long long)count * c * b * b), kThreads, 0, st>>>(
-      blocks, count, c, b, idx, orig_sc, out, h, w, shortcut_pass ? 1 : 0);
+      blocks, count, c, b, idx, orig_sc, out, n, h, w, shortcut_pass ? 1 : 0);
   after_launch("k_residual");
 }
 

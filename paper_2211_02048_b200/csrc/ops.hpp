@@ -28,7 +28,7 @@ void op_scatter_gather(const float* blocks, int count, int pb, const float* orig
                        int ccount, int cb, int ch, int cw, int k, int s, const DevEpilogue& epi,
                        float* out, cudaStream_t st);
 void op_residual_pass(const float* blocks, int count, int c, int b, const int32_t* idx,
-                      const float* orig_sc, float* out, int h, int w, bool shortcut_pass,
+                      const float* orig_sc, float* out, int n, int h, int w, bool shortcut_pass,
                       cudaStream_t st);
 void op_combine(const float* a, const float* b, float sign, size_t n, float* out, cudaStream_t st);
 void op_epilogue_blocks(float* blocks, int count, int c, int bh, const int32_t* idx,

@@ -361,3 +361,27 @@ def test_conv_rejects_unknown_math_mode():
         sb.conv_on_blocks(g, w, None, 1, 6, math=7)
     with pytest.raises(sb.ConfigError, match="conv2d: unknown math mode -1"):
         sb.conv2d(g, w, None, math=-1)
+
+
+def test_scatter_rejects_incompatible_indices_like_reference():
+    """require_scatter_compatible (kernels.cpp:18-35) / require_join_compatible
+    (:276-287) messages; the kernels themselves never write outside the tensor."""
+    base = cu(np.zeros((1, 2, 12, 12), np.float32))
+    blocks = cu(np.ones((2, 2, 6, 6), np.float32))
+    bad_n = cu(np.array([[0, 0, 0], [1, 6, 6]], np.int32))
+    with pytest.raises(sb.ConfigError, match="scatter: block sample out of range"):
+        sb.scatter_inplace(blocks, bad_n, base)
+    with pytest.raises(sb.ConfigError, match="scatter_add: block sample out of range"):
+        sb.scatter_add_inplace(blocks, bad_n, base)
+    with pytest.raises(sb.ConfigError, match="scatter: channel mismatch"):
+        sb.scatter(cu(np.ones((2, 3, 6, 6), np.float32)), cu(np.zeros((2, 3), np.int32)), base)
+    with pytest.raises(sb.ConfigError, match=r"scatter: index resolution 6x6 does not match tensor \(1, 2, 12, 12\)"):
+        sb.scatter(blocks, cu(np.zeros((2, 3), np.int32)), base, idx_hw=(6, 6))
+    with pytest.raises(sb.ConfigError, match=r"block_residual\(main\): block sample out of range"):
+        sb.scatter_with_block_residual(blocks, bad_n, blocks, cu(np.zeros((2, 3), np.int32)), base, base)
+    # straight through the ABI (no wrapper checks): the out-of-range block is skipped
+    t = cu(np.zeros((1, 2, 12, 12), np.float32))
+    assert sb._lib().sige_scatter_inplace(blocks.data_ptr(), 2, 2, 6, bad_n.data_ptr(), t.data_ptr(), 1, 2, 12, 12,
+                                          torch.cuda.current_stream().cuda_stream) == 0
+    got = host(t)
+    assert got[0, :, :6, :6].min() == 1.0 and got[0, :, 6:, 6:].max() == 0.0

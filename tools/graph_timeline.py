@@ -77,5 +77,9 @@ for i, (s_, en, wd, gi) in enumerate(rows):
         if v == v:
             acc[j] = acc.get(j, 0.0) + v
 print("sums " + " ".join(f"{acc.get(j, 0.0):7.1f}" for j in range(6)))
+import json
+with open(os.environ.get("SIGE_TL_MARKS_OUT", "gpurun_out/tl_marks.json"), "w") as f:
+    json.dump([{"slot": gi, "start": s_, "end": en, "wait": wd,
+                "marks": {k: marks[gi * 64 + k] for k in range(64) if marks[gi * 64 + k]}} for (s_, en, wd, gi) in rows], f)
 print(f"sum work {tot_work:.1f} us, sum handoff (incl. non-conv kernels) {tot_hand:.1f} us, "
       f"first->last {(rows[-1][1] - t0) / 1e3:.1f} us")
