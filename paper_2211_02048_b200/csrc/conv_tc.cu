@@ -124,6 +124,15 @@ struct TcParams {
   const char* pf_ptr;       // next conv's packed weights (L2 prefetch), or nullptr
   long long pf_bytes;
   unsigned long long* gtl_marks;  // SIGE_TC_GTL: CTA 0's phase marks per launch (64 slots), or nullptr
+  // Conv -> conv handoff without waiting for grid completion: every CTA
+  // bumps sig_ctr once its global writes are fenced; a conv whose predecessor
+  // in the stream is a conv spins on that counter (wait_ctr >= wait_target,
+  // the predecessor's grid size) instead of griddepcontrol.wait, so the
+  // predecessor's teardown (cluster sync, TMEM dealloc, exit, grid drain)
+  // overlaps this layer. nullptr: plain programmatic dependent launch.
+  unsigned int* sig_ctr;
+  const unsigned int* wait_ctr;
+  unsigned int wait_target;
 };
 
 // ------------------------------------------------------------- PTX ------
@@ -279,6 +288,19 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The dependency wait of a conv launch (see TcParams::wait_ctr).
+__device__ __forceinline__ void dep_wait(const unsigned int* ctr, unsigned int target) {
+  if (!ctr) {
+    pdl_wait();
+    return;
+  }
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(40);
+  }
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // One lane of a converged warp (tcgen05.mma / commit are single-thread
 // instructions; the warp computes the descriptors uniformly).
@@ -1231,7 +1253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // before the previous conv started); the activations and GroupNorm
         // statistics below were produced by the previous kernel.
         if (threadIdx.x == 0) tl_mark(p, 54);
-        pdl_wait();  // the source / GroupNorm statistics were written by the previous kernel
+        dep_wait(p.wait_ctr, p.wait_target);  // the source / GroupNorm statistics were written by the previous kernel
         if (threadIdx.x == 0 && p.gtl) {
           unsigned long long t;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1377,7 +1399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // A CTA without items still orders its completion after the previous
     // grid's (the next kernel's dependency wait relies on this transitively).
-    if (it == 0) pdl_wait();
+    if (it == 0) dep_wait(p.wait_ctr, p.wait_target);
     // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kEpiBase / 32) {
@@ -1413,7 +1435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // into the instruction caches off the critical path (measured: a CTA's
     // first item paid ~1-3 us more than its second for the same work).
     bool dry = p.warm && cid < n_items;
-    if (!dry) pdl_wait();  // the destination / residual inputs were written by earlier kernels
+    if (!dry) dep_wait(p.wait_ctr, p.wait_target);  // the destination / residual inputs were written by earlier kernels
     for (int item = cid; item < n_items;) {
       const int mi = static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices), ni = item - mi * n_slices;
       const int g = mi * p.T + t;
@@ -1590,7 +1612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (dry) {
         dry = false;
-        pdl_wait();
+        dep_wait(p.wait_ctr, p.wait_target);
         continue;
       }
       if (threadIdx.x == kEpiBase && it < 2) tl_mark(p, it ? 57 : 47);
@@ -1757,7 +1779,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tl_clock(p, 61);
   }
   tc_fence_before();
+  if (p.sig_ctr) __threadfence();  // this thread's global writes, before the CTA's signal
   __syncthreads();
+  if (p.sig_ctr && threadIdx.x == 0)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sig_ctr) : "memory");
   if (p.ks > 1) cluster_sync();  // no CTA leaves while a peer may still touch its shared memory
   if (threadIdx.x == 0 && p.gtl) {
     unsigned long long t;
@@ -1941,15 +1966,19 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
   }
 }
 
-void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                    cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad,
-                    const void* pf_ptr, size_t pf_bytes) {
+int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
+                   cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad,
+                   const void* pf_ptr, size_t pf_bytes, unsigned int* sig_ctr, const unsigned int* wait_ctr,
+                   unsigned int wait_target) {
   static_assert(kGtlLaunchesDev == kTimelineSlots, "timeline layout");
   const int sms_all = sm_count();
   const int sms_use = sm_budget > 0 ? std::min(sm_budget, sms_all) : sms_all;
   if (!cw.w_tc) throw ConfigError("conv (tensor core): weights were not packed for this path");
-  if (tiles.capacity == 0) return;
+  if (tiles.capacity == 0) return 0;
   TcParams p{};
+  p.sig_ctr = sig_ctr;
+  p.wait_ctr = wait_ctr;
+  p.wait_target = wait_target;
   p.src = src;
   // Transform mode (F16): the fp16 twin streams by cp.async and the pending
   // chain — [scale-shift, act] or GroupNorm-from-statistics then act — is
@@ -2220,6 +2249,8 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
       if (tunable) {
         double* const gn_saved = p.dst.gn_stats;
         p.dst.gn_stats = nullptr;  // trials must not accumulate statistics
+        p.sig_ctr = nullptr;       // nor signal the next conv (they run to completion here)
+        p.wait_ctr = nullptr;
         cudaEvent_t e0, e1;
         SIGE_CUDA(cudaEventCreate(&e0));
         SIGE_CUDA(cudaEventCreate(&e1));
@@ -2252,6 +2283,8 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
         SIGE_CUDA(cudaEventDestroy(e0));
         SIGE_CUDA(cudaEventDestroy(e1));
         p.dst.gn_stats = gn_saved;
+        p.sig_ctr = sig_ctr;
+        p.wait_ctr = wait_ctr;
         std::lock_guard<std::mutex> g(plans_mu);
         plans[key] = {nt_plan, ks_plan};
       }
@@ -2332,6 +2365,7 @@ void launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const D
       std::fprintf(stderr, "\n");
     }
   }
+  return grid;
 }
 
 }  // namespace sige_b200

@@ -216,11 +216,19 @@ class Engine {
   // so conv i prefetches conv i+1's weights while it runs.
   std::vector<WRef>* seq_ = nullptr;  // the running call's sequence (nullptr: none)
   mutable size_t seq_next_ = 0;
+  // Counter handoff between consecutive tensor-core convs of a sparse call
+  // (TcParams::sig_ctr): one counter per conv launch, zeroed at call start.
+  static constexpr int kMaxCallConvs = 1024;
+  unsigned int* cur_ctrs_ = nullptr;
+  mutable const unsigned int* prev_ctr_ = nullptr;  // the last conv's counter ...
+  mutable unsigned int prev_grid_ = 0;               // ... its grid ...
+  mutable uint64_t prev_mark_ = ~0ull;               // ... and the launch count right after it
   bool timeline_ = false;
   unsigned long long* tl_buf_ = nullptr;
   mutable int tl_next_ = 0;
   mutable std::vector<TlMeta> tl_meta_;
   void timeline_reset();
+  void record_handoff(unsigned int* sig, int grid) const;
   void drop_graphs();
   mutable std::vector<cudaEvent_t> ev_pool_;
   // per-call bindings read by program steps
