@@ -280,6 +280,21 @@ int sige_engine_precompute(sige_engine* eng, const float* original, int step,
  * sparse_forward fails with the reference's check_cache_model ConfigError
  * when it differs from the engine model's (graph.cpp:596-603). */
 int sige_engine_drop_step(sige_engine* eng, int step);
+/* Multi-step caches in host memory: offload_step copies one
+ * step's entries to pinned host memory (kept as the step's home; the cache is
+ * immutable after precompute) and frees their device memory; prefetch_step
+ * uploads them again asynchronously on `stream` — order the step's next
+ * sparse_forward after it. A sparse_forward on an offloaded step fails with the
+ * reference's "precompute required" ConfigError. */
+int sige_engine_offload_step(sige_engine* eng, int step, sige_stream_t stream);
+int sige_engine_prefetch_step(sige_engine* eng, int step, sige_stream_t stream);
+/* output_coverage (graph.hpp:190-192, graph.cpp:1078-1129) on the device: the
+ * out_h x out_w u8 map (device buffer) of output pixels a sparse_forward of
+ * this edit may change — computed from the same on-device IndexPlan the
+ * executor runs (mask = NULL: difference against the cached original). */
+int sige_engine_output_coverage(sige_engine* eng, const float* edited, const uint8_t* mask,
+                                const sige_run_config* cfg, uint8_t* out, int* out_h, int* out_w,
+                                sige_stream_t stream);
 int sige_engine_refresh_step(sige_engine* eng, const float* original, int step, sige_stream_t stream);
 int sige_engine_cache_model_hash(const sige_engine* eng, uint64_t* cache_hash, uint64_t* model_hash);
 int sige_engine_set_cache_model_hash(sige_engine* eng, uint64_t cache_hash);

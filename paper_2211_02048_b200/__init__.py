@@ -549,6 +549,29 @@ class Engine:
         o = self._check_input(original, "precompute")
         _check(_lib().sige_engine_precompute(self.h, o.data_ptr(), step, _stream()))
 
+    def output_coverage(self, edited: torch.Tensor | None = None, mask: torch.Tensor | None = None,
+                        config: RunConfig | None = None) -> torch.Tensor:
+        """output_coverage (graph.cpp:1078-1129) of an edit on the device: (out_h, out_w) uint8."""
+        e = self._check_input(edited, "output_coverage") if edited is not None else None
+        m = self._check_mask(mask, "output_coverage") if mask is not None else None
+        _, oc, oh, ow = self.output_shape()
+        dev = (e if e is not None else m).device
+        out = torch.empty((oh, ow), dtype=torch.uint8, device=dev)
+        h, w = C.c_int(0), C.c_int(0)
+        cfg = config or default_config()
+        _check(_lib().sige_engine_output_coverage(self.h, e.data_ptr() if e is not None else None,
+                                                  m.data_ptr() if m is not None else None, C.byref(cfg),
+                                                  out.data_ptr(), C.byref(h), C.byref(w), _stream()))
+        return out
+
+    def offload_step(self, step: int) -> None:
+        """Move one step's cache entries to pinned host memory, freeing their device memory."""
+        _check(_lib().sige_engine_offload_step(self.h, step, _stream()))
+
+    def prefetch_step(self, step: int) -> None:
+        """Upload an offloaded step again, asynchronously on the current stream."""
+        _check(_lib().sige_engine_prefetch_step(self.h, step, _stream()))
+
     def drop_step(self, step: int) -> None:
         """ActivationCache::drop_step (graph.cpp:271-274): erase (and free) one step's entries."""
         _check(_lib().sige_engine_drop_step(self.h, step))

@@ -193,6 +193,9 @@ SYMBOLS = {
     "sige_engine_profile_read": (_i, [_vp, _vp, _i, C.POINTER(_i), _vp]),
     "sige_engine_set_timeline": (_i, [_vp, _i]),
     "sige_engine_drop_step": (_i, [_vp, _i]),
+    "sige_engine_offload_step": (_i, [_vp, _i, _vp]),
+    "sige_engine_prefetch_step": (_i, [_vp, _i, _vp]),
+    "sige_engine_output_coverage": (_i, [_vp, _vp, _vp, C.POINTER(RunConfig), _vp, C.POINTER(_i), C.POINTER(_i), _vp]),
     "sige_engine_refresh_step": (_i, [_vp, _vp, _i, _vp]),
     "sige_engine_cache_model_hash": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "sige_engine_set_cache_model_hash": (_i, [_vp, _u64]),

@@ -523,6 +523,38 @@ int sige_engine_precompute(sige_engine* eng, const float* original, int step, si
   });
 }
 
+int sige_engine_output_coverage(sige_engine* eng, const float* edited, const uint8_t* mask,
+                                const sige_run_config* cfg, uint8_t* out, int* out_h, int* out_w, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    need(out, "output_coverage");
+    if (!edited && !mask) throw ConfigError("output_coverage: needs the edited input or a mask");
+    sige_run_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      sige_run_config_default(&c);
+    int oh = 0, ow = 0;
+    eng->impl->output_coverage(edited, mask, c, out, &oh, &ow, as_stream(s));
+    if (out_h) *out_h = oh;
+    if (out_w) *out_w = ow;
+  });
+}
+
+int sige_engine_offload_step(sige_engine* eng, int step, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    eng->impl->offload_step(step, as_stream(s));
+  });
+}
+
+int sige_engine_prefetch_step(sige_engine* eng, int step, sige_stream_t s) {
+  return guarded([&] {
+    need(eng, "engine");
+    eng->impl->prefetch_step(step, as_stream(s));
+  });
+}
+
 int sige_engine_drop_step(sige_engine* eng, int step) {
   return guarded([&] {
     need(eng, "engine");

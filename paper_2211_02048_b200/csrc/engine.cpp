@@ -1,6 +1,7 @@
 // engine.cpp — device ActivationCache, dense walk (precompute / dense_forward)
 // and the compiled sparse_forward executor. See engine.hpp.
 #include "engine.hpp"
+#include "ops.hpp"
 
 #include <algorithm>
 #include <cstdio>
@@ -187,6 +188,14 @@ Engine::~Engine() {
   if (fork_ev_) cudaEventDestroy(fork_ev_);
   if (join_ev_) cudaEventDestroy(join_ev_);
   for (void* p : allocations_) cudaFree(p);
+  for (auto& kv : host_cache_) {
+    cudaFreeHost(kv.second.host);
+    if (kv.second.host16) cudaFreeHost(kv.second.host16);
+  }
+  for (auto& kv : host_norms_) {
+    cudaFreeHost(kv.second.scale);
+    cudaFreeHost(kv.second.shift);
+  }
 }
 
 void* Engine::alloc(size_t bytes) {
@@ -747,6 +756,7 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
 void Engine::precompute(const float* original, int step, cudaStream_t st) {
   cache_model_hash_ = structure_hash_;  // precompute (graph.cpp:426-435)
   invalidate_programs();
+  free_host_step(step);  // an offloaded copy of this step is stale now
   DevTensor& in = cache_slot(step, "input", in_c_, in_h_, in_w_, kNCHW);
   SIGE_CUDA(cudaMemcpyAsync(in.p, original, in.numel() * sizeof(float), cudaMemcpyDeviceToDevice, st));
   dense_walk(plain(in), step, /*capture=*/true, /*reused=*/false, nullptr, st);
@@ -793,6 +803,7 @@ void Engine::put_tensor(int step, const std::string& key, const float* host, siz
                       std::to_string(static_cast<size_t>(batch_) * c * h * w) + " values");
   invalidate_programs();
   drop_act(step);
+  free_host_step(step);
   const int layout = is_nchw_key(key) ? kNCHW : kNHWC;
   DevTensor& t = cache_slot(step, key, c, h, w, layout);
   std::vector<float> buf(numel);
@@ -816,6 +827,7 @@ void Engine::put_tensor(int step, const std::string& key, const float* host, siz
 void Engine::put_norm(int step, const std::string& key, const float* sc, const float* sh, size_t np) {
   invalidate_programs();
   drop_act(step);
+  free_host_step(step);
   DevNorm& n = norm_slot(step, key, static_cast<int>(np));
   SIGE_CUDA(cudaMemcpy(n.scale, sc, np * sizeof(float), cudaMemcpyHostToDevice));
   SIGE_CUDA(cudaMemcpy(n.shift, sh, np * sizeof(float), cudaMemcpyHostToDevice));
@@ -1390,7 +1402,12 @@ void Engine::release(void* p) {
 }
 
 void Engine::drop_step(int step) {  // ActivationCache::drop_step (graph.cpp:271-274)
-  invalidate_programs();            // programs and captured graphs point into the dropped entries
+  free_device_step(step);
+  free_host_step(step);  // an offloaded copy goes too
+}
+
+void Engine::free_device_step(int step) {
+  invalidate_programs();  // programs and captured graphs point into the dropped entries
   for (auto it = cache_.begin(); it != cache_.end();) {
     if (it->first.first != step) {
       ++it;
@@ -1411,6 +1428,93 @@ void Engine::drop_step(int step) {  // ActivationCache::drop_step (graph.cpp:271
   }
 }
 
+void Engine::free_host_step(int step) {
+  for (auto it = host_cache_.begin(); it != host_cache_.end();) {
+    if (it->first.first != step) {
+      ++it;
+      continue;
+    }
+    cudaFreeHost(it->second.host);
+    if (it->second.host16) cudaFreeHost(it->second.host16);
+    it = host_cache_.erase(it);
+  }
+  for (auto it = host_norms_.begin(); it != host_norms_.end();) {
+    if (it->first.first != step) {
+      ++it;
+      continue;
+    }
+    cudaFreeHost(it->second.scale);
+    cudaFreeHost(it->second.shift);
+    it = host_norms_.erase(it);
+  }
+}
+
+// The host copy is the step's home once offloaded (the cache is immutable
+// after precompute); a later offload of the same, unchanged step only frees
+// the device memory again.
+void Engine::offload_step(int step, cudaStream_t st) {
+  bool any = false;
+  for (auto& kv : cache_) {
+    if (kv.first.first != step) continue;
+    any = true;
+    if (host_cache_.count(kv.first)) continue;  // host copy already current
+    const DevTensor& t = kv.second;
+    HostEntry& h = host_cache_[kv.first];
+    h.meta = t;
+    h.meta.p = nullptr;
+    h.meta.h16 = nullptr;
+    SIGE_CUDA(cudaMallocHost(&h.host, std::max<size_t>(t.bytes(), 16)));
+    SIGE_CUDA(cudaMemcpyAsync(h.host, t.p, t.bytes(), cudaMemcpyDeviceToHost, st));
+    if (t.h16) {
+      SIGE_CUDA(cudaMallocHost(&h.host16, std::max<size_t>(t.numel() * 2, 16)));
+      SIGE_CUDA(cudaMemcpyAsync(h.host16, t.h16, t.numel() * 2, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  for (auto& kv : norms_) {
+    if (kv.first.first != step || host_norms_.count(kv.first)) continue;
+    HostNorm& h = host_norms_[kv.first];
+    h.np = kv.second.np;
+    SIGE_CUDA(cudaMallocHost(&h.scale, std::max<size_t>(h.np * sizeof(float), 16)));
+    SIGE_CUDA(cudaMallocHost(&h.shift, std::max<size_t>(h.np * sizeof(float), 16)));
+    SIGE_CUDA(cudaMemcpyAsync(h.scale, kv.second.scale, h.np * sizeof(float), cudaMemcpyDeviceToHost, st));
+    SIGE_CUDA(cudaMemcpyAsync(h.shift, kv.second.shift, h.np * sizeof(float), cudaMemcpyDeviceToHost, st));
+  }
+  if (!any) throw ConfigError("offload_step: no cache entry for step " + std::to_string(step));
+  SIGE_CUDA(cudaStreamSynchronize(st));  // the copies landed: the device memory can go
+  free_device_step(step);
+}
+
+// Asynchronous on `st`: the H2D copies overlap whatever runs on other streams
+// (PAPER.md:389); the step's sparse_forward must be ordered after them.
+void Engine::prefetch_step(int step, cudaStream_t st) {
+  bool any = false;
+  for (auto& kv : host_cache_) {
+    if (kv.first.first != step) continue;
+    any = true;
+    const HostEntry& h = kv.second;
+    if (cache_.count(kv.first)) continue;  // already resident
+    DevTensor& t = cache_slot(step, kv.first.second, h.meta.c, h.meta.h, h.meta.w, h.meta.layout, h.meta.half);
+    SIGE_CUDA(cudaMemcpyAsync(t.p, h.host, t.bytes(), cudaMemcpyHostToDevice, st));
+    if (h.host16) {
+      if (!t.h16) t.h16 = alloc(t.numel() * 2);
+      SIGE_CUDA(cudaMemcpyAsync(t.h16, h.host16, t.numel() * 2, cudaMemcpyHostToDevice, st));
+    }
+  }
+  for (auto& kv : host_norms_) {
+    if (kv.first.first != step || norms_.count(kv.first)) continue;
+    DevNorm& n = norm_slot(step, kv.first.second, kv.second.np);
+    SIGE_CUDA(cudaMemcpyAsync(n.scale, kv.second.scale, kv.second.np * sizeof(float), cudaMemcpyHostToDevice, st));
+    SIGE_CUDA(cudaMemcpyAsync(n.shift, kv.second.shift, kv.second.np * sizeof(float), cudaMemcpyHostToDevice, st));
+  }
+  if (!any) throw ConfigError("prefetch_step: step " + std::to_string(step) + " was not offloaded");
+}
+
+bool Engine::step_offloaded(int step) const {
+  for (auto& kv : host_cache_)
+    if (kv.first.first == step && !cache_.count(kv.first)) return true;
+  return false;
+}
+
 void Engine::refresh_step(const float* original, int step, cudaStream_t st) {  // graph.cpp:437-444
   drop_step(step);
   precompute(original, step, st);
@@ -1420,6 +1524,108 @@ void Engine::set_sm_budget(int sms) {
   if (sms < 0) throw ConfigError("engine: SM budget must be >= 0");
   if (sms != sm_budget_) invalidate_programs();  // captured launches carry the old grids
   sm_budget_ = sms;
+}
+
+// output_coverage (graph.cpp:1078-1129) on the device: the output pixels a
+// sparse_forward with this mask / config may change — the same layer walk over
+// the same on-device IndexPlan the executor uses (tile footprints of sparse
+// layers, dilation / downsample / 2x upsample of the running coverage for
+// dense ones, everything for fresh-statistics norms). A cross-check of the
+// executor's coverage against the reference's (tests/test_gpu_engine.py).
+void Engine::output_coverage(const float* edited, const uint8_t* mask, const sige_run_config& cfg, uint8_t* out,
+                             int* oh, int* ow, cudaStream_t st) {
+  if (cfg.mask_threshold < 0.0f) throw ConfigError("config: threshold must be >= 0");
+  if (cfg.dilate_full < 0 || cfg.dilate_scale < 0) throw ConfigError("config: dilation radii must be >= 0");
+  if (cfg.block3 < 1 || cfg.block1 < 1) throw ConfigError("config: block sizes must be >= 1");
+  *oh = out_h_;
+  *ow = out_w_;
+  Program& P = program(cfg, false);
+  size_t cap = static_cast<size_t>(in_h_) * in_w_;
+  for (const LayerShape& sh : shapes_) cap = std::max(cap, static_cast<size_t>(sh.h_out) * sh.w_out);
+  uint8_t* a = static_cast<uint8_t*>(alloc(cap));
+  uint8_t* b = static_cast<uint8_t*>(alloc(cap));
+  uint8_t* t = static_cast<uint8_t*>(alloc(cap));
+  struct Free {
+    Engine* e;
+    std::vector<void*> p;
+    ~Free() {
+      cudaDeviceSynchronize();
+      for (void* q : p) e->release(q);
+    }
+  } fr{this, {a, b, t}};
+  SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t), st));
+  if (mask) {
+    launch_mask_u8_to_bits(mask, in_h_, in_w_, P.bits, P.any, st);
+    SIGE_CUDA(cudaMemcpyAsync(a, mask, static_cast<size_t>(in_h_) * in_w_, cudaMemcpyDeviceToDevice, st));
+  } else {
+    const DevTensor& orig = cache_tensor(cfg.step, "input");
+    launch_mask_bits(orig.p, edited, batch_, in_c_, in_h_, in_w_, cfg.mask_threshold, P.bits, a, P.any, st);
+  }
+  int h = in_h_, w = in_w_;
+  auto entry = [&](int eh, int ew, int eb) -> const PlanEntryDev& {
+    for (const PlanEntryDev& e : P.entries)
+      if (e.h == eh && e.w == ew && e.b == eb) return e;
+    throw ConfigError("output_coverage: no plan entry for " + std::to_string(eh) + "x" + std::to_string(ew));
+  };
+  auto footprint = [&](const PlanEntryDev& e, bool clear) {
+    if (clear) SIGE_CUDA(cudaMemsetAsync(a, 0, static_cast<size_t>(e.h) * e.w, st));
+    op_cov_footprint(e.idx, e.count, e.capacity, e.b, e.h, e.w, a, st);
+  };
+  auto dilate = [&](int r) {
+    if (r <= 0) return;
+    op_dilate_mask(a, h, w, r, b, t, st);
+    std::swap(a, b);
+  };
+  if (cfg.sparse) {
+    launch_plan(P.bits, in_h_, in_w_, cfg.dilate_full, cfg.dilate_scale, batch_, P.entries_dev,
+                static_cast<int>(P.entries.size()), st);
+    dilate(cfg.dilate_full);
+    for (size_t i = 0; i < layers_.size(); ++i) {
+      const LayerDev& L = layers_[i];
+      const LayerShape& s = shapes_[i];
+      const bool sp = runs_sparse(L, s.h_in, s.w_in, cfg);
+      switch (L.kind) {
+        case SIGE_LAYER_CONV:
+        case SIGE_LAYER_DOWNSAMPLE:
+          if (sp) {
+            footprint(entry(s.h_out, s.w_out, L.conv.k == 3 ? cfg.block3 : cfg.block1), true);
+          } else {
+            dilate((L.conv.k - 1) / 2);
+            if (L.conv.stride == 2) {
+              op_downsample_mask(a, h, w, s.h_out, s.w_out, b, st);
+              std::swap(a, b);
+            }
+          }
+          break;
+        case SIGE_LAYER_NORM:
+          if (L.norm_kind != SIGE_NORM_BATCH && !cfg.norm_precompute)
+            SIGE_CUDA(cudaMemsetAsync(a, 1, static_cast<size_t>(s.h_out) * s.w_out, st));
+          break;
+        case SIGE_LAYER_UPSAMPLE:
+          op_cov_up2(a, h, w, b, st);
+          std::swap(a, b);
+          break;
+        case SIGE_LAYER_RESBLOCK:
+          if (sp) {
+            footprint(entry(s.h_out, s.w_out, cfg.block3), true);
+            footprint(entry(s.h_out, s.w_out, cfg.block1), false);
+          } else {
+            dilate(2);
+            if (L.norm_kind != SIGE_NORM_BATCH && !cfg.norm_precompute)
+              SIGE_CUDA(cudaMemsetAsync(a, 1, static_cast<size_t>(s.h_out) * s.w_out, st));
+          }
+          break;
+        default:
+          break;
+      }
+      h = s.h_out;
+      w = s.w_out;
+    }
+  }
+  const long long n = static_cast<long long>(out_h_) * out_w_;
+  op_cov_final(a, n, P.any, cfg.sparse ? 0 : 1, st);  // empty mask -> nothing; dense -> everything
+  if (!cfg.sparse) op_cov_final(a, n, P.any, 0, st);
+  SIGE_CUDA(cudaMemcpyAsync(out, a, n, cudaMemcpyDeviceToDevice, st));
 }
 
 int Engine::trace(uint64_t* rows, int cap, cudaStream_t st) {

@@ -81,6 +81,14 @@ class Engine {
   // against a cache built for another model (check_cache_model, graph.cpp:596-603).
   void drop_step(int step);
   void refresh_step(const float* original_nchw, int step, cudaStream_t st);
+  // Multi-step caches in host memory ("store the activations in
+  // CPU memory and load the on-demand ones on GPU"): offload_step moves one
+  // step's entries to pinned host memory and frees their device memory;
+  // prefetch_step brings them back asynchronously on `st` (the caller orders
+  // the step's next sparse_forward after it, e.g. with an event).
+  void offload_step(int step, cudaStream_t st);
+  void prefetch_step(int step, cudaStream_t st);
+  bool step_offloaded(int step) const;
   uint64_t structure_hash() const { return structure_hash_; }
   uint64_t cache_model_hash() const { return cache_model_hash_; }
   void set_cache_model_hash(uint64_t h) { cache_model_hash_ = h; }
@@ -100,6 +108,8 @@ class Engine {
   void output_shape(int* n, int* c, int* h, int* w) const;
   int last_launch_count() const { return last_launches_; }
   int trace(uint64_t* rows, int cap, cudaStream_t st);
+  void output_coverage(const float* edited, const uint8_t* mask, const sige_run_config& cfg, uint8_t* out, int* oh,
+                       int* ow, cudaStream_t st);
   size_t cache_bytes() const;
   void set_profiling(bool on);
   void set_graphs(bool on);
@@ -177,6 +187,18 @@ class Engine {
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
 
   std::string name_;
+  struct HostEntry {  // an offloaded cache entry (pinned host copies)
+    DevTensor meta;     // shape / layout (device pointers unset)
+    void* host = nullptr;
+    void* host16 = nullptr;  // fp16 twin, if the entry had one
+  };
+  struct HostNorm {
+    int np = 0;
+    float* scale = nullptr;  // pinned, np each
+    float* shift = nullptr;
+  };
+  std::map<std::pair<int, std::string>, HostEntry> host_cache_;
+  std::map<std::pair<int, std::string>, HostNorm> host_norms_;
   uint64_t structure_hash_ = 0;     // of the engine's model
   uint64_t cache_model_hash_ = 0;   // of the model the cache was built for
   int batch_, math_, in_c_, in_h_, in_w_;
@@ -236,6 +258,8 @@ class Engine {
   float* cur_out_ = nullptr;
   void* alloc(size_t bytes);
   void release(void* p);  // frees an alloc() block early (dropped cache entries)
+  void free_device_step(int step);
+  void free_host_step(int step);
 };
 
 }  // namespace sige_b200

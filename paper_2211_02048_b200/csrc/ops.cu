@@ -753,4 +753,51 @@ void op_expf_sweep(uint32_t first, long long count, int mode, float* out, cudaSt
   after_launch("k_expf_sweep");
 }
 
+// ---- output_coverage (graph.cpp:1078-1129) building blocks on the device --
+// footprint: the clipped tile rectangles of sample 0 (graph.cpp:1047-1060)
+// OR-ed into m (h x w, zeroed by the caller); tile list + device count.
+__global__ void k_cov_footprint(const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int b, int h,
+                                int w, uint8_t* __restrict__ m) {
+  const int cnt = *count;
+  const long long total = static_cast<long long>(cnt) * b * b;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int g = static_cast<int>(q / (b * b)), cell = static_cast<int>(q - static_cast<long long>(g) * b * b);
+    if (idx[3 * g] != 0) continue;  // sample 0 only
+    const int y = idx[3 * g + 1] + cell / b, x = idx[3 * g + 2] + cell % b;
+    if (y < h && x < w) m[static_cast<size_t>(y) * w + x] = 1;
+  }
+}
+// upsample_mask2x (graph.cpp:1068-1074)
+__global__ void k_cov_up2(const uint8_t* __restrict__ m, int h, int w, uint8_t* __restrict__ out) {
+  const long long total = 4LL * h * w;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int y = static_cast<int>(q / (2 * w)), x = static_cast<int>(q - static_cast<long long>(y) * 2 * w);
+    out[q] = m[static_cast<size_t>(y / 2) * w + x / 2];
+  }
+}
+// the empty-mask / dense cases (graph.cpp:1083-1085): value = any ? 1 : 0, or fill
+__global__ void k_cov_final(uint8_t* m, long long n, const int32_t* __restrict__ any, int mode) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    if (mode == 1) m[q] = 1;             // not sparse: everything can change
+    else if (!*any) m[q] = 0;            // empty mask: nothing changes
+  }
+}
+
+void op_cov_footprint(const int32_t* idx, const int32_t* count, int capacity, int b, int h, int w, uint8_t* m,
+                      cudaStream_t st) {
+  if (capacity == 0) return;
+  k_cov_footprint<<<grid_for(static_cast<long long>(capacity) * b * b), kThreads, 0, st>>>(idx, count, b, h, w, m);
+  after_launch("k_cov_footprint");
+}
+void op_cov_up2(const uint8_t* m, int h, int w, uint8_t* out, cudaStream_t st) {
+  k_cov_up2<<<grid_for(4LL * h * w), kThreads, 0, st>>>(m, h, w, out);
+  after_launch("k_cov_up2");
+}
+void op_cov_final(uint8_t* m, long long n, const int32_t* any, int mode, cudaStream_t st) {
+  k_cov_final<<<grid_for(n), kThreads, 0, st>>>(m, n, any, mode);
+  after_launch("k_cov_final");
+}
+
 }  // namespace sige_b200

@@ -41,6 +41,10 @@ void op_gather_spade(const float* x, const float* gamma, const float* beta, int 
                      const int32_t* idx, int count, int b, int ih, int iw, int k, int s, const DevEpilogue& epi,
                      int act, float* out, cudaStream_t st);
 void op_resize_nearest(const float* in, int n, int c, int h, int w, int oh, int ow, float* out, cudaStream_t st);
+void op_cov_footprint(const int32_t* idx, const int32_t* count, int capacity, int b, int h, int w, uint8_t* m,
+                      cudaStream_t st);
+void op_cov_up2(const uint8_t* m, int h, int w, uint8_t* out, cudaStream_t st);
+void op_cov_final(uint8_t* m, long long n, const int32_t* any, int mode, cudaStream_t st);
 void op_expf_sweep(uint32_t first, long long count, int mode, float* out, cudaStream_t st);
 
 }  // namespace sige_b200

@@ -277,3 +277,94 @@ def test_cache_lifecycle_steps_and_model_guard(orc):
         run(b_edit, 0)
     eng.set_cache_model_hash(model_h)
     assert np.array_equal(run(b_edit, 0), want(b_orig, b_edit))
+
+
+COV_CASES = [
+    ("mini_unet_gn", "rect5", 1, 3, {}),
+    ("mini_unet_gn", "blob5", 2, 4, {"norm_precompute": 0}),
+    ("mini_unet_bn", "rect15", 1, 5, {"dilate_full": 3}),
+    ("gaugan_stack_in", "multi15", 1, 6, {}),
+    ("ddim_stack_64x32", "rect5", 1, 7, {"dilate_full": 5, "min_sparse_res": 16}),
+    ("ddim_stack_64x32", "rect1", 1, 8, {"dilate_full": 2, "min_sparse_res": 8, "block3": 4, "block1": 2}),
+    ("ddim_stack", "rect1", 1, 7, {"dilate_full": 5, "min_sparse_res": 64}),
+    ("mini_unet_gn", "rect5", 1, 9, {"sparse": 0}),
+]
+
+
+@pytest.mark.parametrize("case", COV_CASES, ids=[f"{c[0]}-{c[1]}-{i}" for i, c in enumerate(COV_CASES)])
+def test_output_coverage_matches_reference(orc, ref, case):
+    """Device output_coverage (graph.cpp:1078-1129) from the executor's own
+    on-device IndexPlan == the reference's, for the computed mask and for an
+    explicit (empty) mask; and the sparse output differs from the cache only
+    inside it."""
+    import ctypes as C
+
+    name, fx, n, seed, over = case
+    om = orc.model(name)
+    c, h, w = sb.Model(name).in_shape
+    orig, edited = orc.make_edit_fixture(fx, n, c, h, w, seed)
+    over = dict(over)
+    df = over.pop("dilate_full", None)
+    cfg = sb.default_config(dilate_full=om.required_dilation() if df is None else df, **over)
+    eng = sb.Engine(sb.Model(name), batch=n, math=sb.MATH_F16)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    mask = orc.difference_mask(orig, edited)
+    rm = ref.model(name)
+    oc, oh, ow = rm.output_shape()
+    want = np.zeros((oh, ow), np.uint8)
+    hh, ww = C.c_int(), C.c_int()
+    assert ref.lib.ref_output_coverage(rm.h, mask.ctypes.data, h, w, n, C.byref(cfg), want.ctypes.data,
+                                       C.byref(hh), C.byref(ww)) == 0
+    got = eng.output_coverage(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
+    assert np.array_equal(got, want)
+    got_m = eng.output_coverage(mask=torch.from_numpy(mask).cuda(), config=cfg).cpu().numpy()
+    assert np.array_equal(got_m, want)
+    empty = eng.output_coverage(mask=torch.zeros((h, w), dtype=torch.uint8, device="cuda"), config=cfg)
+    assert int(empty.sum()) == 0
+    out = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).cpu().numpy()
+    fin = eng.get_tensor("final", out.shape).numpy()
+    outside = np.broadcast_to(want[None, None] == 0, out.shape)
+    assert np.array_equal(out[outside], fin[outside])
+
+
+@pytest.mark.parametrize("math", [sb.MATH_EXACT, sb.MATH_F16])
+def test_offload_and_prefetch_steps(orc, math):
+    """Multi-step caches with host offload: an offloaded step's
+    device memory is freed, a call on it fails like a missing cache entry,
+    prefetch_step on a side stream brings it back and the call gives the same
+    bits as before; other steps are untouched."""
+    name = "mini_unet_gn"
+    om = orc.model(name)
+    a_orig, a_edit = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 71)
+    b_orig, b_edit = orc.make_edit_fixture("blob5", 1, 3, 64, 64, 72)
+    eng = sb.Engine(sb.Model(name), math=math)
+    eng.precompute(torch.from_numpy(a_orig).cuda(), step=0)
+    eng.precompute(torch.from_numpy(b_orig).cuda(), step=1)
+    cfg0 = sb.default_config(dilate_full=om.required_dilation(), step=0)
+    cfg1 = sb.default_config(dilate_full=om.required_dilation(), step=1)
+    xa, xb = torch.from_numpy(a_edit).cuda(), torch.from_numpy(b_edit).cuda()
+    want_a = eng.sparse_forward(xa, config=cfg0).cpu()
+    want_b = eng.sparse_forward(xb, config=cfg1).cpu()
+    full = eng.cache_bytes()
+    eng.offload_step(1)
+    assert eng.cache_bytes() < full
+    with pytest.raises(sb.ConfigError, match="precompute required"):
+        eng.sparse_forward(xb, config=cfg1)
+    assert torch.equal(eng.sparse_forward(xa, config=cfg0).cpu(), want_a)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        eng.prefetch_step(1)
+    torch.cuda.current_stream().wait_stream(side)
+    assert eng.cache_bytes() == full
+    for _ in range(3):  # direct, capture, replay
+        assert torch.equal(eng.sparse_forward(xb, config=cfg1).cpu(), want_b)
+    eng.offload_step(1)  # unchanged step: only the device copy goes
+    eng.prefetch_step(1)
+    assert torch.equal(eng.sparse_forward(xb, config=cfg1).cpu(), want_b)
+    with pytest.raises(sb.ConfigError, match="was not offloaded"):
+        eng.prefetch_step(5)
+    if math == sb.MATH_EXACT:
+        cache = om.precompute(b_orig)
+        want, _ = om.sparse_forward(cache, b_edit, orc.difference_mask(b_orig, b_edit),
+                                    sb.default_config(dilate_full=om.required_dilation()))
+        assert np.array_equal(want_b.numpy(), want)

@@ -385,3 +385,23 @@ def test_scatter_rejects_incompatible_indices_like_reference():
                                           torch.cuda.current_stream().cuda_stream) == 0
     got = host(t)
     assert got[0, :, :6, :6].min() == 1.0 and got[0, :, 6:, 6:].max() == 0.0
+
+
+@pytest.mark.parametrize("win_b,n,c,h,w", [(6, 2, 70, 36, 44), (2, 1, 5, 16, 12), (6, 1, 33, 20, 20)])
+def test_gather_tma_boxes_match_oracle(orc, win_b, n, c, h, w):
+    """The TMA-box gather (8x8 / 4x4 windows, W % 4 == 0): ragged channel
+    slices, tiles at every fringe (negative window origins zero-filled by the
+    tensor map), per-sample epilogue with SiLU on in-canvas cells only —
+    bit-exact vs the oracle, with and without the epilogue."""
+    rng = np.random.default_rng(win_b * 1000 + c)
+    x = rng.uniform(-3, 3, (n, c, h, w)).astype(np.float32)
+    b = win_b
+    m = np.zeros((h, w), np.uint8)
+    m[0, 0] = m[-1, -1] = m[0, -1] = m[-1, 0] = 1
+    m[h // 2, w // 2] = 1
+    m |= (rng.random((h, w)) < 0.05).astype(np.uint8)
+    idx, _ = orc.mask_to_block_indices(m, b, n)
+    for epi in ([], rand_epi_np(rng, c, n, silu=True, per_sample=True)):
+        want = orc.gather(x, idx, b, h, w, 3, 1, epi)
+        got = host(sb.gather(cu(x), cu(idx), b, 3, 1, to_dev_epi(epi) if epi else None))
+        assert bits_equal(got, want)
