@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-single-thread", type=int, default=1, help="also time one 1-thread reference edit")
     ap.add_argument("--requests", type=int, default=64, help="config 5: independent requests over all ranks")
     ap.add_argument("--group", type=int, default=8, help="config 5: requests per grouped engine")
+    ap.add_argument("--sweep", type=int, default=1, help="config 4: edit-area x block sweep (N=1)")
     return ap.parse_args()
 
 
@@ -260,6 +261,75 @@ def grouped_requests(sb, torch, model, cfg, math, n_requests=64, group=16, round
             "checksums": len(res),
             "workload": f"config 5: {n_requests} config-2 requests (rect1, seeds 7..{6 + n_requests}), request i on "
                         f"GPU i mod {world}, grouped engines of <= {group} requests, L2 flushed per round"}
+
+
+# ------------------------------------------------ config 4: area x block --
+
+SWEEP_AREAS = [0.005, 0.012, 0.05, 0.15, 0.30]
+SWEEP_BLOCKS = [(4, 4), (6, 4), (8, 4)]
+
+
+def sweep_edit(sb, torch, orig, area):
+    """Edited input for a target edit area: the reference fixtures where they
+    exist (rect1 1.196 %, rect5, rect15; fixtures.cpp:105-128), otherwise a
+    square placed like place_square (fixtures.cpp:26-34) from seeded draws."""
+    n, c, h, w = orig.shape
+    named = {0.012: "rect1", 0.05: "rect5", 0.15: "rect15"}
+    if area in named:
+        return sb.make_edit_fixture(named[area], n, c, h, w, WORKLOAD["seed"])[1]
+    side = max(1, int(round((area * h * w) ** 0.5)))
+    g = torch.Generator().manual_seed(int(area * 1e4))
+    y0 = int(torch.randint(0, h - side + 1, (1,), generator=g))
+    x0 = int(torch.randint(0, w - side + 1, (1,), generator=g))
+    e = orig.clone()
+    e[:, :, y0:y0 + side, x0:x0 + side] += 0.3
+    return e
+
+
+def config4_sweep(sb, torch, eng, orig, flush, reps=10):
+    """BASELINE config 4: edit-area sweep (0.5-30 %) x block-size sweep on the
+    config-2 model, sparse vs the engine's dense pass, F16; crossover = the
+    smallest area where the sparse edit is no faster than the dense pass."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[len(ts) // 2]
+
+    x0 = orig.to(dev)
+    dense = timed(lambda: eng.dense_forward(x0))
+    points, edits = [], {}
+    for area in SWEEP_AREAS:
+        ed = sweep_edit(sb, torch, orig, area)
+        edits[area] = ed
+        edd = ed.to(dev)
+        out = torch.empty(eng.output_shape(), device=dev)
+        for b3, b1 in SWEEP_BLOCKS:
+            cfg = sb.default_config(**{**{k: WORKLOAD[k] for k in ("dilate_full", "dilate_scale", "min_sparse_res")},
+                                       "block3": b3, "block1": b1})
+            t = timed(lambda: eng.sparse_forward(edd, config=cfg, out=out))
+            tr = eng.trace().numpy()
+            macs, dmacs = int(tr[:, 3].sum()), int(tr[:, 4].sum())
+            points.append({"area_pct": round(100 * float(((ed - orig).abs().amax(dim=(0, 1)) > 1e-3).float().mean()), 3),
+                           "block3": b3, "block1": b1, "sparse_ms": round(t, 4),
+                           "speedup_vs_dense": round(dense / t, 3), "mac_reduction": round(dmacs / max(macs, 1), 3)})
+    b6 = [p for p in points if p["block3"] == 6]
+    cross = next((p["area_pct"] for p in b6 if p["speedup_vs_dense"] <= 1.0), None)
+    return {"dense_ms": round(dense, 4), "points": points, "crossover_area_pct_b6": cross,
+            "workload": "config 4: config-2 model, edits of 0.5-30 % area (reference rect fixtures where they exist), "
+                        "block3 in {4, 6, 8}, F16, L2 flushed"}, edits
 
 
 # ------------------------------------------------------------ reference --
@@ -533,6 +603,14 @@ def main_ours(args):
     conv_flops = float(flops.sum())
     achieved_tf = conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
 
+    # ---- config 4: edit-area x block-size sweep (rank 0 only, one GPU)
+    sweep, sweep_edits = None, {}
+    if world == 1 and args.sweep:
+        try:
+            sweep, sweep_edits = config4_sweep(sb, torch, eng, orig, flush)
+        except Exception as e:  # report, never hide
+            sweep = {"error": str(e)}
+
     # ---- config 5: grouped independent requests, request i on rank i mod N
     grouped = None
     if args.requests > 1:
@@ -585,6 +663,8 @@ def main_ours(args):
     }
     if grouped is not None:
         line["batched_requests"] = grouped
+    if sweep is not None:
+        line["edit_area_sweep"] = sweep
     # Tensor-pipe context at throughput-shaped work (same kernels): the whole
     # dense pass, and the batched requests' aggregate (algorithmic FLOPs = the
     # reference's MAC counts x 2, graph.cpp:712-714) — the single edit is
@@ -619,6 +699,20 @@ def main_ours(args):
             got = out.cpu().numpy()
             line["parity"] = parity_block(R, rm, ref_outs[-1], got, m2, cfg,
                                           eng.get_tensor("final", got.shape).numpy())
+            if isinstance(sweep, dict) and "points" in sweep:
+                # config-4 parity: the reference on the same cache, b6 points
+                import numpy as np
+                errs = []
+                for area, ed in sweep_edits.items():
+                    cfg6 = sb.default_config(**{k: WORKLOAD[k] for k in ("dilate_full", "dilate_scale",
+                                                                         "min_sparse_res", "block3", "block1")})
+                    en = ed.numpy()
+                    mk = R.difference_mask(o2, en)
+                    ref_o, _ = rm.sparse_forward(cache, en, mk, cfg6)
+                    got6 = eng.sparse_forward(ed.to(out.device), config=cfg6).cpu().numpy()
+                    errs.append(float(np.abs(got6 - ref_o).max() / max(float(np.abs(ref_o).max()), 1e-30)))
+                sweep["parity_b6_max_norm_err"] = [round(e, 6) for e in errs]
+                sweep["parity_b6_within_tolerance"] = all(e <= 1e-2 for e in errs)
             if args.cpu_single_thread:
                 os.environ["SIGE_THREADS"] = "1"  # re-read by every reference call
                 t1 = time_reference_edits(rm, cache, e2, m2, cfg, 1)
