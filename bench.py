@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--requests", type=int, default=64, help="config 5: independent requests over all ranks")
     ap.add_argument("--group", type=int, default=8, help="config 5: requests per grouped engine")
     ap.add_argument("--sweep", type=int, default=1, help="config 4: edit-area x block sweep (N=1)")
+    ap.add_argument("--spade", type=int, default=1, help="config 3: GauGAN SPADE generator edit (N=1)")
     return ap.parse_args()
 
 
@@ -330,6 +331,63 @@ def config4_sweep(sb, torch, eng, orig, flush, reps=10):
     return {"dense_ms": round(dense, 4), "points": points, "crossover_area_pct_b6": cross,
             "workload": "config 4: config-2 model, edits of 0.5-30 % area (reference rect fixtures where they exist), "
                         "block3 in {4, 6, 8}, F16, L2 flushed"}, edits
+
+
+def config3_spade(sb, torch, flush, reps=10):
+    """BASELINE config 3: the GauGAN SPADE generator (Cityscapes 256x512, 36
+    labels, nf 64, random init) through the engine, F16, one relabelled square
+    (1.2 % of the pixels) per edit, L2 flushed; sparse vs the engine's dense
+    pass. Every layer sparse (min_sparse_res 1), dilation 1 / 1: the MAC
+    reduction this gives (18.3x) is the paper's (281 G -> 15.3 G, 18x,
+    PAPER.md:290). Quality (random init, so only indicative): distance to the
+    dense pass with the cached instance-norm statistics (the dilation's loss)
+    and to the fresh-statistics dense pass; tools/spade_probe.py sweeps the
+    settings (profiles/r2_spade_probe.txt)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    m = sb.Model("gaugan_spade")
+    c, h, w = m.in_shape
+    orig, edited = sb.make_seg_fixture(1, c, h, w, 11)
+    eng = sb.Engine(m, batch=1, math=sb.MATH_F16)
+    x0, x1 = orig.to(dev), edited.to(dev)
+    eng.precompute(x0)
+    cfg = sb.default_config(dilate_full=1, dilate_scale=1, min_sparse_res=1)
+    out = torch.empty(eng.output_shape(), device=dev)
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[len(ts) // 2]
+
+    sparse = timed(lambda: eng.sparse_forward(x1, config=cfg, out=out))
+    tr = eng.trace().numpy()
+    macs, dmacs = int(tr[:, 3].sum()), int(tr[:, 4].sum())
+    dense = timed(lambda: eng.dense_forward(x1))
+    got = eng.sparse_forward(x1, config=cfg).float()
+    cached = eng.dense_forward(x1, reused_stats=True)
+    fresh = eng.dense_forward(x1)
+
+    def ne(a, b):
+        return round(float((a - b).abs().max() / b.abs().max().clamp_min(1e-30)), 6)
+
+    area = float(((orig - edited).abs().amax(dim=(0, 1)) > 0).float().mean())
+    return {"workload": "config 3: gaugan_spade 36x256x512 one-hot map, relabelled square, F16, L2 flushed; "
+                        "dilate_full 1, dilate_scale 1, min_sparse_res 1, block 6/4",
+            "edit_area_pct": round(100 * area, 3), "sparse_ms": round(sparse, 4), "dense_ms": round(dense, 4),
+            "paper": "281 G -> 15.3 G MACs (18x), 45.4 -> 11.1 ms (4.1x) on RTX 3090 (BASELINE.md)",
+            "speedup_vs_dense": round(dense / sparse, 3), "macs": macs, "dense_macs": dmacs,
+            "mac_reduction": round(dmacs / max(macs, 1), 3), "launches_per_edit": eng.last_launch_count(),
+            "max_norm_err_vs_dense_cached_stats": ne(got, cached), "max_norm_err_vs_dense_fresh": ne(got, fresh)}
 
 
 # ------------------------------------------------------------ reference --
@@ -611,6 +669,14 @@ def main_ours(args):
         except Exception as e:  # report, never hide
             sweep = {"error": str(e)}
 
+    # ---- config 3: GauGAN SPADE generator (rank 0 only, one GPU)
+    spade = None
+    if world == 1 and args.spade:
+        try:
+            spade = config3_spade(sb, torch, flush)
+        except Exception as e:  # report, never hide
+            spade = {"error": str(e)}
+
     # ---- config 5: grouped independent requests, request i on rank i mod N
     grouped = None
     if args.requests > 1:
@@ -665,6 +731,8 @@ def main_ours(args):
         line["batched_requests"] = grouped
     if sweep is not None:
         line["edit_area_sweep"] = sweep
+    if spade is not None:
+        line["config3_spade"] = spade
     # Tensor-pipe context at throughput-shaped work (same kernels): the whole
     # dense pass, and the batched requests' aggregate (algorithmic FLOPs = the
     # reference's MAC counts x 2, graph.cpp:712-714) — the single edit is

@@ -96,8 +96,23 @@ enum {
   SIGE_LAYER_ACTIVATION = 2,
   SIGE_LAYER_RESBLOCK = 3,
   SIGE_LAYER_DOWNSAMPLE = 4,
-  SIGE_LAYER_UPSAMPLE = 5
+  SIGE_LAYER_UPSAMPLE = 5,
+  /* Config 3 (GauGAN; no reference counterpart): */
+  SIGE_LAYER_SPADE_RESBLOCK = 6, /* SPADE residual block, see sige_spade_desc */
+  SIGE_LAYER_RESIZE = 7          /* the model INPUT resized (nearest) to resize_h x resize_w (integer factors) */
 };
+
+/* One SPADE normalisation (Park et al. 2019): the param-free instance norm of
+ * its input x (per sample and channel, eps), modulated per pixel by the
+ * segmentation map s (the model input, nearest-resized to x's resolution):
+ *   a = ReLU(shared(s)),  SPADE(x) = norm(x) * (1 + gamma(a)) + beta(a)
+ * shared: 3x3 label_nc -> nhidden; gamma, beta: 3x3 nhidden -> C. */
+typedef struct sige_spade_desc {
+  float eps;
+  sige_conv_desc shared;
+  sige_conv_desc gamma;
+  sige_conv_desc beta;
+} sige_spade_desc;
 
 /* `sige::Layer` (graph.hpp:53-61) flattened. For RESBLOCK: conv = conv1,
  * conv2, norm, act and (has_shortcut) shortcut, as ResBlockSpec
@@ -112,6 +127,14 @@ typedef struct sige_layer_desc {
   sige_conv_desc conv2;
   int has_shortcut;
   sige_conv_desc shortcut;
+  /* SPADE_RESBLOCK (config 3): conv = conv_0 (3x3 fin -> fmiddle), conv2 =
+   * conv_1 (3x3 fmiddle -> fout), shortcut = conv_s (1x1, no bias) when
+   * has_shortcut, act = the block activation (SIGE_ACT_LEAKY_RELU);
+   * spade[0] normalises conv_0's input, spade[1] conv_1's, spade[2] the
+   * shortcut's. out = (has_shortcut ? conv_s(SPADE_s(x)) : x)
+   *                 + conv_1(act(SPADE_1(conv_0(act(SPADE_0(x)))))). */
+  const sige_spade_desc* spade;
+  int resize_h, resize_w; /* RESIZE */
 } sige_layer_desc;
 
 /* `sige::ModelSpec` (graph.hpp:63-71). */
@@ -388,6 +411,10 @@ size_t sige_engine_cache_bytes(const sige_engine* eng);
 
 /* ---- synthetic inputs (fixtures.hpp, models.hpp) -------------------------- */
 
+/* Config 3 input: a one-hot segmentation map (n, label_nc, h, w) of random
+ * labelled rectangles and its edit — a rect1-style square (1.2 % of the
+ * pixels) relabelled, the GauGAN edit of SIGE. Host buffers. */
+int sige_make_seg_fixture(int n, int label_nc, int h, int w, uint32_t seed, float* orig, float* edited);
 /* make_edit_fixture (fixtures.hpp:23-24, fixtures.cpp:105-128) into host
  * buffers of n*c*h*w floats. Returns SIGE_ERR_CONFIG for unknown kinds. */
 int sige_make_edit_fixture(const char* kind, int n, int c, int h, int w, uint32_t seed,

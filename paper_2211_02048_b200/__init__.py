@@ -418,6 +418,14 @@ def make_edit_fixture(kind: str, n: int, c: int, h: int, w: int, seed: int):
     return o, e
 
 
+def make_seg_fixture(n: int, label_nc: int, h: int, w: int, seed: int):
+    """Config 3: one-hot segmentation map and its edit (a relabelled 1.2 % square), host float32."""
+    o = torch.empty((n, label_nc, h, w), dtype=torch.float32)
+    e = torch.empty((n, label_nc, h, w), dtype=torch.float32)
+    _check(_lib().sige_make_seg_fixture(n, label_nc, h, w, seed, o.data_ptr(), e.data_ptr()))
+    return o, e
+
+
 # ------------------------------------------------ on-disk formats (io.hpp) --
 
 def save_tensor(path: str, t: torch.Tensor) -> None:

@@ -25,6 +25,8 @@ EPI_SCALE_SHIFT, EPI_ACTIVATION = 0, 1
 MAX_EPI_STEPS = 4
 NORM_GROUP, NORM_INSTANCE, NORM_BATCH = 0, 1, 2
 LAYER_CONV, LAYER_NORM, LAYER_ACTIVATION, LAYER_RESBLOCK, LAYER_DOWNSAMPLE, LAYER_UPSAMPLE = range(6)
+LAYER_SPADE_RESBLOCK, LAYER_RESIZE = 6, 7
+ACT_LEAKY_RELU = 3
 MATH_EXACT, MATH_TF32, MATH_FP32_FMA, MATH_F16 = 0, 1, 2, 3
 
 FloatP = C.POINTER(C.c_float)
@@ -68,6 +70,10 @@ class NormDesc(C.Structure):
     ]
 
 
+class SpadeDesc(C.Structure):
+    _fields_ = [("eps", C.c_float), ("shared", ConvDesc), ("gamma", ConvDesc), ("beta", ConvDesc)]
+
+
 class LayerDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int),
@@ -79,6 +85,9 @@ class LayerDesc(C.Structure):
         ("conv2", ConvDesc),
         ("has_shortcut", C.c_int),
         ("shortcut", ConvDesc),
+        ("spade", C.POINTER(SpadeDesc)),
+        ("resize_h", C.c_int),
+        ("resize_w", C.c_int),
     ]
 
 
@@ -207,6 +216,7 @@ SYMBOLS = {
     "sige_engine_timeline_read": (_i, [_vp, _vp, _i, C.POINTER(_i)]),
     "sige_engine_cache_entries": (_i, [_vp, _i, C.c_char_p, _sz, C.POINTER(_sz)]),
     "sige_make_edit_fixture": (_i, [C.c_char_p, _i, _i, _i, _i, _u32, _vp, _vp]),
+    "sige_make_seg_fixture": (_i, [_i, _i, _i, _i, _u32, _vp, _vp]),
     "sige_gather_spade": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(Epilogue), _i, _vp, _vp]),
     "sige_resize_nearest": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     "sige_save_tensor": (_i, [C.c_char_p, _vp, _i, _i, _i, _i]),

@@ -729,6 +729,15 @@ int sige_engine_cache_entries(const sige_engine* eng, int step, char* buf, size_
 size_t sige_engine_cache_bytes(const sige_engine* eng) { return eng ? eng->impl->cache_bytes() : 0; }
 
 // ---- synthetic inputs
+int sige_make_seg_fixture(int n, int label_nc, int h, int w, uint32_t seed, float* orig, float* edited) {
+  return guarded([&] {
+    if (n < 1 || label_nc < 2 || h < 8 || w < 8) throw ConfigError("seg fixture: bad shape");
+    need(orig, "seg fixture");
+    need(edited, "seg fixture");
+    sige_b200::make_seg_fixture(n, label_nc, h, w, seed, orig, edited);
+  });
+}
+
 int sige_make_edit_fixture(const char* kind, int n, int c, int h, int w, uint32_t seed,
                            float* original_host, float* edited_host) {
   return guarded([&] { make_edit_fixture(kind, n, c, h, w, seed, original_host, edited_host); });

@@ -94,6 +94,7 @@ DevEpilogue make_dev_epilogue(const sige_epilogue* e, int channels, int batch);
 // Reference activation arithmetic (eltwise.cpp:23-36), no FMA contraction.
 __device__ __forceinline__ float dev_act(float v, int kind, int fma_expf, int fast = 0) {
   if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;  // NaN -> 0, -0 -> +0
+  if (kind == SIGE_ACT_LEAKY_RELU) return v > 0.0f ? v : __fmul_rn(0.2f, v);  // SPADE blocks (config 3)
   if (kind == SIGE_ACT_SILU && fast) return __fdividef(v, 1.0f + __expf(-v));
   if (kind == SIGE_ACT_SILU) {
     float e = glibc_expf(-v, fma_expf != 0);

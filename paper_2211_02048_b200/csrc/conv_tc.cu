@@ -405,6 +405,7 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 // instruction cache (an epilogue with a chain ran 5x slower than without).
 __device__ __forceinline__ float tc_act(float v, int kind) {
   if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;
+  if (kind == SIGE_ACT_LEAKY_RELU) return v > 0.0f ? v : __fmul_rn(0.2f, v);
   if (kind == SIGE_ACT_SILU) return __fdividef(v, 1.0f + __expf(-v));
   return v;
 }
@@ -1984,10 +1985,12 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
   // chain — [scale-shift, act] or GroupNorm-from-statistics then act — is
   // applied in shared memory after the copy lands.
   const DevEpilogue& e = src.epi;
-  const bool chain_ok =
+  bool chain_ok =
       src.gn_stats ? (e.num_steps == 0 || (e.num_steps == 1 && e.kind[0] == SIGE_EPI_ACTIVATION))
                    : (e.num_steps >= 1 && e.num_steps <= 2 && e.kind[0] == SIGE_EPI_SCALE_SHIFT &&
                       (e.num_steps == 1 || e.kind[1] == SIGE_EPI_ACTIVATION));
+  for (int i = 0; i < e.num_steps; ++i)  // the in-smem transform knows ReLU and SiLU
+    if (e.kind[i] == SIGE_EPI_ACTIVATION && e.act[i] != SIGE_ACT_RELU && e.act[i] != SIGE_ACT_SILU) chain_ok = false;
   const int twin_c = src.twin_c ? src.twin_c : src.c;
   const bool twin_ok = f16 && src.twin && !src.half && src.c == cw.c_in && twin_c % 8 == 0;
   bool xform = twin_ok && chain_ok && cw.stride == 1 && static_cast<long long>(src.n) * src.c <= 4096;

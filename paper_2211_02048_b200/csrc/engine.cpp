@@ -158,6 +158,36 @@ Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), m
       L.has_shortcut = d.has_shortcut;
       if (d.has_shortcut) L.shortcut = up_conv(d.shortcut);
     }
+    if (d.kind == SIGE_LAYER_SPADE_RESBLOCK) {
+      L.conv = up_conv(d.conv);
+      L.conv2 = up_conv(d.conv2);
+      L.has_shortcut = d.has_shortcut;
+      if (d.has_shortcut) L.shortcut = up_conv(d.shortcut);
+      L.n_spade = d.has_shortcut ? 3 : 2;
+      for (int k = 0; k < L.n_spade; ++k) {
+        const sige_spade_desc& sp = d.spade[k];
+        L.spade_shared[k] = up_conv(sp.shared);
+        L.spade_eps[k] = sp.eps;
+        // gamma and beta as one conv: output channels [gamma | beta]
+        const int C = sp.gamma.c_out, nh = sp.gamma.c_in;
+        const size_t wn = static_cast<size_t>(C) * nh * 9;
+        std::vector<float> w2(2 * wn), b2(2 * static_cast<size_t>(C), 0.0f);
+        std::memcpy(w2.data(), sp.gamma.weight, wn * sizeof(float));
+        std::memcpy(w2.data() + wn, sp.beta.weight, wn * sizeof(float));
+        if (sp.gamma.bias) std::memcpy(b2.data(), sp.gamma.bias, C * sizeof(float));
+        if (sp.beta.bias) std::memcpy(b2.data() + C, sp.beta.bias, C * sizeof(float));
+        const sige_conv_desc gb{nh, 2 * C, 3, 1, w2.data(), b2.data()};
+        L.spade_gb[k] = up_conv(gb);
+        const std::vector<float> ones(C, 1.0f), zeros(C, 0.0f);
+        L.spade_ones[k] = upload(ones.data(), C);
+        L.spade_zeros[k] = upload(zeros.data(), C);
+      }
+    }
+    if (d.kind == SIGE_LAYER_RESIZE) {
+      if (i != 0) throw ConfigError("model layer L" + std::to_string(i) + ": resize is supported on the input only");
+      L.resize_h = d.resize_h;
+      L.resize_w = d.resize_w;
+    }
     if (d.kind == SIGE_LAYER_NORM || d.kind == SIGE_LAYER_RESBLOCK) {
       const sige_norm_desc& n = d.norm;
       L.norm_kind = n.kind;
@@ -238,7 +268,8 @@ const DevNorm& Engine::cache_norm(int step, const std::string& key) const {
 
 bool Engine::wants_twin(const std::string& key, int layout, int half) const {
   if (math_ != SIGE_MATH_F16 || layout != kNHWC || half) return false;
-  if (ends_with(key, ".sum")) return true;
+  if (ends_with(key, ".sum") || ends_with(key, ".mod")) return true;
+  if (ends_with(key, ".conv0.out") || ends_with(key, ".sc.out")) return false;  // read by the modulation / join only
   return ends_with(key, ".out") && !ends_with(key, "conv1.out") && !ends_with(key, "conv2.out") &&
          !ends_with(key, "shortcut.out");
 }
@@ -634,6 +665,74 @@ void Engine::invalidate_programs() {
 // ---------------------------------------------------------- dense walk --
 // dense_walk (graph.cpp:343-412) on the device. capture=true stores every
 // cache entry (precompute); reused=true takes folded norms from the cache.
+// ---------------------------------------------------- SPADE (config 3) --
+Src Engine::seg_at(const float* in, int h, int w, DevTensor& buf, cudaStream_t st) {
+  if (math_ == SIGE_MATH_F16 && !buf.h16) buf.h16 = alloc(static_cast<size_t>(batch_) * h * w * ((in_c_ + 7) / 8 * 8) * 2);
+  const int c16 = (in_c_ + 7) / 8 * 8;
+  launch_resize_nhwc(in, batch_, in_c_, in_h_, in_w_, h, w, buf.p, buf.h16, c16, st);
+  Src s = plain(buf);
+  s.twin = buf.h16;
+  s.twin_c = c16;
+  return s;
+}
+
+// One SPADE residual block over every pixel, in the restatement's order
+// (oracle/spade.py): per SPADE norm k, a = ReLU(shared(seg)), [gamma|beta] =
+// gb(a), mod = act(instnorm(input) (1 + gamma) + beta); conv_0(mod_0) ->
+// conv_1(mod_1) + (conv_s(mod_s) | x).
+Src Engine::spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg, bool reused,
+                        const std::function<DevTensor&(const std::string&, int, int)>& tensor,
+                        const std::function<DevNorm&(const std::string&, int)>& norm, cudaStream_t st) {
+  (void)li;
+  const int h = x.h, w = x.w;
+  const Tiles t3 = dense_tiles(h, w, 3, 1), t1 = dense_tiles(h, w, 1, 1);
+  auto modulate = [&](int k, const Src& in, int act) -> Src {
+    const std::string sk = ".spade" + std::to_string(k);
+    const int nh = L.spade_shared[k].c_out, C = in.c;
+    DevTensor& a = tensor(sk + ".a", nh, 0);
+    Dst da = to_dst(a);
+    Src as = plain(a);
+    if (use_act()) {  // the gamma/beta conv stages ReLU(a) once per pixel (fp16 in F16)
+      DevTensor& aa = tensor(sk + ".aact", nh, act_half());
+      da.act = aa.p;
+      da.act_half = aa.half;
+      da.act_epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+      epi_push_act(da.act_epi, SIGE_ACT_RELU);
+      as = plain(aa);
+    } else {
+      epi_push_act(as.epi, SIGE_ACT_RELU);
+    }
+    conv(seg, t3, L.spade_shared[k], da, st);
+    DevTensor& gb = tensor(sk + ".gb", 2 * C, 0);
+    conv(as, t3, L.spade_gb[k], to_dst(gb), st);
+    DevNorm& nf = norm(sk + ".norm", batch_ * C);
+    if (!reused) {
+      if (!gn_scratch_) gn_scratch_ = static_cast<double*>(alloc(kGnScratch * sizeof(double)));
+      launch_gn_fold(in, C, L.spade_eps[k], L.spade_ones[k], L.spade_zeros[k], nf.scale, nf.shift, gn_scratch_,
+                     kGnScratch, tensor_cores() ? 0 : 1, st);
+    }
+    DevTensor& mod = tensor(sk + ".mod", C, 0);
+    launch_spade_mod(in, nf.scale, nf.shift, gb.p, act, nullptr, mod.p, mod.h16, st);
+    return plain(mod);
+  };
+  const Src m0 = modulate(0, x, L.act);
+  DevTensor& c0 = tensor(".conv0.out", L.conv.c_out, 0);
+  conv(m0, t3, L.conv, to_dst(c0), st);
+  Src addend = x;
+  if (L.has_shortcut) {
+    const Src ms = modulate(2, x, SIGE_ACT_NONE);
+    DevTensor& sc = tensor(".sc.out", L.shortcut.c_out, 0);
+    conv(ms, t1, L.shortcut, to_dst(sc), st);
+    addend = plain(sc);
+  }
+  const Src m1 = modulate(1, plain(c0), L.act);
+  DevTensor& sum = tensor(".sum", L.conv2.c_out, 0);
+  Dst d = to_dst(sum, kAddSrc);
+  d.addend = addend;
+  conv(m1, t3, L.conv2, d, st);
+  return plain(sum);
+}
+
 void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
                         cudaStream_t st) {
   Src x = input;
@@ -678,6 +777,29 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         x.h *= 2;
         x.w *= 2;
         break;
+      case SIGE_LAYER_RESIZE: {
+        DevTensor& o = capture ? cache_slot(step, key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC)
+                               : scratch("dense." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
+        launch_resize_nhwc(input.ptr, batch_, in_c_, in_h_, in_w_, sh.h_out, sh.w_out, o.p, o.h16,
+                           in_c_, st);
+        x = plain(o);
+        break;
+      }
+      case SIGE_LAYER_SPADE_RESBLOCK: {
+        DevTensor& segb = scratch("dense.seg@" + std::to_string(sh.h_in) + "x" + std::to_string(sh.w_in), in_c_,
+                                  sh.h_in, sh.w_in, kNHWC);
+        const Src seg = seg_at(input.ptr, sh.h_in, sh.w_in, segb, st);
+        auto tensor = [&](const std::string& sfx, int c, int half) -> DevTensor& {
+          return capture ? cache_slot(step, key + sfx, c, sh.h_in, sh.w_in, kNHWC, half)
+                         : scratch("dense." + key + sfx, c, sh.h_in, sh.w_in, kNHWC, half);
+        };
+        auto norm = [&](const std::string& sfx, int np) -> DevNorm& {
+          if (reused) return const_cast<DevNorm&>(cache_norm(step, key + sfx));
+          return capture ? norm_slot(step, key + sfx, np) : scratch_norm("dense." + key + sfx, np);
+        };
+        x = spade_dense(L, static_cast<int>(i), x, seg, reused, tensor, norm, st);
+        break;
+      }
       case SIGE_LAYER_RESBLOCK: {
         const int c1 = L.conv.c_out, co = L.conv2.c_out, h = sh.h_in, w = sh.w_in;
         if (!capture && !reused && fused_gn(L)) {
@@ -1045,6 +1167,131 @@ struct ProgramBuilder {
           flow.w *= 2;
           has_blocks = false;  // materialize (graph.cpp:762-770)
           break;
+        case SIGE_LAYER_RESIZE: {
+          // the input resized per call, dense (a few KB to a few MB)
+          DevTensor& o = E.scratch("sparse." + key + ".out", sh.c_out, sh.h_out, sh.w_out, kNHWC);
+          const DevTensor oc = o;
+          const int ic = E.in_c_, ih = E.in_h_, iw = E.in_w_, n = N;
+          add([eng, oc, ic, ih, iw, n](cudaStream_t st) {
+            launch_resize_nhwc(eng->cur_in_, n, ic, ih, iw, oc.h, oc.w, oc.p, oc.h16, ic, st);
+          });
+          flow = plain(o);
+          flow_is_input = false;
+          has_blocks = false;
+          break;
+        }
+        case SIGE_LAYER_SPADE_RESBLOCK: {
+          const int h = flow.h, w = flow.w;
+          const Src x0 = flow;
+          const int li = static_cast<int>(i);
+          const int c16 = (E.in_c_ + 7) / 8 * 8;
+          DevTensor& segb =
+              E.scratch("sparse.seg@" + std::to_string(h) + "x" + std::to_string(w), E.in_c_, h, w, kNHWC);
+          if (E.math_ == SIGE_MATH_F16 && !segb.h16) segb.h16 = E.alloc(static_cast<size_t>(N) * h * w * c16 * 2);
+          const DevTensor segc = segb;
+          auto add_trace = [&](int entry_idx) {
+            for (int k = 0; k < L.n_spade; ++k) {
+              P.trace.push_back({entry_idx, L.spade_shared[k].c_in, L.spade_shared[k].c_out, 3, 1, h, w, N});
+              P.trace.push_back({entry_idx, L.spade_gb[k].c_in, L.spade_gb[k].c_out, 3, 1, h, w, N});
+            }
+            P.trace.push_back({entry_idx, L.conv.c_in, L.conv.c_out, 3, 1, h, w, N});
+            if (L.has_shortcut) P.trace.push_back({entry_idx, L.shortcut.c_in, L.shortcut.c_out, 1, 1, h, w, N});
+            P.trace.push_back({entry_idx, L.conv2.c_in, L.conv2.c_out, 3, 1, h, w, N});
+          };
+          if (!runs_sparse(L, h, w, cfg) || !cfg.norm_precompute) {
+            // dense fallback with fresh statistics (as ResBlocks, graph.cpp:799-815)
+            DevTensor& sum = E.scratch("sparse." + key + ".sum", L.conv2.c_out, h, w, kNHWC);
+            const LayerDev Lc = L;
+            add([eng, Lc, li, x0, fin, bind, segc, key](cudaStream_t st) {
+              DevTensor seg_buf = segc;
+              const Src seg = eng->seg_at(eng->cur_in_, x0.h, x0.w, seg_buf, st);
+              auto tensor = [&](const std::string& sfx, int c, int half) -> DevTensor& {
+                return eng->scratch("sparse." + key + sfx, c, x0.h, x0.w, kNHWC, half);
+              };
+              auto norm = [&](const std::string& sfx, int np) -> DevNorm& {
+                return eng->scratch_norm("sparse." + key + sfx, np);
+              };
+              eng->spade_dense(Lc, li, bind(x0, fin), seg, false, tensor, norm, st);
+            }, 0);
+            add_trace(-1);
+            flow = plain(sum);
+            has_blocks = false;
+          } else {
+            // sparse: every SPADE conv, the modulation and conv_0/conv_s/conv_1
+            // run on the main tiles; working buffers restored afterwards.
+            const int em = entry(h, w, cfg.block3);
+            const Tiles tm = tiles(em);
+            auto W = [&](const std::string& sfx) -> DevTensor& {
+              DevTensor& wb = E.work_buffer(step, key + sfx);
+              restore(wb, E.cache_tensor(step, key + sfx), em);
+              return wb;
+            };
+            add([eng, segc](cudaStream_t st) {  // this resolution's segmentation map
+              DevTensor seg_buf = segc;
+              eng->seg_at(eng->cur_in_, segc.h, segc.w, seg_buf, st);
+            });
+            Src seg = plain(segb);
+            seg.twin = segb.h16;
+            seg.twin_c = c16;
+            auto modulate = [&](int k, const Src& in, int act, bool in_is_input) -> Src {
+              const std::string sk = ".spade" + std::to_string(k);
+              DevTensor& a = W(sk + ".a");
+              Dst da = to_dst(a);
+              Src as = plain(a);
+              if (E.use_act()) {
+                DevTensor& aa = W(sk + ".aact");
+                da.act = aa.p;
+                da.act_half = aa.half;
+                da.act_epi.fma_expf = host_expf_is_fma() ? 1 : 0;
+                epi_push_act(da.act_epi, SIGE_ACT_RELU);
+                as = plain(aa);
+              } else {
+                epi_push_act(as.epi, SIGE_ACT_RELU);
+              }
+              conv_step(seg, tm, L.spade_shared[k], da);
+              DevTensor& gb = W(sk + ".gb");
+              conv_step(as, tm, L.spade_gb[k], to_dst(gb));
+              const DevNorm& nf = E.cache_norm(step, key + sk + ".norm");
+              DevTensor& mod = W(sk + ".mod");
+              const float* scp = nf.scale;
+              const float* shp = nf.shift;
+              const float* gbp = gb.p;
+              float* mp = mod.p;
+              void* m16 = mod.h16;
+              add([in, in_is_input, bind, scp, shp, gbp, act, tm, mp, m16](cudaStream_t st) {
+                launch_spade_mod(bind(in, in_is_input), scp, shp, gbp, act, &tm, mp, m16, st);
+              });
+              return plain(mod);
+            };
+            const Src m0 = modulate(0, x0, L.act, fin);
+            DevTensor& c0 = W(".conv0.out");
+            conv_step(m0, tm, L.conv, to_dst(c0));
+            Src addend = x0;
+            if (L.has_shortcut) {
+              const Src ms = modulate(2, x0, SIGE_ACT_NONE, fin);
+              DevTensor& sc = W(".sc.out");
+              conv_step(ms, tm, L.shortcut, to_dst(sc));
+              addend = plain(sc);
+            }
+            const Src m1 = modulate(1, plain(c0), L.act, false);
+            DevTensor& sum = W(".sum");
+            Dst d = to_dst(sum, kAddSrc);
+            d.addend = addend;
+            const bool add_in = !L.has_shortcut && fin;
+            const ConvW c2w = L.conv2;
+            add([eng, m1, tm, c2w, d, add_in, bind](cudaStream_t st) {
+              Dst dd = d;
+              if (add_in) dd.addend = bind(d.addend, true);
+              eng->conv(m1, tm, c2w, dd, st);
+            });
+            add_trace(em);
+            flow = plain(sum);
+            has_blocks = true;
+            blocks_entry = em;
+          }
+          flow_is_input = false;
+          break;
+        }
         case SIGE_LAYER_RESBLOCK: {
           const int h = flow.h, w = flow.w, c1 = L.conv.c_out, co = L.conv2.c_out;
           Src x0 = flow;
@@ -1605,6 +1852,9 @@ void Engine::output_coverage(const float* edited, const uint8_t* mask, const sig
           op_cov_up2(a, h, w, b, st);
           std::swap(a, b);
           break;
+        case SIGE_LAYER_SPADE_RESBLOCK:
+        case SIGE_LAYER_RESIZE:
+          throw ConfigError("output_coverage: SPADE models (config 3) are not supported");
         case SIGE_LAYER_RESBLOCK:
           if (sp) {
             footprint(entry(s.h_out, s.w_out, cfg.block3), true);

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -52,6 +53,16 @@ struct LayerDev {
   int norm_kind = 0, groups = 1, channels = 0;
   float eps = 1e-5f;
   float *gamma = nullptr, *beta = nullptr, *rmean = nullptr, *rvar = nullptr;
+  // SPADE_RESBLOCK (config 3): per SPADE norm k (0: conv_0's input, 1:
+  // conv_1's, 2: the shortcut's) the shared conv (segmentation -> hidden,
+  // then ReLU) and gamma/beta stacked into one conv (hidden -> 2C: gamma
+  // channels first), the instance-norm eps and its param-free affine (ones,
+  // zeros) for the fold.
+  int n_spade = 0;
+  ConvW spade_shared[3], spade_gb[3];
+  float spade_eps[3] = {1e-5f, 1e-5f, 1e-5f};
+  float *spade_ones[3] = {}, *spade_zeros[3] = {};
+  int resize_h = 0, resize_w = 0;  // RESIZE
 };
 
 struct TraceInfo {
@@ -185,6 +196,14 @@ class Engine {
   cudaStream_t side_stream_ = nullptr;
   cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
+  // Config 3: a SPADE residual block over every pixel (dense walk / dense
+  // fallback; buffers from `tensor` / `norm`, statistics folded unless
+  // `reused`) — returns the block output; and the segmentation map (the model
+  // input `in`, NCHW) nearest-resized to (h, w) as an NHWC source.
+  Src spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg, bool reused,
+                  const std::function<DevTensor&(const std::string&, int, int)>& tensor,
+                  const std::function<DevNorm&(const std::string&, int)>& norm, cudaStream_t st);
+  Src seg_at(const float* in, int h, int w, DevTensor& buf, cudaStream_t st);
 
   std::string name_;
   struct HostEntry {  // an offloaded cache entry (pinned host copies)

@@ -623,6 +623,71 @@ __global__ void k_nhwc_to_nchw(const float* __restrict__ in, float* __restrict__
   }
 }
 
+// --------------------------------------------------------- SPADE (config 3) --
+// Nearest resize of an NCHW map by integer factors into NHWC (+ an fp16 twin
+// with channels padded to c16): the segmentation map at a block's resolution,
+// and the RESIZE layer. down: (y f, x f); up: (y / u, x / u) — resize_nearest.
+__global__ void k_resize_nhwc(const float* __restrict__ in, int n, int c, int H, int W, int h, int w,
+                              float* __restrict__ out, __half* __restrict__ out16, int c16) {
+  pdl_enter();
+  const long long total = static_cast<long long>(n) * h * w * c16;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int ch = static_cast<int>(q % c16);
+    long long p = q / c16;
+    const int x = static_cast<int>(p % w);
+    p /= w;
+    const int y = static_cast<int>(p % h);
+    const int in_n = static_cast<int>(p / h);
+    const int sy = h <= H ? y * (H / h) : y / (h / H), sx = w <= W ? x * (W / w) : x / (w / W);
+    const float v = ch < c ? __ldg(in + ((static_cast<size_t>(in_n) * c + ch) * H + sy) * W + sx) : 0.0f;
+    const size_t pix = (static_cast<size_t>(in_n) * h + y) * w + x;
+    if (ch < c && out) out[pix * c + ch] = v;
+    if (out16) out16[pix * c16 + ch] = __float2half_rn(v);
+  }
+}
+
+// SPADE modulation (Park et al. 2019): out = act((x sc + sh) (1 + gamma) + beta)
+// with the folded param-free instance norm (sc, sh per sample and channel),
+// gamma / beta the two halves of gb (NHWC, 2C channels), every operation
+// rounded on its own (the restatement's order, oracle/spade.py). Over the
+// tiles of `t` (sparse) or every pixel (t.idx == nullptr); NHWC fp32 out plus
+// the fp16 twin the consuming conv streams.
+__global__ void k_spade_mod(Src x, const float* __restrict__ sc, const float* __restrict__ sh,
+                            const float* __restrict__ gb, int act, Tiles t, float* __restrict__ out,
+                            __half* __restrict__ out16) {
+  pdl_enter();
+  const int c = x.c;
+  const bool dense = t.idx == nullptr;
+  const int count = dense ? 0 : (t.count_dev ? *t.count_dev : t.count);
+  const long long total =
+      dense ? static_cast<long long>(x.n) * x.h * x.w * c : static_cast<long long>(count) * t.bh * t.bw * c;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int n, y, xx, ch;
+    if (dense) {
+      ch = static_cast<int>(q % c);
+      long long p = q / c;
+      xx = static_cast<int>(p % x.w);
+      p /= x.w;
+      y = static_cast<int>(p % x.h);
+      n = static_cast<int>(p / x.h);
+    } else if (!tile_elem(t, count, c, x.h, x.w, q, n, y, xx, ch)) {
+      continue;
+    }
+    const size_t pix = (static_cast<size_t>(n) * x.h + y) * x.w + xx;
+    const int k = n * c + ch;
+    const float v = src_val(x, n, ch, y, xx);
+    const float nv = __fadd_rn(__fmul_rn(v, __ldg(sc + k)), __ldg(sh + k));
+    const float g = __ldg(gb + pix * 2 * c + ch), b = __ldg(gb + pix * 2 * c + c + ch);
+    float m = __fadd_rn(__fmul_rn(nv, __fadd_rn(1.0f, g)), b);
+    if (act == SIGE_ACT_LEAKY_RELU) m = m > 0.0f ? m : __fmul_rn(0.2f, m);
+    else if (act == SIGE_ACT_RELU) m = m > 0.0f ? m : 0.0f;
+    out[pix * c + ch] = m;
+    if (out16) out16[pix * c + ch] = __float2half_rn(m);
+  }
+}
+
 }  // namespace
 
 void launch_mask_bits(const float* orig, const float* edited, int n, int c, int h, int w, float thr,
@@ -657,7 +722,8 @@ void launch_plan(const uint32_t* bits, int H, int W, int dilate_full, int dilate
   const size_t smem = sizeof(uint32_t) * 3 * H * ((W + 31) >> 5);
   const int use_smem = smem <= 96 * 1024 ? 1 : 0;
   static std::atomic<uint64_t> attr_done{0};
-  if (use_smem && smem > 48 * 1024 && first_on_device(attr_done))
+  // (k_plan also has ~140 B of static shared memory: opt in above 47 KB)
+  if (use_smem && smem > 47 * 1024 && first_on_device(attr_done))
     SIGE_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   k_plan<<<num_entries, 1024, use_smem ? smem : 0, st>>>(bits, H, W, dilate_full, dilate_scale,
                                                          batch, entries_dev, use_smem, per_sample);
@@ -789,6 +855,28 @@ void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w
 void launch_nhwc_to_nchw(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st) {
   k_nhwc_to_nchw<<<grid_cap(static_cast<long long>(n) * c * h * w, 256), 256, 0, st>>>(in, out, n, c, h, w);
   after_launch("k_nhwc_to_nchw");
+}
+
+void launch_resize_nhwc(const float* in, int n, int c, int H, int W, int h, int w, float* out, void* out16, int c16,
+                        cudaStream_t st) {
+  const long long total = static_cast<long long>(n) * h * w * c16;
+  launch_pdl(k_resize_nhwc, dim3(grid_cap(total, 256)), dim3(256), st, in, n, c, H, W, h, w, out,
+             static_cast<__half*>(out16), c16);
+  after_launch("k_resize_nhwc");
+}
+
+void launch_spade_mod(const Src& x, const float* sc, const float* sh, const float* gb, int act, const Tiles* tiles,
+                      float* out, void* out16, cudaStream_t st) {
+  Tiles t{};
+  long long total = static_cast<long long>(x.n) * x.h * x.w * x.c;
+  if (tiles) {
+    t = *tiles;
+    total = static_cast<long long>(t.capacity) * t.bh * t.bw * x.c;
+  }
+  if (total == 0) return;
+  launch_pdl(k_spade_mod, dim3(grid_cap(total, 256)), dim3(256), st, x, sc, sh, gb, act, t, out,
+             static_cast<__half*>(out16));
+  after_launch("k_spade_mod");
 }
 
 }  // namespace sige_b200

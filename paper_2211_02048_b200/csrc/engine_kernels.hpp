@@ -226,6 +226,13 @@ void launch_add_h(const float* a, const float* b, float* out, void* out_h16, siz
 void launch_input_twin(const float* in, int n, int c, int h, int w, int c_pad, void* out, cudaStream_t st);
 // dst_h16 = fp16(src) elementwise (same layout).
 void launch_to_half(const float* src, void* dst_h16, size_t n, cudaStream_t st);
+// Config 3 (SPADE): nearest resize NCHW -> NHWC (+ fp16 twin padded to c16
+// channels; out or out16 may be null), and the SPADE modulation over tiles
+// (tiles != nullptr) or every pixel.
+void launch_resize_nhwc(const float* in, int n, int c, int H, int W, int h, int w, float* out, void* out16, int c16,
+                        cudaStream_t st);
+void launch_spade_mod(const Src& x, const float* sc, const float* sh, const float* gb, int act, const Tiles* tiles,
+                      float* out, void* out16, cudaStream_t st);
 // Layout conversions.
 void launch_nchw_to_nhwc(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);
 void launch_nhwc_to_nchw(const float* in, float* out, int n, int c, int h, int w, cudaStream_t st);

@@ -87,6 +87,7 @@ struct OwnedModel {
   std::string name;
   std::vector<sige_layer_desc> layers;
   std::vector<std::unique_ptr<std::vector<float>>> buffers;
+  std::vector<std::unique_ptr<sige_spade_desc[]>> spades;
 
   const float* keep(std::vector<float> v) {
     buffers.push_back(std::make_unique<std::vector<float>>(std::move(v)));
@@ -149,6 +150,38 @@ struct OwnedModel {
       L.has_shortcut = 1;
       L.shortcut = conv(r, ci, co, 1, 1);
     }
+    layers.push_back(L);
+  }
+  void add_resize(int h, int w) {
+    sige_layer_desc L = blank(SIGE_LAYER_RESIZE);
+    L.resize_h = h;
+    L.resize_w = w;
+    layers.push_back(L);
+  }
+  // SPADE residual block (SPADEResnetBlock of Park et al. 2019): fmiddle =
+  // min(fin, fout), learned 1x1 shortcut (no bias) when fin != fout, LeakyReLU(0.2),
+  // three SPADE norms (instance norm, nhidden-wide shared 3x3 + ReLU, 3x3 gamma/beta).
+  void add_spade_res(Rng& r, int fin, int fout, int label_nc, int nhidden) {
+    sige_layer_desc L = blank(SIGE_LAYER_SPADE_RESBLOCK);
+    const int fmid = std::min(fin, fout);
+    L.conv = conv(r, fin, fmid, 3, 1);
+    L.conv2 = conv(r, fmid, fout, 3, 1);
+    L.act = SIGE_ACT_LEAKY_RELU;
+    if (fin != fout) {
+      L.has_shortcut = 1;
+      L.shortcut = conv(r, fin, fout, 1, 1);
+      L.shortcut.bias = nullptr;
+    }
+    auto sp = std::make_unique<sige_spade_desc[]>(3);
+    const int chans[3] = {fin, fmid, fin};
+    for (int k = 0; k < (fin != fout ? 3 : 2); ++k) {
+      sp[k].eps = 1e-5f;
+      sp[k].shared = conv(r, label_nc, nhidden, 3, 1);
+      sp[k].gamma = conv(r, nhidden, chans[k], 3, 1);
+      sp[k].beta = conv(r, nhidden, chans[k], 3, 1);
+    }
+    L.spade = sp.get();
+    spades.push_back(std::move(sp));
     layers.push_back(L);
   }
   sige_model_desc* finish(const std::string& nm, int ci, int h, int w) {
@@ -216,7 +249,63 @@ sige_model_desc* build_ddim(OwnedModel* m, int res, int base) {
   return m->finish("ddim_stack", 3, res, res);
 }
 
+// GauGAN SPADE generator (BASELINE config 3; SPADEGenerator, Park et al. 2019,
+// "normal" upsampling): the segmentation map (label_nc channels) is resized to
+// (h/32, w/32) and mapped by a 3x3 conv to 16 nf channels, then 7 SPADE
+// residual blocks with nearest 2x upsampling between levels (16nf, 16nf, 16nf,
+// 8nf, 4nf, 2nf, nf), LeakyReLU(0.2) and a 3x3 conv to RGB (the final tanh is
+// a pointwise map on the result and not part of the sparse path). Random init,
+// Rng seed 3003.
+sige_model_desc* build_gaugan(OwnedModel* m, const std::string& name, int label_nc, int h, int w, int nf,
+                              int nhidden) {
+  Rng r(3003);
+  m->add_resize(h / 32, w / 32);
+  m->add_conv(r, label_nc, 16 * nf, 3, 1);
+  m->add_spade_res(r, 16 * nf, 16 * nf, label_nc, nhidden);  // head_0
+  m->add_up();
+  m->add_spade_res(r, 16 * nf, 16 * nf, label_nc, nhidden);  // G_middle_0
+  m->add_spade_res(r, 16 * nf, 16 * nf, label_nc, nhidden);  // G_middle_1
+  const int ch[5] = {16 * nf, 8 * nf, 4 * nf, 2 * nf, nf};
+  for (int i = 0; i < 4; ++i) {
+    m->add_up();
+    m->add_spade_res(r, ch[i], ch[i + 1], label_nc, nhidden);  // up_0 .. up_3
+  }
+  m->add_act(SIGE_ACT_LEAKY_RELU);
+  m->add_conv(r, nf, 3, 3, 1);  // conv_img
+  return m->finish(name, label_nc, h, w);
+}
+
 }  // namespace
+
+// A synthetic segmentation map (config 3): one-hot over label_nc classes of
+// random axis-aligned regions on a background class, and an edited copy where
+// a rect1-style square (fixtures.cpp:26-34, 1.2 % of the pixels) is relabelled
+// — the SIGE GauGAN edit (change the label of a region).
+void make_seg_fixture(int n, int label_nc, int h, int w, uint32_t seed, float* orig, float* edited) {
+  Rng r(seed);
+  std::vector<int> lab(static_cast<size_t>(h) * w, 0);
+  for (int k = 0; k < 12; ++k) {
+    const int cls = r.uniform_int(1, label_nc - 1);
+    const int he = r.uniform_int(h / 8, h / 2), we = r.uniform_int(w / 8, w / 2);
+    const int y0 = r.uniform_int(0, h - he), x0 = r.uniform_int(0, w - we);
+    for (int y = y0; y < y0 + he; ++y)
+      for (int x = x0; x < x0 + we; ++x) lab[static_cast<size_t>(y) * w + x] = cls;
+  }
+  Region g{h, w, std::vector<uint8_t>(static_cast<size_t>(h) * w, 0)};
+  square(g, r, 0.012 * h * w, 0, w);
+  const int new_cls = r.uniform_int(1, label_nc - 1);
+  for (int in = 0; in < n; ++in)
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        const size_t px = static_cast<size_t>(y) * w + x;
+        const int lo = lab[px], le = g.on[px] ? new_cls : lo;
+        for (int c = 0; c < label_nc; ++c) {
+          const size_t at = ((static_cast<size_t>(in) * label_nc + c) * h + y) * w + x;
+          orig[at] = c == lo ? 1.0f : 0.0f;
+          edited[at] = c == le ? 1.0f : 0.0f;
+        }
+      }
+}
 
 void make_edit_fixture(const std::string& kind, int n, int c, int h, int w, uint32_t seed,
                        float* orig, float* edited) {
@@ -285,10 +374,14 @@ sige_model_desc* build_model(const std::string& name) {
     d = build_ddim(m.get(), 256, 128);
   } else if (name == "ddim_stack_64x32") {
     d = build_ddim(m.get(), 64, 32);
+  } else if (name == "gaugan_spade") {  // BASELINE config 3: Cityscapes 256x512, 36 labels, nf 64
+    d = build_gaugan(m.get(), name, 36, 256, 512, 64, 128);
+  } else if (name == "gaugan_spade_mini") {  // the same generator at 64x128, nf 8 (tests)
+    d = build_gaugan(m.get(), name, 8, 64, 128, 8, 16);
   } else {
     throw ConfigError("unknown model: " + name +
                       " (expected one of conv3x3_128, mini_unet_gn, mini_unet_bn, gaugan_stack_in,"
-                      " single_conv64, ddim_stack, ddim_stack_64x32)");
+                      " single_conv64, ddim_stack, ddim_stack_64x32, gaugan_spade, gaugan_spade_mini)");
   }
   m.release();
   return d;
@@ -358,6 +451,26 @@ uint64_t model_structure_hash(const sige_model_desc* d) {
         if (has_sc) h = sconv(L.shortcut, h);
         break;
       }
+      case SIGE_LAYER_RESIZE: {
+        const int rs[2] = {L.resize_h, L.resize_w};
+        h = fnv1a64(rs, sizeof(rs), h);
+        break;
+      }
+      case SIGE_LAYER_SPADE_RESBLOCK: {  // no reference counterpart: the same scheme over every weight
+        h = sconv(L.conv, h);
+        h = sconv(L.conv2, h);
+        h = fnv1a64(&L.act, sizeof(L.act), h);
+        const int has_sc = L.has_shortcut ? 1 : 0;
+        h = fnv1a64(&has_sc, sizeof(has_sc), h);
+        if (has_sc) h = sconv(L.shortcut, h);
+        for (int k = 0; k < (has_sc ? 3 : 2); ++k) {
+          h = fnv1a64(&L.spade[k].eps, sizeof(float), h);
+          h = sconv(L.spade[k].shared, h);
+          h = sconv(L.spade[k].gamma, h);
+          h = sconv(L.spade[k].beta, h);
+        }
+        break;
+      }
       default:
         break;
     }
@@ -382,6 +495,16 @@ uint64_t model_weight_hash(const sige_model_desc* d) {  // models.cpp:185-207
         h = hnorm(L.norm, h);
         h = hconv(L.conv2, h);
         if (L.has_shortcut) h = hconv(L.shortcut, h);
+        break;
+      case SIGE_LAYER_SPADE_RESBLOCK:
+        h = hconv(L.conv, h);
+        h = hconv(L.conv2, h);
+        if (L.has_shortcut) h = hconv(L.shortcut, h);
+        for (int k = 0; k < (L.has_shortcut ? 3 : 2); ++k) {
+          h = hconv(L.spade[k].shared, h);
+          h = hconv(L.spade[k].gamma, h);
+          h = hconv(L.spade[k].beta, h);
+        }
         break;
       default:
         break;
@@ -448,6 +571,44 @@ std::vector<LayerShape> walk_shapes(const sige_model_desc* m) {  // graph.cpp:12
         h *= 2;
         w *= 2;
         break;
+      case SIGE_LAYER_RESIZE:
+        if (L.resize_h < 1 || L.resize_w < 1) fail("resize to a non-positive size");
+        if ((L.resize_h <= h ? h % L.resize_h : L.resize_h % h) || (L.resize_w <= w ? w % L.resize_w : L.resize_w % w))
+          fail("resize by a non-integer factor");
+        h = L.resize_h;
+        w = L.resize_w;
+        break;
+      case SIGE_LAYER_SPADE_RESBLOCK: {
+        check_conv(L.conv, i);
+        check_conv(L.conv2, i);
+        if (L.conv.k != 3 || L.conv.stride != 1 || L.conv2.k != 3 || L.conv2.stride != 1)
+          fail("spade block convs must be 3x3 stride 1");
+        if (L.conv.c_in != c || L.conv2.c_in != L.conv.c_out) fail("spade block channel mismatch");
+        if (!L.spade) fail("spade block without SPADE norms");
+        if (L.has_shortcut) {
+          check_conv(L.shortcut, i);
+          if (L.shortcut.k != 1 || L.shortcut.c_in != c || L.shortcut.c_out != L.conv2.c_out)
+            fail("spade block shortcut mismatch");
+        } else if (L.conv2.c_out != c) {
+          fail("identity shortcut requires c_in == c_out");
+        }
+        const int chans[3] = {c, L.conv.c_out, c};
+        for (int k = 0; k < (L.has_shortcut ? 3 : 2); ++k) {
+          const sige_spade_desc& sp = L.spade[k];
+          check_conv(sp.shared, i);
+          check_conv(sp.gamma, i);
+          check_conv(sp.beta, i);
+          if (sp.shared.k != 3 || sp.gamma.k != 3 || sp.beta.k != 3 || sp.shared.stride != 1 || sp.gamma.stride != 1 ||
+              sp.beta.stride != 1)
+            fail("SPADE convs must be 3x3 stride 1");
+          if (sp.shared.c_in != m->in_channels) fail("SPADE shared conv must read the segmentation map");
+          if (sp.gamma.c_in != sp.shared.c_out || sp.beta.c_in != sp.shared.c_out) fail("SPADE hidden width");
+          if (sp.gamma.c_out != chans[k] || sp.beta.c_out != chans[k]) fail("SPADE modulation channels");
+          if (!(sp.eps > 0.0f)) fail("SPADE eps must be > 0");
+        }
+        c = L.conv2.c_out;
+        break;
+      }
       default:
         fail("unknown layer kind");
     }
@@ -469,6 +630,8 @@ int required_dilation(const sige_model_desc* m) {  // graph.cpp:195-218
       g += ((L.conv.k - 1) / 2) * f;
     else if (L.kind == SIGE_LAYER_RESBLOCK)
       g += ((L.conv.k - 1) / 2 + (L.conv2.k - 1) / 2) * f;
+    else if (L.kind == SIGE_LAYER_SPADE_RESBLOCK)  // segmentation -> shared -> gamma/beta -> conv_0 -> conv_1
+      g += 4 * f;
   }
   return g;
 }

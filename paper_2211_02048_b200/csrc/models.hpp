@@ -16,6 +16,8 @@ uint64_t fnv1a64(const void* data, size_t bytes, uint64_t seed = kFnvSeed);
 void make_edit_fixture(const std::string& kind, int n, int c, int h, int w, uint32_t seed,
                        float* orig, float* edited);
 sige_model_desc* build_model(const std::string& name);
+// Config 3 inputs: one-hot segmentation map and its edit (a relabelled 1.2 % square).
+void make_seg_fixture(int n, int label_nc, int h, int w, uint32_t seed, float* orig, float* edited);
 void free_model(sige_model_desc* d);
 uint64_t model_weight_hash(const sige_model_desc* d);
 uint64_t model_structure_hash(const sige_model_desc* d);  // ModelSpec::structure_hash (graph.cpp:89-127)

@@ -141,3 +141,54 @@ def test_gpu_resize_nearest_and_config3_shape(orc):
         assert np.array_equal(host(sb.resize_nearest(cu(lab), oh, ow)), orc.resize_nearest(lab, oh, ow))
     with pytest.raises(sb.ConfigError, match="resize_nearest: non-integer scale"):
         sb.resize_nearest(cu(lab), 48, 64)
+
+
+def test_spade_oracle_matches_torch_functional():
+    """oracle/spade.py (numpy float64) against an independent statement of the
+    published SPADE generator in torch.nn.functional (conv2d, instance_norm,
+    interpolate nearest, leaky_relu), on the config-3 mini generator."""
+    import torch.nn.functional as F
+
+    from oracle import spade as osp
+
+    m = sb.Model("gaugan_spade_mini")
+    c, h, w = m.in_shape
+    orig, _ = sb.make_seg_fixture(1, c, h, w, 5)
+    d = m.desc.contents
+
+    def cw(cd):
+        wt, b, s = osp.conv_weights(cd)
+        return torch.from_numpy(wt), None if b is None else torch.from_numpy(b), s
+
+    def conv(x, cd):
+        wt, b, s = cw(cd)
+        return F.conv2d(x, wt, b, stride=s, padding=(wt.shape[-1] - 1) // 2)
+
+    def spade(x, seg, sd):
+        segk = F.interpolate(seg, size=x.shape[2:], mode="nearest")
+        a = F.relu(conv(segk, sd.shared))
+        return F.instance_norm(x, eps=sd.eps) * (1 + conv(a, sd.gamma)) + conv(a, sd.beta)
+
+    seg = orig.double()
+    x = seg
+    for i in range(d.num_layers):
+        L = d.layers[i]
+        if L.kind == osp.LAYER_RESIZE:
+            x = F.interpolate(seg, size=(L.resize_h, L.resize_w), mode="nearest")
+        elif L.kind == osp.LAYER_CONV:
+            x = conv(x, L.conv)
+        elif L.kind == osp.LAYER_UP:
+            x = F.interpolate(x, scale_factor=2, mode="nearest")
+        elif L.kind == osp.LAYER_ACT:
+            x = F.leaky_relu(x, 0.2)
+        else:
+            assert L.kind == osp.LAYER_SPADE
+            sp = L.spade
+            dx = conv(F.leaky_relu(spade(x, seg, sp[0]), 0.2), L.conv)
+            dx = conv(F.leaky_relu(spade(dx, seg, sp[1]), 0.2), L.conv2)
+            xs = conv(spade(x, seg, sp[2]), L.shortcut) if L.has_shortcut else x
+            x = xs + dx
+    want = x.numpy()
+    got = osp.forward(m.desc, orig.numpy())
+    assert got.shape == (1, 3, h, w)
+    assert np.abs(got - want).max() <= 1e-9 * np.abs(want).max()
