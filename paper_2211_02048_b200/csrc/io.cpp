@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <map>
 #include <sstream>
 #include <string>
@@ -101,48 +102,70 @@ void io_save_mask_pbm(const std::string& path, const uint8_t* m, int h, int w) {
 
 namespace {
 
-std::string next_pbm_token(std::istream& is, const std::string& path) {
-  std::string tok;
-  while (is >> tok) {
-    if (tok[0] == '#') {
-      std::string rest;
-      std::getline(is, rest);
-      continue;
+// The file is read whole and scanned by position (the reference streams it,
+// io.cpp:118-160; the accepted grammar and the error texts are the same).
+// Header fields are runs of non-space bytes; a field opening with '#' comments
+// out the rest of its line. Payload bits may be packed without separators.
+class PbmScanner {
+ public:
+  PbmScanner(std::string text, const std::string& path) : s_(std::move(text)), path_(path) {}
+
+  std::string field() {
+    for (;;) {
+      while (pos_ < s_.size() && is_space(s_[pos_])) ++pos_;
+      if (pos_ == s_.size()) throw ConfigError(path_ + ": truncated PBM file");
+      const size_t from = pos_;
+      while (pos_ < s_.size() && !is_space(s_[pos_])) ++pos_;
+      if (s_[from] != '#') return s_.substr(from, pos_ - from);
+      skip_line();
     }
-    return tok;
   }
-  throw ConfigError(path + ": truncated PBM file");
-}
+
+  // Fills up to n bits; returns how many were present.
+  size_t bits(uint8_t* out, size_t n) {
+    size_t got = 0;
+    while (got < n && pos_ < s_.size()) {
+      const char c = s_[pos_++];
+      if (c == '0' || c == '1') {
+        out[got++] = static_cast<uint8_t>(c - '0');
+      } else if (c == '#') {
+        skip_line();
+      } else if (!is_space(c)) {
+        throw ConfigError(path_ + ": unexpected character in PBM payload");
+      }
+    }
+    return got;
+  }
+
+ private:
+  static bool is_space(char c) { return std::isspace(static_cast<unsigned char>(c)) != 0; }
+  void skip_line() {
+    const size_t nl = s_.find('\n', pos_);
+    pos_ = nl == std::string::npos ? s_.size() : nl + 1;
+  }
+  std::string s_;
+  const std::string& path_;
+  size_t pos_ = 0;
+};
 
 }  // namespace
 
 // dims only when out == nullptr
 void io_load_mask_pbm(const std::string& path, int* h, int* w, uint8_t* out, size_t cap) {
-  std::ifstream is(path);
+  std::ifstream is(path, std::ios::binary);
   if (!is) throw ConfigError(path + ": cannot open");
-  const std::string magic = next_pbm_token(is, path);
+  PbmScanner sc(std::string(std::istreambuf_iterator<char>(is), std::istreambuf_iterator<char>()), path);
+  const std::string magic = sc.field();
   if (magic != "P1") throw ConfigError(path + ": expected plain PBM (P1), got '" + magic + "'");
-  const int ww = std::stoi(next_pbm_token(is, path));
-  const int hh = std::stoi(next_pbm_token(is, path));
+  const int ww = std::stoi(sc.field());
+  const int hh = std::stoi(sc.field());
   if (ww < 1 || hh < 1) throw ConfigError(path + ": bad PBM dimensions");
   *h = hh;
   *w = ww;
   if (!out) return;
   const size_t n = static_cast<size_t>(hh) * ww;
   if (cap < n) throw ConfigError(path + ": output buffer too small");
-  size_t filled = 0;
-  char ch;
-  while (filled < n && is.get(ch)) {
-    if (ch == '0' || ch == '1') {
-      out[filled++] = ch == '1' ? 1 : 0;
-    } else if (ch == '#') {
-      std::string rest;
-      std::getline(is, rest);
-    } else if (!std::isspace(static_cast<unsigned char>(ch))) {
-      throw ConfigError(path + ": unexpected character in PBM payload");
-    }
-  }
-  if (filled != n) throw ConfigError(path + ": truncated PBM file");
+  if (sc.bits(out, n) != n) throw ConfigError(path + ": truncated PBM file");
 }
 
 // ------------------------------------------------------------ block stacks

@@ -95,7 +95,23 @@ def test_pbm_bytes_and_cross_load(refio, tmp_path):
     assert np.array_equal(back.reshape(m.shape), m)
 
 
-@pytest.mark.parametrize("text", ["P2\n2 2\n0 1 1 0\n", "P1\n2 2\n0 1 1\n", "P1\n2 2\n0 1 x 0\n", "P1\n0 2\n"])
+@pytest.mark.parametrize("text", ["P1 #c 9\n3 2 # w h\n1 0 1\n# mid-payload comment 1 1\n0 1 0\n",
+                                  "P1\n3 2\n101#x\n010", "#lead\nP1\n3\n2\n1\t0 1 0 1 0 1 1 1",
+                                  "P1\n3 2 101010"])
+def test_pbm_grammar_matches_reference(refio, tmp_path, text):
+    """Header comments, payload comments, packed / tab-separated bits, a missing
+    final newline and trailing extra bits load the same as the reference's."""
+    p = tmp_path / "g.pbm"
+    p.write_text(text)
+    h, w = _i(), _i()
+    want = np.empty(6, np.uint8)
+    _ok(refio, refio.ref_io_load_mask_pbm(str(p).encode(), want.ctypes.data, want.size, C.byref(h), C.byref(w)))
+    assert (h.value, w.value) == (2, 3)
+    assert np.array_equal(sb.load_mask_pbm(str(p)).numpy().reshape(-1), want)
+
+
+@pytest.mark.parametrize("text", ["P2\n2 2\n0 1 1 0\n", "P1\n2 2\n0 1 1\n", "P1\n2 2\n0 1 x 0\n", "P1\n0 2\n",
+                                  "P1\n2", "# only a comment\n", "P1\n2 2\n0 1 # 1 0\n"])
 def test_pbm_errors_match_reference(refio, tmp_path, text):
     p = tmp_path / "bad.pbm"
     p.write_text(text)
