@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--cpu-sample-edits", type=int, default=2)
     ap.add_argument("--cpu-single-thread", type=int, default=1, help="also time one 1-thread reference edit")
     ap.add_argument("--requests", type=int, default=64, help="config 5: independent requests over all ranks")
-    ap.add_argument("--group", type=int, default=8, help="config 5: requests per grouped engine")
+    ap.add_argument("--group", type=int, default=32, help="config 5: requests per grouped engine")
     ap.add_argument("--sweep", type=int, default=1, help="config 4: edit-area x block sweep (N=1)")
     ap.add_argument("--spade", type=int, default=1, help="config 3: GauGAN SPADE generator edit (N=1)")
     return ap.parse_args()

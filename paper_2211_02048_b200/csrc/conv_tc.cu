@@ -873,6 +873,10 @@ __device__ __forceinline__ bool addend_vectorizable(const Dst& d) {
                                d.addend.epi.num_steps == 0 && (d.addend.c & 3) == 0);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 __device__ __forceinline__ const float* aux_ptr(const Dst& d, size_t pix, int n, int y, int x, int oc0) {
   return d.mode == kAddSrc ? d.addend.ptr + ((static_cast<size_t>(n) * d.addend.h + y) * d.addend.w + x) * d.addend.c + oc0
                            : d.aux + pix + oc0;
@@ -1413,6 +1417,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (k / na) & 1; barrier 3 (producers + helpers) brackets the tables and
       // every chunk, so the producers arrive on bar_afull only after all
       // units of the chunk are transformed.
+      // While the producers fold the tables: pull item 0's epilogue operands
+      // (bias slice, this row's residual / addend pixel) into L2, so the
+      // epilogue's staging after the transform does not wait on HBM
+      // (measured 1 % per edit; SIGE_TC_DEBUG bit 32 turns it off for A/B).
+      if (!(p.dbg & 32)) {
+        const int slice0 = n_tile >> p.ks_log2, oc0 = rank * slice0, el = threadIdx.x - kEpiBase;
+        if (p.bias && el * 32 < slice0 && oc0 + el * 32 < p.c_out) prefetch_l2(p.bias + oc0 + el * 32);
+        const int mi0 = static_cast<int>((static_cast<float>(cid) + 0.5f) * inv_slices);
+        const int m0 = (warp & 3) * 32 + lane, t0 = m0 / p.Mt, r0 = m0 - t0 * p.Mt;
+        const int oy0 = r0 / p.P, ox0 = r0 - oy0 * p.P, g0 = mi0 * p.T + t0;
+        if (p.dst.mode != kStore && t0 < p.T && g0 < count && oy0 < p.tiles.bh && ox0 < p.tiles.bw) {
+          const int n0 = __ldg(p.tiles.idx + 3 * g0), y0 = __ldg(p.tiles.idx + 3 * g0 + 1) + oy0,
+                    x0 = __ldg(p.tiles.idx + 3 * g0 + 2) + ox0;
+          if (y0 < p.dst.h && x0 < p.dst.w && addend_vectorizable(p.dst)) {
+            const size_t pix0 = ((static_cast<size_t>(n0) * p.dst.h + y0) * p.dst.w + x0) * p.dst.c;
+            const int ni0 = cid - mi0 * n_slices;
+            for (int j = 0; j < slice0 && ni0 * n_tile + oc0 + j < p.c_out; j += 32)
+              prefetch_l2(aux_ptr(p.dst, pix0, n0, y0, x0, ni0 * n_tile + oc0 + j));
+          }
+        }
+      }
       asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));  // tables folded
       const int htid = kProdThreads + static_cast<int>(threadIdx.x) - kEpiBase;
       for (int k = 0; k < c_end - c_begin; ++k) {
@@ -1435,7 +1460,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // first item are still in flight — it pulls the epilogue's instructions
     // into the instruction caches off the critical path (measured: a CTA's
     // first item paid ~1-3 us more than its second for the same work).
-    bool dry = p.warm && cid < n_items;
+    // (not in helper layers: there the epilogue warps are busy until the
+    // transform ends, and a warm-up pass after it sits on the critical path —
+    // measured 2 % per edit; SIGE_TC_DEBUG bit 64 restores it for A/B)
+    bool dry = p.warm && cid < n_items && (!helpers || (p.dbg & 64));
     if (!dry) dep_wait(p.wait_ctr, p.wait_target);  // the destination / residual inputs were written by earlier kernels
     for (int item = cid; item < n_items;) {
       const int mi = static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices), ni = item - mi * n_slices;
