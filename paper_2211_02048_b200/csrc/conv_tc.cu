@@ -1258,6 +1258,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // before the previous conv started); the activations and GroupNorm
         // statistics below were produced by the previous kernel.
         if (threadIdx.x == 0) tl_mark(p, 54);
+        if (p.xform) {  // the fold's per-channel operands into L2 before the wait (prefetch: safe on produced data too)
+          const Src& s = p.src;
+          const int c_lo = c_begin * 64, c_hi = min(s.c, c_end * 64);
+          const float* fa = s.gn_stats ? s.gn_gamma : s.epi.scale[0];
+          const float* fb = s.gn_stats ? s.gn_beta : s.epi.shift[0];
+          const int rows = s.gn_stats || !s.epi.per_sample[0] ? 1 : s.n;
+          for (int j = c_lo + 32 * static_cast<int>(threadIdx.x); j < c_hi; j += 32 * kProdThreads)
+            for (int r = 0; r < rows; ++r) {
+              prefetch_l2(fa + r * s.c + j);
+              prefetch_l2(fb + r * s.c + j);
+            }
+        }
         dep_wait(p.wait_ctr, p.wait_target);  // the source / GroupNorm statistics were written by the previous kernel
         if (threadIdx.x == 0 && p.gtl) {
           unsigned long long t;
@@ -1276,26 +1288,48 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int c_lo = c_begin * 64, c_hi = min(s.c, c_end * 64);
           const int span = c_hi - c_lo;
           const int cpg = s.gn_stats ? s.c / s.gn_groups : 1;
-          for (int i = threadIdx.x; i < s.n * span; i += kProdThreads) {
-            const int n = i / span, c = c_lo + (i - n * span);
-            float sc, sh;
-            if (s.gn_stats) {
-              const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + c / cpg);
-              const double mean = st[0] * p.gn_inv_count;
-              const float var = fmaxf(static_cast<float>(st[1] * p.gn_inv_count - mean * mean), 0.0f);
-              sc = __ldg(s.gn_gamma + c) * rsqrtf(var + s.gn_eps);
-              sh = fmaf(-static_cast<float>(mean), sc, __ldg(s.gn_beta + c));
-            } else {
-              const int off = s.epi.per_sample[0] ? n * s.c + c : c;
-              sc = __ldg(s.epi.scale[0] + off);
-              sh = __ldg(s.epi.shift[0] + off);
+          // Four entries per thread per round: every round's loads are issued
+          // before any is used (one L2 round trip per round, not per entry).
+          const int total = s.n * span;
+          for (int i0 = threadIdx.x; i0 < total; i0 += 4 * kProdThreads) {
+            double m1[4], m2[4];
+            float ga[4], be[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * kProdThreads;
+              if (i >= total) continue;
+              const int n = i / span, c = c_lo + (i - n * span);
+              if (s.gn_stats) {
+                const double* st = s.gn_stats + 2 * (static_cast<size_t>(n) * s.gn_groups + c / cpg);
+                m1[u] = st[0];
+                m2[u] = st[1];
+                ga[u] = __ldg(s.gn_gamma + c);
+                be[u] = __ldg(s.gn_beta + c);
+              } else {
+                const int off = s.epi.per_sample[0] ? n * s.c + c : c;
+                ga[u] = __ldg(s.epi.scale[0] + off);
+                be[u] = __ldg(s.epi.shift[0] + off);
+              }
             }
-            if (p.xf_act == SIGE_ACT_SILU) {  // halved for the transform's SiLU form (exact: power of two)
-              sc *= 0.5f;
-              sh *= 0.5f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * kProdThreads;
+              if (i >= total) continue;
+              const int n = i / span, c = c_lo + (i - n * span);
+              float sc = ga[u], sh = be[u];
+              if (s.gn_stats) {
+                const double mean = m1[u] * p.gn_inv_count;
+                const float var = fmaxf(static_cast<float>(m2[u] * p.gn_inv_count - mean * mean), 0.0f);
+                sc = ga[u] * rsqrtf(var + s.gn_eps);
+                sh = fmaf(-static_cast<float>(mean), sc, be[u]);
+              }
+              if (p.xf_act == SIGE_ACT_SILU) {  // halved for the transform's SiLU form (exact: power of two)
+                sc *= 0.5f;
+                sh *= 0.5f;
+              }
+              xf_scale[n * s.c + c] = sc;
+              xf_shift[n * s.c + c] = sh;
             }
-            xf_scale[n * s.c + c] = sc;
-            xf_shift[n * s.c + c] = sh;
           }
           asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads));
           // helpers (epilogue warps) transform item 0 with us: tables ready
