@@ -389,10 +389,11 @@ def test_scatter_rejects_incompatible_indices_like_reference():
 
 @pytest.mark.parametrize("win_b,n,c,h,w", [(6, 2, 70, 36, 44), (2, 1, 5, 16, 12), (6, 1, 33, 20, 20)])
 def test_gather_tma_boxes_match_oracle(orc, win_b, n, c, h, w):
-    """The TMA-box gather (8x8 / 4x4 windows, W % 4 == 0): ragged channel
-    slices, tiles at every fringe (negative window origins zero-filled by the
-    tensor map), per-sample epilogue with SiLU on in-canvas cells only —
-    bit-exact vs the oracle, with and without the epilogue."""
+    """Gather at the shapes of the (measured slower and removed) TMA-box
+    variant — 8x8 / 4x4 windows, W % 4 == 0: ragged channel slices, tiles at
+    every fringe (negative window origins zero-filled), per-sample epilogue
+    with SiLU on in-canvas cells only — bit-exact vs the oracle, with and
+    without the epilogue."""
     rng = np.random.default_rng(win_b * 1000 + c)
     x = rng.uniform(-3, 3, (n, c, h, w)).astype(np.float32)
     b = win_b

@@ -80,10 +80,16 @@ def main():
     base = int(rows[0][0], 16)
     by_role = collections.Counter()
     by_rr = collections.defaultdict(collections.Counter)
+    by_line = collections.Counter()
+    ex_line = collections.Counter()
+    ei = h.index("Instructions Executed") if "Instructions Executed" in h else None
     for x in rows:
         line = amap.get(int(x[0], 16) - base)
         ro = role(line) if line else "unmapped"
         by_role[ro] += num(x[si])
+        by_line[line] += num(x[si])
+        if ei is not None:
+            ex_line[line] += num(x[ei])
         for c in sc:
             by_rr[ro][h[c][6:]] += num(x[c])
     tot = sum(by_role.values())
@@ -91,6 +97,18 @@ def main():
     for ro, v in by_role.most_common():
         top = ", ".join(f"{k} {w:.0f}" for k, w in by_rr[ro].most_common(5))
         print(f"{ro:14s} {v:7.0f} {100 * v / max(tot, 1):5.1f}%  [{top}]")
+    if len(sys.argv) > 4:
+        src = open(SRC).read().split("\n")
+        n = int(sys.argv[4])
+        ex_tot = sum(ex_line.values())
+        print(f"top source lines (stall samples; warp instructions executed of {ex_tot:.0f}):")
+        for line, v in by_line.most_common(n):
+            text = src[line - 1].strip()[:90] if line else "?"
+            print(f"  {line}: {v:6.0f} {ex_line[line]:10.0f}  {text}")
+        print("top source lines by instructions executed:")
+        for line, v in ex_line.most_common(n):
+            text = src[line - 1].strip()[:90] if line else "?"
+            print(f"  {line}: {v:10.0f} {by_line[line]:6.0f}  {text}")
 
 
 if __name__ == "__main__":
