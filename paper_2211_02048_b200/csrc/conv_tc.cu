@@ -1077,6 +1077,13 @@ struct MmaCtx {
 template <bool F16, int K, int S, int TPS>
 __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_chunk) {
   static_assert((K * K) % TPS == 0, "taps per stage must divide the tap count");
+  // One election per chunk: the converged warp keeps the same leader lane, so
+  // the chunk's MMAs are one straight run of UTCHMMA with their descriptors in
+  // uniform registers — ~3 instructions per MMA instead of ~19 with an
+  // elect.sync per MMA (the issuing warp was ~80 % instruction-fetch stalled;
+  // measured 6.5 % per config-2 edit, profiles/r2_mma_lean_ab.txt). The
+  // 14-bit start-field wrap is kept (the TF32 path depends on it).
+  const bool leader = elect_one();
 #pragma unroll
   for (int tg = 0; tg < K * K / TPS; ++tg) {
     mbar_wait(&c.bar_bfull[c.bslot], c.bphase);
@@ -1093,13 +1100,13 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
       const uint32_t boff = bbase + static_cast<uint32_t>(tt) * c.tap_b16;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of K = 32 bytes each
+        const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
         const uint64_t ad = c.adesc0 | static_cast<uint64_t>((aoff + kk * c.kstep16) & 0x3FFFu);
         const uint64_t bd = c.bdesc0 | static_cast<uint64_t>((boff + kk * 2) & 0x3FFFu);
-        const uint32_t accum = (!first_chunk || tap != 0 || kk != 0) ? 1u : 0u;
-        if (elect_one()) umma<F16>(c.tmem_d, ad, bd, c.idesc, accum);
+        if (leader) umma<F16>(c.tmem_d, ad, bd, c.idesc, accum);
       }
     }
-    if (elect_one()) umma_commit(&c.bar_bempty[c.bslot]);
+    if (leader) umma_commit(&c.bar_bempty[c.bslot]);
     if (++c.bslot == c.nb) {
       c.bslot = 0;
       c.bphase ^= 1;
@@ -1660,8 +1667,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ops.has_aux = b == 0 && pre_aux && ni * n_tile + own0 + 16 <= p.c_out;
 #pragma unroll
           for (int j = 0; j < 16; ++j) ops.aux[j] = aux_next[j];
+          if (threadIdx.x == kEpiBase && it == 0 && b == 0 && !dry) tl_mark(p, 58);
           if (valid || dry) out16(p, pix, n, y, x, ni * n_tile + own0 + b * 16, tot, wv, ops, dry);
+          if (threadIdx.x == kEpiBase && it == 0 && b == 0 && !dry) tl_mark(p, 59);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, ni * n_tile + own0 + b * 16, n, valid || dry, wv, dry);
+          if (threadIdx.x == kEpiBase && it == 0 && b == 0 && !dry) tl_mark(p, 62);
           if (dry) break;
         }
         // Slots free again — only needed when another item follows (its
