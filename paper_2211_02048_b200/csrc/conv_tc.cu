@@ -410,6 +410,23 @@ __device__ __forceinline__ float tc_act(float v, int kind) {
   return v;
 }
 
+// CNT values through one activation: the (warp-uniform) kind is tested once
+// per vector, so a layer runs only its own activation's instructions (a
+// per-element tc_act was if-converted into all three bodies per element).
+template <int CNT>
+__device__ __forceinline__ void tc_act_vec(float* v, int kind) {
+  if (kind == SIGE_ACT_SILU) {
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) v[j] = __fdividef(v[j], 1.0f + __expf(-v[j]));
+  } else if (kind == SIGE_ACT_RELU) {
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+  } else if (kind == SIGE_ACT_LEAKY_RELU) {
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) v[j] = v[j] > 0.0f ? v[j] : __fmul_rn(0.2f, v[j]);
+  }
+}
+
 __device__ __forceinline__ float tc_epi(const DevEpilogue& e, float v, int ch, int channels, int n) {
 #pragma unroll
   for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
@@ -431,9 +448,7 @@ __device__ __forceinline__ void tc_epi_vec(const DevEpilogue& e, float* v, int c
   for (int s = 0; s < SIGE_MAX_EPI_STEPS; ++s) {
     if (s >= e.num_steps) break;
     if (e.kind[s] == SIGE_EPI_ACTIVATION) {
-      const int k = e.act[s];
-#pragma unroll
-      for (int j = 0; j < CNT; ++j) v[j] = tc_act(v[j], k);
+      tc_act_vec<CNT>(v, e.act[s]);
     } else {
       const int off = e.per_sample[s] ? n * channels + ch0 : ch0;
       if ((off & 3) == 0) {
@@ -951,11 +966,7 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
     if (ops.ssc) {  // [SS (staged), ACT...]
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(__fmul_rn(ops.ssc[j], v[j]), ops.ssh[j]);
-      for (int s2 = 1; s2 < d.act_epi.num_steps; ++s2) {
-        const int k = d.act_epi.act[s2];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = tc_act(v[j], k);
-      }
+      for (int s2 = 1; s2 < d.act_epi.num_steps; ++s2) tc_act_vec<16>(v, d.act_epi.act[s2]);
     } else {
       tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
     }
