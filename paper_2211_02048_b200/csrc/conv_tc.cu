@@ -83,6 +83,7 @@ constexpr int kMaxNB = 16;         // B (weight) ring slots (max)
 constexpr int kMaxNTile = 256;     // accumulator columns per TMEM buffer
 constexpr int kTmemCols = 2 * kMaxNTile;  // two accumulators: epilogue of item i overlaps MMA of item i+1
 constexpr int kGtlLaunchesDev = 1024;  // == kGtlLaunches (timeline buffer layout)
+constexpr int kMarkStride = 64 + 3 * 160;  // marks build: CTA 0's 64 phase marks + (start, wait, end) of CTAs 0..159
 constexpr int kDynSmem = 222 * 1024;  // dynamic shared memory per CTA (+ ~4 KB static, 227 KB cap)
 constexpr int kBatch = 4;          // 16-byte groups staged per thread per batch (synchronous path)
 
@@ -149,7 +150,15 @@ __device__ __forceinline__ void tl_mark(const TcParams& p, int idx) {
   } else if (p.gtl_marks && blockIdx.x == 0) {  // graph-safe phase marks of CTA 0 (SIGE_TC_GTL)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.gtl_marks[p.gtl_idx * 64 + idx] = t;
+    p.gtl_marks[p.gtl_idx * kMarkStride + idx] = t;
+  }
+}
+// Per-CTA (start, dependency-wait exit, end) stamps of every launch (marks build).
+__device__ __forceinline__ void tl_cta_stamp(const TcParams& p, int which) {
+  if (p.gtl_marks && blockIdx.x < 160) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.gtl_marks[p.gtl_idx * kMarkStride + 64 + 3 * blockIdx.x + which] = t;
   }
 }
 __device__ __forceinline__ void tl_cta(const TcParams& p, int base) {
@@ -164,6 +173,7 @@ __device__ __forceinline__ void tl_clock(const TcParams& p, int idx) {
 }
 #else
 __device__ __forceinline__ void tl_mark(const TcParams&, int) {}
+__device__ __forceinline__ void tl_cta_stamp(const TcParams&, int) {}
 __device__ __forceinline__ void tl_cta(const TcParams&, int) {}
 __device__ __forceinline__ void tl_clock(const TcParams&, int) {}
 #endif
@@ -398,15 +408,27 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 // ----------------------------------------------------- element-wise chain --
 // Chains evaluated inside this kernel (pending GroupNorm scale-shift + act on
 // staged values, act buffers written by the epilogue) run in the tensor-core
-// modes only, whose operands carry 10-bit mantissas: SiLU uses __expf and the
+// modes only, whose operands carry 10-bit mantissas: SiLU uses the approximate MUFU forms (silu_fast) and the
 // fast divide. Compile-time fast keeps the glibc-expf + IEEE-divide body (the
 // exact mode's arithmetic) out of this kernel — with it every inlined chain
 // multiplied the kernel to >1 MB of SASS and the warp roles thrashed the
 // instruction cache (an epilogue with a chain ran 5x slower than without).
+// SiLU in the tensor-core modes: v * rcp(1 + 2^(-v log2 e)) with the
+// flush-to-zero approximate MUFU forms — 5 instructions; the kernel is built
+// without -ftz, so __expf / __fdividef carried denormal fix-ups (~17
+// instructions per element in ncu). Relative error ~2^-21, below the fp16 /
+// tf32 operand rounding of these modes.
+__device__ __forceinline__ float silu_fast(float v) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(v, -1.4426950408889634f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(1.0f, e)));
+  return __fmul_rn(v, r);
+}
+
 __device__ __forceinline__ float tc_act(float v, int kind) {
   if (kind == SIGE_ACT_RELU) return v > 0.0f ? v : 0.0f;
   if (kind == SIGE_ACT_LEAKY_RELU) return v > 0.0f ? v : __fmul_rn(0.2f, v);
-  if (kind == SIGE_ACT_SILU) return __fdividef(v, 1.0f + __expf(-v));
+  if (kind == SIGE_ACT_SILU) return silu_fast(v);
   return v;
 }
 
@@ -417,7 +439,7 @@ template <int CNT>
 __device__ __forceinline__ void tc_act_vec(float* v, int kind) {
   if (kind == SIGE_ACT_SILU) {
 #pragma unroll
-    for (int j = 0; j < CNT; ++j) v[j] = __fdividef(v[j], 1.0f + __expf(-v[j]));
+    for (int j = 0; j < CNT; ++j) v[j] = silu_fast(v[j]);
   } else if (kind == SIGE_ACT_RELU) {
 #pragma unroll
     for (int j = 0; j < CNT; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
@@ -1164,6 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (threadIdx.x == 0) {
     tl_mark(p, 0);
+    tl_cta_stamp(p, 0);
     tl_cta(p, 1024);
     tl_clock(p, 60);
   }
@@ -1294,7 +1317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
           atomicMin(p.gtl + 2 * kGtlLaunchesDev + p.gtl_idx, t);
         }
-        if (threadIdx.x == 0) tl_mark(p, 49);
+        if (threadIdx.x == 0) {
+          tl_mark(p, 49);
+          tl_cta_stamp(p, 1);
+        }
         if (early_a && threadIdx.x == 0) issue_a(0, c_begin, nt);  // slot 0, first use: no free-wait
         if (p.xform) {
           // Scale-shift table of the transform, for this CTA's input channels only
@@ -1873,6 +1899,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(p.gtl + 2 * p.gtl_idx + 1, t);
   }
+  if (threadIdx.x == 0) tl_cta_stamp(p, 2);
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kTmemCols)
@@ -1977,12 +2004,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 constexpr int kGtlLaunches = 1024;
 static const bool g_gtl_on = std::getenv("SIGE_TC_GTL") != nullptr;
 static unsigned long long* g_gtl_buf = nullptr;  // allocated at the first instrumented launch
-static unsigned long long* g_gtl_marks = nullptr;  // [launch][64] phase marks of CTA 0
+static unsigned long long* g_gtl_marks = nullptr;  // [launch][kMarkStride]: CTA 0's phase marks, per-CTA stamps
 static void gtl_reset() {
   std::vector<unsigned long long> init(3 * kGtlLaunches, ~0ull);  // [start, end] pairs, then wait-done
   for (int i = 0; i < kGtlLaunches; ++i) init[2 * i + 1] = 0;
   SIGE_CUDA(cudaMemcpy(g_gtl_buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
-  SIGE_CUDA(cudaMemset(g_gtl_marks, 0, 64 * kGtlLaunches * 8));
+  SIGE_CUDA(cudaMemset(g_gtl_marks, 0, static_cast<size_t>(kMarkStride) * kGtlLaunches * 8));
 }
 static int g_gtl_next = 0;
 
@@ -1990,7 +2017,7 @@ int debug_conv_marks(unsigned long long* out, int cap) {
   if (!g_gtl_marks) return 0;
   SIGE_CUDA(cudaDeviceSynchronize());
   const int n = std::min(cap, kGtlLaunches);
-  SIGE_CUDA(cudaMemcpy(out, g_gtl_marks, static_cast<size_t>(n) * 64 * 8, cudaMemcpyDeviceToHost));
+  SIGE_CUDA(cudaMemcpy(out, g_gtl_marks, static_cast<size_t>(n) * kMarkStride * 8, cudaMemcpyDeviceToHost));
   return n;
 }
 
@@ -2413,7 +2440,7 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
   } else if (g_gtl_on) {
     if (!g_gtl_buf) {
       SIGE_CUDA(cudaMalloc(&g_gtl_buf, 3 * kGtlLaunches * 8));
-      SIGE_CUDA(cudaMalloc(&g_gtl_marks, 64 * kGtlLaunches * 8));
+      SIGE_CUDA(cudaMalloc(&g_gtl_marks, static_cast<size_t>(kMarkStride) * kGtlLaunches * 8));
       gtl_reset();
     }
     p.gtl = g_gtl_buf;

@@ -39,7 +39,8 @@ a.record()
 eng.sparse_forward(ed, config=cfg, out=out)
 b.record()
 torch.cuda.synchronize()
-marks = (C.c_ulonglong * (64 * 1024))()
+STRIDE = 64 + 3 * 160  # conv_tc.cu kMarkStride
+marks = (C.c_ulonglong * (STRIDE * 1024))()
 lib.sige_debug_conv_marks(marks, 1024)
 n = lib.sige_debug_conv_timeline(buf, 1024)
 rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2], i) for i in range(n) if buf[3 * i + 1]]
@@ -62,7 +63,7 @@ print("CTA 0 phases (us): wait->A landed (22-49), MMAs (9-22), acc ready (5-9), 
 
 
 def mk(gi, k):
-    v = marks[gi * 64 + k]
+    v = marks[gi * STRIDE + k]
     return v if v else None
 
 
@@ -80,6 +81,8 @@ print("sums " + " ".join(f"{acc.get(j, 0.0):7.1f}" for j in range(6)))
 import json
 with open(os.environ.get("SIGE_TL_MARKS_OUT", "gpurun_out/tl_marks.json"), "w") as f:
     json.dump([{"slot": gi, "start": s_, "end": en, "wait": wd,
-                "marks": {k: marks[gi * 64 + k] for k in range(64) if marks[gi * 64 + k]}} for (s_, en, wd, gi) in rows], f)
+                "marks": {k: marks[gi * STRIDE + k] for k in range(64) if marks[gi * STRIDE + k]},
+                "ctas": [[marks[gi * STRIDE + 64 + 3 * c + j] for j in range(3)] for c in range(160)
+                         if marks[gi * STRIDE + 64 + 3 * c]]} for (s_, en, wd, gi) in rows], f)
 print(f"sum work {tot_work:.1f} us, sum handoff (incl. non-conv kernels) {tot_hand:.1f} us, "
       f"first->last {(rows[-1][1] - t0) / 1e3:.1f} us")
