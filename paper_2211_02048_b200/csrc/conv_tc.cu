@@ -977,7 +977,7 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
       }
     }
   }
-  if (!dry)
+  if (!dry && !d.no_main)
 #pragma unroll
     for (int j = 0; j < 16; j += 4) st4(o + j, v + j);
   if (d.gn_stats) {

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <tuple>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <sstream>
@@ -1398,9 +1399,13 @@ struct ProgramBuilder {
               epi_push_act(d1.act_epi, L.act);
               restore(wa, ca, em);
               mid = plain(wa);
+              // conv2 reads act1 only: W(conv1.out) is never read in this mode,
+              // so conv1 skips its fp32 store (2/3 of its epilogue bytes) and
+              // the buffer needs no restore.
+              d1.no_main = c1 % 16 == 0 && w1.c % 4 == 0 && !std::getenv("SIGE_KEEP_CONV1_OUT") ? 1 : 0;
             }
             add([eng, x0, tm, c1w, d1, fin, bind](cudaStream_t st) { eng->conv(bind(x0, fin), tm, c1w, d1, st); });
-            restore(w1, c1c, em);
+            if (!d1.no_main) restore(w1, c1c, em);
             if (reuse && E.use_act()) {
               // mid already reads W(act1)
             } else if (reuse) {

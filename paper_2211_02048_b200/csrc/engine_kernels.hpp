@@ -106,6 +106,10 @@ struct Dst {
   // zeroed by the caller) — the next layer folds them (Src::gn_stats).
   double* gn_stats = nullptr;
   int gn_groups = 0;
+  // Tensor-core conv only: skip the main (fp32) store — the value is consumed
+  // through `act` alone (conv1 of a ResBlock whose conv2 stages act1); needs
+  // c_out % 16 == 0 and c % 4 == 0 (the vector epilogue path).
+  int no_main = 0;
 };
 
 
