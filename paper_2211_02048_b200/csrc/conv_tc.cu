@@ -941,7 +941,13 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
   const size_t at = pix + oc0;
   if (p.bias) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], ops.sb[j]);
+    for (int j = 0; j < 16; j += 4) {  // 16-byte shared loads (ops.sb is 64-byte aligned)
+      const float4 b4 = *reinterpret_cast<const float4*>(ops.sb + j);
+      v[j] = __fadd_rn(v[j], b4.x);
+      v[j + 1] = __fadd_rn(v[j + 1], b4.y);
+      v[j + 2] = __fadd_rn(v[j + 2], b4.z);
+      v[j + 3] = __fadd_rn(v[j + 3], b4.w);
+    }
   }
   float* o = d.ptr + at;
   if (d.mode != kStore) {
@@ -987,7 +993,14 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
   if (d.act) {
     if (ops.ssc) {  // [SS (staged), ACT...]
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(__fmul_rn(ops.ssc[j], v[j]), ops.ssh[j]);
+      for (int j = 0; j < 16; j += 4) {
+        const float4 a4 = *reinterpret_cast<const float4*>(ops.ssc + j);
+        const float4 c4 = *reinterpret_cast<const float4*>(ops.ssh + j);
+        v[j] = __fadd_rn(__fmul_rn(a4.x, v[j]), c4.x);
+        v[j + 1] = __fadd_rn(__fmul_rn(a4.y, v[j + 1]), c4.y);
+        v[j + 2] = __fadd_rn(__fmul_rn(a4.z, v[j + 2]), c4.z);
+        v[j + 3] = __fadd_rn(__fmul_rn(a4.w, v[j + 3]), c4.w);
+      }
       for (int s2 = 1; s2 < d.act_epi.num_steps; ++s2) tc_act_vec<16>(v, d.act_epi.act[s2]);
     } else {
       tc_epi_vec<16>(d.act_epi, v, oc0, d.c, n);
@@ -1169,7 +1182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base;
   __shared__ int4 s_tile[16];  // producers' current item tiles: (n, window origin y, x, -); n = -1 empty slot
   __shared__ int16_t s_rown[kMaxARows];  // transform: sample of each staged A row, -1 = no pixel data
-  __shared__ float s_bias[kMaxNTile], s_asc[kMaxNTile], s_ash[kMaxNTile];  // epilogue operands of the item
+  __shared__ __align__(16) float s_bias[kMaxNTile];  // epilogue operands of the item (float4-read)
+  __shared__ __align__(16) float s_asc[kMaxNTile];
+  __shared__ __align__(16) float s_ash[kMaxNTile];
 
   uint8_t* abuf0 = smem;
   uint8_t* bbuf = smem + p.na * p.a_bytes;
