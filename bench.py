@@ -467,7 +467,7 @@ def parity_block(R, rm, ref_out, got, mask, cfg, final):
 
 
 def main_reference(args):
-    rank, world, _ = dist_env()
+    rank, world, _ = dist_env()  # the line's config names the same workload as the B200 arm
     if rank != 0:
         return
     import paper_2211_02048_b200 as sb
@@ -486,7 +486,8 @@ def main_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference Rng fixtures, seed 7)",
-        "config": {**CONFIG, "parallelism": "host threads (reference CPU path)"},
+        "config": {**CONFIG, "parallelism": f"request-sharded x{world} (no data-path collective)"},
+        "execution": "reference CPU path (oracle/_ref), host threads, rank 0 only",
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": nthreads, "kind": "reference",
                          "sample": f"{args.steps} sparse_forward edits of config 2 at SIGE_THREADS={nthreads}"},
         "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -503,9 +504,17 @@ def main_ours(args):
     import paper_2211_02048_b200 as sb
 
     rank, world, local = dist_env()
+    shared_gpu = False
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.device_count() >= world:  # (the same decision on every rank)
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            # fewer GPUs than ranks: a functional test of the N>1 path (ranks
+            # share a GPU over gloo); never a scaling number
+            shared_gpu = True
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -702,6 +711,7 @@ def main_ours(args):
                   sb.MATH_EXACT: "f32"}[math],
         "data": "synthetic (reference Rng fixtures + random-init weights, seed 2211)",
         "config": {**CONFIG, "parallelism": f"request-sharded x{world} (no data-path collective)"},
+        "execution": "B200 engine, one process per GPU" + (" (TEST: ranks share one GPU over gloo)" if shared_gpu else ""),
         "speedup_vs_dense": round(dense_ms / ms_per_step, 3),
         "dense_ms": round(dense_ms, 4),
         "dense_cudnn_ms": round(dense_torch, 4) if isinstance(dense_torch, float) else dense_torch,
