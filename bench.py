@@ -119,12 +119,14 @@ class ClockSampler:
 
 def conv_traffic():
     """DRAM bytes per k_conv_tc launch (read + write) from the committed ncu
-    capture of one sparse step (profiles/r1_conv_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_conv_traffic.json")) as f:
-            return json.load(f)["dram_bytes_per_launch"]
-    except Exception:
-        return None
+    capture of one sparse step (profiles/r2_conv_traffic.json, else r1), or None."""
+    for name in ("r2_conv_traffic.json", "r1_conv_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f)["dram_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
 def measured_peaks():
