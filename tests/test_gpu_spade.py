@@ -135,3 +135,24 @@ def test_output_coverage_rejects_spade(fx):
     eng.precompute(fx["orig"].cuda())
     with pytest.raises(Exception):
         eng.output_coverage(fx["edited"].cuda())
+
+
+def test_grouped_requests_equal_separate_engines(fx):
+    """Two SPADE requests (different label maps and edits) through one grouped
+    engine give each request's own single-engine result bit for bit (EXACT),
+    at the required dilation and at the default one."""
+    m = fx["m"]
+    _, label_nc, h, w = (1,) + m.in_shape
+    pairs = [sb.make_seg_fixture(1, label_nc, h, w, s) for s in (11, 12)]
+    r = m.required_dilation()
+    for cfg in (sb.default_config(dilate_full=r, dilate_scale=1, min_sparse_res=1), sb.default_config(min_sparse_res=1)):
+        singles = []
+        for o, e in pairs:
+            eng = sb.Engine(m, 1, sb.MATH_EXACT)
+            eng.precompute(o.cuda())
+            singles.append(eng.sparse_forward(e.cuda(), config=cfg).cpu())
+        geng = sb.Engine(m, 2, sb.MATH_EXACT)
+        geng.precompute(torch.cat([o for o, _ in pairs]).cuda())
+        got = geng.sparse_forward_grouped(torch.cat([e for _, e in pairs]).cuda(), config=cfg).cpu()
+        for i in range(2):
+            assert torch.equal(got[i:i + 1], singles[i])
