@@ -115,6 +115,7 @@ struct TcParams {
   // usable), N slices (n_pad / width), weight stages per chunk, ring slots.
   int w_nt[5], w_slices[5], w_tgroups[5], w_nb[5];
   float w_inv_slices[5];
+  float inv_tm, inv_mt, inv_p;  // 1 / (T * Mt), 1 / Mt, 1 / P: division-free row_info (exact for q < 2^20)
   int ks_log2;    // log2(ks)
   int c_lo[9];    // split-K chunk range of rank r: [c_lo[r], c_lo[r + 1])
   unsigned long long* tl;  // debug timeline (SIGE_TC_TIMELINE), nullptr normally
@@ -498,11 +499,13 @@ __device__ __forceinline__ void tc_epi_vec(const DevEpilogue& e, float* v, int c
 // (bit 31 = row carries window data). The item's tiles live in s_tile as
 // (n, window origin y, x). A staging unit is (row q, 16-byte channel group j).
 __device__ __forceinline__ int32_t row_info(const TcParams& p, int q) {
+  // (q + 0.5) * (1 / d) truncates to q / d for the small q, d here (float
+  // reciprocals from the host: no integer-division sequences in the prologue)
   const int tm = p.T * p.Mt;
-  const int ph = q / tm;
+  const int ph = static_cast<int>((static_cast<float>(q) + 0.5f) * p.inv_tm);
   const int rem = q - ph * tm;
-  const int t = rem / p.Mt, rr = rem - t * p.Mt;
-  const int pr = rr / p.P, pc = rr - pr * p.P;
+  const int t = static_cast<int>((static_cast<float>(rem) + 0.5f) * p.inv_mt), rr = rem - t * p.Mt;
+  const int pr = static_cast<int>((static_cast<float>(rr) + 0.5f) * p.inv_p), pc = rr - pr * p.P;
   const int wy = pr * p.s + (ph >> 1), wx = pc * p.s + (ph & 1);
   if (wy >= p.win_h || wx >= p.win_w) return 0;
   return static_cast<int32_t>(0x80000000u | (static_cast<uint32_t>(t) << 24) | (static_cast<uint32_t>(wy) << 12) |
@@ -1205,35 +1208,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     tl_cta(p, 1024);
     tl_clock(p, 60);
   }
-  for (int q = threadIdx.x; q < p.phases * p.T * p.Mt; q += blockDim.x) row_tab[q] = row_info(p, q);
-
   // The live tile count (IndexPlan output, complete before the previous conv
   // started) is the first dependent load: issue it before the setup work.
   const int count = p.tiles.count_dev ? *p.tiles.count_dev : p.tiles.count;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kMaxNB; ++i) {
-      mbar_init(&bar_bfull[i], 1);
-      mbar_init(&bar_bempty[i], 1);
+  // Prologue in parallel: the epilogue warps fill the row table while warp 0
+  // initialises the barriers (one lane each) and warp 2 allocates TMEM.
+  if (warp >= kEpiBase / 32)
+    for (int q = threadIdx.x - kEpiBase; q < p.phases * p.T * p.Mt; q += kEpiThreads) row_tab[q] = row_info(p, q);
+  if (threadIdx.x == kEpiBase) tl_mark(p, 3);
+  if (warp == 0) {
+    if (lane < kMaxNB) {
+      mbar_init(&bar_bfull[lane], 1);
+      mbar_init(&bar_bempty[lane], 1);
     }
-    for (int i = 0; i < p.na; ++i) {
+    if (lane >= 16 && lane - 16 < p.na) {
+      const int i = lane - 16;
       mbar_init(&bar_afull[i], p.tma_a && !p.xform ? 1 : kProdThreads);
       mbar_init(&bar_aland[i], 1);  // TMA + transform: the boxes landed (before the in-smem chain)
       mbar_init(&bar_afree[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_acc_full[i], 1);
-      mbar_init(&bar_acc_empty[i], kEpiThreads);
+    if (lane >= 24 && lane < 26) {
+      mbar_init(&bar_acc_full[lane - 24], 1);
+      mbar_init(&bar_acc_empty[lane - 24], kEpiThreads);
     }
-    mbar_init(&bar_red_full, 1);  // the owner's arrive.expect_tx; the peers' st.async complete the bytes
-    mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
-    if (p.tma_a && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
+    if (lane == 26) {
+      mbar_init(&bar_red_full, 1);  // the owner's arrive.expect_tx; the peers' st.async complete the bytes
+      mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
+      if (p.tma_a && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (lane == 0) tl_mark(p, 7);
   }
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (lane == 0) tl_mark(p, 8);
   }
   tc_fence_before();
   __syncthreads();
@@ -2174,6 +2185,9 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
     p.T = 1;
   }
   if (p.T > 16) throw ConfigError("conv (tensor core): more than 16 tiles per MMA");
+  p.inv_tm = 1.0f / static_cast<float>(p.T * p.Mt);
+  p.inv_mt = 1.0f / static_cast<float>(p.Mt);
+  p.inv_p = 1.0f / static_cast<float>(p.P);
   const int pad_rows = cw.k == 3 ? (cw.stride == 1 ? 2 * p.P + 2 : p.P + 1) : 0;
   int r_total = p.phases * p.T * p.Mt + pad_rows + 8;
   r_total = (r_total + 7) / 8 * 8 + 1;  // odd number of 16-byte rows spreads groups over banks
