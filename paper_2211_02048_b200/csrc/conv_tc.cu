@@ -1120,6 +1120,7 @@ struct MmaCtx {
   uint64_t* bar_bfull;
   uint64_t* bar_bempty;
   uint32_t bslot = 0, bphase = 0;
+  const TcParams* mark_p = nullptr;  // phase marks (marks build; first item only)
 };
 
 // All MMAs of one K chunk: K*K taps x 4 k-steps, one weight stage per TPS taps.
@@ -1136,6 +1137,7 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
 #pragma unroll
   for (int tg = 0; tg < K * K / TPS; ++tg) {
     mbar_wait(&c.bar_bfull[c.bslot], c.bphase);
+    if (first_chunk && tg == 0 && c.mark_p && (threadIdx.x & 31) == 0) tl_mark(*c.mark_p, 44);  // weights of the first stage landed
     __syncwarp();
     tc_fence_after();
     const uint32_t bbase = c.b0 + c.bslot * c.bstage16;
@@ -1843,6 +1845,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.idesc = idesc;
     c.bar_bfull = bar_bfull;
     c.bar_bempty = bar_bempty;
+#ifdef SIGE_TC_MARKS
+    c.mark_p = &p;
+#endif
     const uint32_t astage16 = static_cast<uint32_t>(p.a_bytes >> 4), na = static_cast<uint32_t>(p.na);
     uint32_t aslot = 0, aphase = 0, it = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
