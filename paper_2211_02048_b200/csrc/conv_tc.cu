@@ -924,7 +924,8 @@ __device__ __forceinline__ const float* aux_ptr(const Dst& d, size_t pix, int n,
 
 // dry: the warm-up pass — same instruction stream, no memory access.
 __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int y, int x, int oc0, float* v,
-                                      float* written, const EpiOps& ops, bool dry = false, int lim = 16) {
+                                      float* written, const EpiOps& ops, bool dry = false, int lim = 16,
+                                      bool mk = false) {
   const Dst& d = p.dst;
   const int cnt = min(lim, p.c_out - oc0);
   if (cnt <= 0) return;
@@ -986,9 +987,11 @@ __device__ __forceinline__ void out16(const TcParams& p, size_t pix, int n, int 
       }
     }
   }
+  if (mk) tl_mark(p, 45);  // value math done (marks build)
   if (!dry && !d.no_main)
 #pragma unroll
     for (int j = 0; j < 16; j += 4) st4(o + j, v + j);
+  if (mk) tl_mark(p, 63);  // main stores issued
   if (d.gn_stats) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) written[j] = v[j];
@@ -1657,7 +1660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) ops.aux[j] = aux_cur[j];
           ops.join = in_join;
           float wv[16];
-          if (valid || dry) out16(p, pix, n, y, x, oc, v, wv, ops, dry);
+          if (valid || dry) out16(p, pix, n, y, x, oc, v, wv, ops, dry, 16, !dry && it == 0 && cb == 0 && threadIdx.x == kEpiBase);
           if (p.dst.gn_stats) gn_accumulate(p.dst, p.c_out, oc, n, valid || dry, wv, dry);
           if (dry) break;
           if (threadIdx.x == kEpiBase && it == 0) tl_mark(p, 40 + min(cb >> 4, 3));
