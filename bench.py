@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-edits", type=int, default=2)
     ap.add_argument("--cpu-single-thread", type=int, default=1, help="also time one 1-thread reference edit")
+    ap.add_argument("--cpu-procs", type=int, default=1, help="also time nproc concurrent 1-thread reference processes")
     ap.add_argument("--requests", type=int, default=64, help="config 5: independent requests over all ranks")
     ap.add_argument("--group", type=int, default=32, help="config 5: requests per grouped engine")
     ap.add_argument("--sweep", type=int, default=1, help="config 4: edit-area x block sweep (N=1)")
@@ -441,6 +442,43 @@ def time_reference_edits(rm, cache, edited, mask, cfg, edits, outs=None):
     return ts
 
 
+def reference_procs(rm, cache, edited, mask, cfg, procs, timeout_s=120):
+    """The reference's best CPU throughput: `procs` independent
+    1-thread processes, one config-2 edit each, on the same (forked, read-only)
+    cache — the reference spawns threads per call, so process parallelism is
+    its throughput mode. Returns edits/s over the wall clock of the batch."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    os.environ["SIGE_THREADS"] = "1"
+
+    def work(q):
+        t0 = time.perf_counter()
+        rm.sparse_forward(cache, edited, mask, cfg)
+        q.put(time.perf_counter() - t0)
+        q.close()
+        q.join_thread()
+        os._exit(0)  # no interpreter / CUDA teardown in the forked child
+
+    try:
+        q = ctx.Queue()
+        ps = [ctx.Process(target=work, args=(q,)) for _ in range(procs)]
+        t0 = time.perf_counter()
+        for p in ps:
+            p.start()
+        per = [q.get(timeout=timeout_s) for _ in ps]
+        wall = time.perf_counter() - t0
+        for p in ps:
+            p.join(timeout=10)
+        return {"value": round(procs / wall, 4), "unit": "edits/s", "cores": procs, "kind": "reference",
+                "per_edit_s_median": round(sorted(per)[len(per) // 2], 3),
+                "sample": f"{procs} concurrent 1-thread processes (fork), one config-2 sparse_forward edit each"}
+    except Exception as e:  # report, never hide
+        return {"value": None, "unit": "edits/s", "cores": procs, "kind": "reference", "sample": f"unavailable: {e}"}
+    finally:
+        os.environ["SIGE_THREADS"] = str(os.cpu_count() or 1)
+
+
 def parity_block(R, rm, ref_out, got, mask, cfg, final):
     """The engine's edit vs the reference's sparse_forward on the same cache:
     normalised max error (north star: <= 1e-2), the SURVEY §8(c) elementwise
@@ -799,6 +837,8 @@ def main_ours(args):
                 os.environ["SIGE_THREADS"] = str(nthreads)
                 line["cpu_baseline_1thread"] = {"value": round(t1[0], 3), "unit": "ms", "cores": 1,
                                                 "kind": "reference", "sample": "1 sparse_forward edit of config 2"}
+            if args.cpu_procs:
+                line["cpu_baseline_procs"] = reference_procs(rm, cache, e2, m2, cfg, nthreads)
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"unavailable: {e}"}
