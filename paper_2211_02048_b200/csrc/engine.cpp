@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <set>
 #include <sstream>
 
 namespace sige_b200 {
@@ -737,6 +739,7 @@ Src Engine::spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg,
 void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
                         cudaStream_t st) {
   Src x = input;
+  std::map<std::string, Src> seg_done;  // SPADE label maps resized in this walk
   size_t dense_stats_used = 0;
   if (!capture && !reused && math_ == SIGE_MATH_F16) {
     if (!dense_stats_) {
@@ -787,9 +790,19 @@ void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, f
         break;
       }
       case SIGE_LAYER_SPADE_RESBLOCK: {
-        DevTensor& segb = scratch("dense.seg@" + std::to_string(sh.h_in) + "x" + std::to_string(sh.w_in), in_c_,
-                                  sh.h_in, sh.w_in, kNHWC);
-        const Src seg = seg_at(input.ptr, sh.h_in, sh.w_in, segb, st);
+        // the label map at this resolution: the input itself at full
+        // resolution (its fp16 twin already exists), else one resize per
+        // resolution and walk (blocks sharing a resolution reuse it)
+        Src seg;
+        if (sh.h_in == in_h_ && sh.w_in == in_w_) {
+          seg = input;
+        } else {
+          const std::string sk = "dense.seg@" + std::to_string(sh.h_in) + "x" + std::to_string(sh.w_in);
+          DevTensor& segb = scratch(sk, in_c_, sh.h_in, sh.w_in, kNHWC);
+          auto hit = seg_done.find(sk);
+          if (hit == seg_done.end()) hit = seg_done.emplace(sk, seg_at(input.ptr, sh.h_in, sh.w_in, segb, st)).first;
+          seg = hit->second;
+        }
         auto tensor = [&](const std::string& sfx, int c, int half) -> DevTensor& {
           return capture ? cache_slot(step, key + sfx, c, sh.h_in, sh.w_in, kNHWC, half)
                          : scratch("dense." + key + sfx, c, sh.h_in, sh.w_in, kNHWC, half);
@@ -1088,6 +1101,7 @@ struct ProgramBuilder {
     bool has_blocks = false;
     int blocks_entry = -1;
     Engine* eng = &E;
+    std::set<std::string> seg_keys;  // SPADE label-map resolutions already resized in this program
     // Source pointer resolution at launch time for steps that read the input.
     // The first layers read the per-call input (and, in F16, its fp16 twin
     // written by k_input_twin at the start of the call).
@@ -1186,10 +1200,16 @@ struct ProgramBuilder {
           const Src x0 = flow;
           const int li = static_cast<int>(i);
           const int c16 = (E.in_c_ + 7) / 8 * 8;
-          DevTensor& segb =
-              E.scratch("sparse.seg@" + std::to_string(h) + "x" + std::to_string(w), E.in_c_, h, w, kNHWC);
-          if (E.math_ == SIGE_MATH_F16 && !segb.h16) segb.h16 = E.alloc(static_cast<size_t>(N) * h * w * c16 * 2);
+          // full resolution: the label map is the input itself (bound per call,
+          // fp16 twin from the call's input conversion); lower resolutions are
+          // resized once per call and resolution (blocks sharing one reuse it)
+          const bool seg_full = h == E.in_h_ && w == E.in_w_;
+          const std::string seg_key = "sparse.seg@" + std::to_string(h) + "x" + std::to_string(w);
+          DevTensor& segb = E.scratch(seg_key, E.in_c_, seg_full ? 1 : h, seg_full ? 1 : w, kNHWC);
+          if (!seg_full && E.math_ == SIGE_MATH_F16 && !segb.h16)
+            segb.h16 = E.alloc(static_cast<size_t>(N) * h * w * c16 * 2);
           const DevTensor segc = segb;
+          const bool seg_new = !seg_full && seg_keys.insert(seg_key).second;
           auto add_trace = [&](int entry_idx) {
             for (int k = 0; k < L.n_spade; ++k) {
               P.trace.push_back({entry_idx, L.spade_shared[k].c_in, L.spade_shared[k].c_out, 3, 1, h, w, N});
@@ -1203,9 +1223,11 @@ struct ProgramBuilder {
             // dense fallback with fresh statistics (as ResBlocks, graph.cpp:799-815)
             DevTensor& sum = E.scratch("sparse." + key + ".sum", L.conv2.c_out, h, w, kNHWC);
             const LayerDev Lc = L;
-            add([eng, Lc, li, x0, fin, bind, segc, key](cudaStream_t st) {
+            Src in_seg = in_src;
+            in_seg.ptr = nullptr;
+            add([eng, Lc, li, x0, fin, bind, segc, key, seg_full, in_seg](cudaStream_t st) {
               DevTensor seg_buf = segc;
-              const Src seg = eng->seg_at(eng->cur_in_, x0.h, x0.w, seg_buf, st);
+              const Src seg = seg_full ? bind(in_seg, true) : eng->seg_at(eng->cur_in_, x0.h, x0.w, seg_buf, st);
               auto tensor = [&](const std::string& sfx, int c, int half) -> DevTensor& {
                 return eng->scratch("sparse." + key + sfx, c, x0.h, x0.w, kNHWC, half);
               };
@@ -1227,13 +1249,19 @@ struct ProgramBuilder {
               restore(wb, E.cache_tensor(step, key + sfx), em);
               return wb;
             };
-            add([eng, segc](cudaStream_t st) {  // this resolution's segmentation map
-              DevTensor seg_buf = segc;
-              eng->seg_at(eng->cur_in_, segc.h, segc.w, seg_buf, st);
-            });
+            if (seg_new) {
+              add([eng, segc](cudaStream_t st) {  // this resolution's segmentation map
+                DevTensor seg_buf = segc;
+                eng->seg_at(eng->cur_in_, segc.h, segc.w, seg_buf, st);
+              });
+            }
             Src seg = plain(segb);
             seg.twin = segb.h16;
             seg.twin_c = c16;
+            if (seg_full) {
+              seg = in_src;  // NCHW input + twin, pointers bound at launch
+              seg.ptr = nullptr;
+            }
             auto modulate = [&](int k, const Src& in, int act, bool in_is_input) -> Src {
               const std::string sk = ".spade" + std::to_string(k);
               DevTensor& a = W(sk + ".a");
@@ -1249,7 +1277,12 @@ struct ProgramBuilder {
               } else {
                 epi_push_act(as.epi, SIGE_ACT_RELU);
               }
-              conv_step(seg, tm, L.spade_shared[k], da);
+              {
+                const ConvW sw = L.spade_shared[k];
+                add([eng, seg, tm, sw, da, bind, seg_full](cudaStream_t st) {
+                  eng->conv(bind(seg, seg_full), tm, sw, da, st);
+                });
+              }
               DevTensor& gb = W(sk + ".gb");
               conv_step(as, tm, L.spade_gb[k], to_dst(gb));
               const DevNorm& nf = E.cache_norm(step, key + sk + ".norm");
