@@ -156,3 +156,16 @@ def test_grouped_requests_equal_separate_engines(fx):
         got = geng.sparse_forward_grouped(torch.cat([e for _, e in pairs]).cuda(), config=cfg).cpu()
         for i in range(2):
             assert torch.equal(got[i:i + 1], singles[i])
+
+
+def test_host_buffer_path_and_graph_replay(fx):
+    """The e2e entry point (host buffers, sige_engine_sparse_forward_host) and
+    repeated graph-replayed calls give the device call's bits (F16)."""
+    eng = sb.Engine(fx["m"], 1, sb.MATH_F16)
+    eng.precompute(fx["orig"].cuda())
+    cfg = sb.default_config(min_sparse_res=1)
+    want = eng.sparse_forward(fx["edited"].cuda(), config=cfg).cpu()
+    for _ in range(3):  # direct run, capture, replays
+        assert torch.equal(eng.sparse_forward(fx["edited"].cuda(), config=cfg).cpu(), want)
+    got = eng.sparse_forward_host(fx["edited"].pin_memory(), config=cfg)
+    assert torch.equal(got, want)
