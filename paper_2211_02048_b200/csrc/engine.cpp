@@ -206,6 +206,11 @@ Engine::Engine(const sige_model_desc* m, int batch, int math) : batch_(batch), m
     }
     layers_.push_back(L);
   }
+  for (const LayerDev& L : layers_)  // SPADE models: branch stream + events up front (never created under capture)
+    if (L.kind == SIGE_LAYER_SPADE_RESBLOCK) {
+      br_event(kBrDense + 3);
+      break;
+    }
 }
 
 Engine::~Engine() {
@@ -218,6 +223,8 @@ Engine::~Engine() {
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   if (cap_stream_) cudaStreamDestroy(cap_stream_);
   if (side_stream_) cudaStreamDestroy(side_stream_);
+  if (br_stream_) cudaStreamDestroy(br_stream_);
+  for (cudaEvent_t e : br_events_) cudaEventDestroy(e);
   if (fork_ev_) cudaEventDestroy(fork_ev_);
   if (join_ev_) cudaEventDestroy(join_ev_);
   for (void* p : allocations_) cudaFree(p);
@@ -689,9 +696,20 @@ Src Engine::spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg,
   (void)li;
   const int h = x.h, w = x.w;
   const Tiles t3 = dense_tiles(h, w, 3, 1), t1 = dense_tiles(h, w, 1, 1);
-  auto modulate = [&](int k, const Src& in, int act) -> Src {
+  // The label-map convs of the block's norms depend on seg only: they run on
+  // the branch stream (fork here, one event per norm, join at the end), so
+  // the gamma/beta of norm_s and norm_1 overlap conv_0 (as in the sparse program).
+  static const bool no_branch = std::getenv("SIGE_NO_SPADE_BRANCH") != nullptr;
+  const bool branch = !no_branch && br_stream_ != nullptr;
+  cudaStream_t bs = branch ? br_stream_ : st;
+  if (branch) {
+    SIGE_CUDA(cudaEventRecord(br_events_[kBrDense], st));
+    SIGE_CUDA(cudaStreamWaitEvent(bs, br_events_[kBrDense], 0));
+  }
+  DevTensor* gbt[3] = {nullptr, nullptr, nullptr};
+  auto label_convs = [&](int k, int C) {
     const std::string sk = ".spade" + std::to_string(k);
-    const int nh = L.spade_shared[k].c_out, C = in.c;
+    const int nh = L.spade_shared[k].c_out;
     DevTensor& a = tensor(sk + ".a", nh, 0);
     Dst da = to_dst(a);
     Src as = plain(a);
@@ -705,17 +723,26 @@ Src Engine::spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg,
     } else {
       epi_push_act(as.epi, SIGE_ACT_RELU);
     }
-    conv(seg, t3, L.spade_shared[k], da, st);
-    DevTensor& gb = tensor(sk + ".gb", 2 * C, 0);
-    conv(as, t3, L.spade_gb[k], to_dst(gb), st);
+    conv(seg, t3, L.spade_shared[k], da, bs);
+    gbt[k] = &tensor(sk + ".gb", 2 * C, 0);
+    conv(as, t3, L.spade_gb[k], to_dst(*gbt[k]), bs);
+    if (branch) SIGE_CUDA(cudaEventRecord(br_events_[kBrDense + 1 + k], bs));
+  };
+  label_convs(0, x.c);
+  if (L.has_shortcut) label_convs(2, x.c);
+  label_convs(1, L.conv.c_out);
+  auto modulate = [&](int k, const Src& in, int act) -> Src {
+    const std::string sk = ".spade" + std::to_string(k);
+    const int C = in.c;
     DevNorm& nf = norm(sk + ".norm", batch_ * C);
     if (!reused) {
       if (!gn_scratch_) gn_scratch_ = static_cast<double*>(alloc(kGnScratch * sizeof(double)));
       launch_gn_fold(in, C, L.spade_eps[k], L.spade_ones[k], L.spade_zeros[k], nf.scale, nf.shift, gn_scratch_,
                      kGnScratch, tensor_cores() ? 0 : 1, st);
     }
+    if (branch) SIGE_CUDA(cudaStreamWaitEvent(st, br_events_[kBrDense + 1 + k], 0));
     DevTensor& mod = tensor(sk + ".mod", C, 0);
-    launch_spade_mod(in, nf.scale, nf.shift, gb.p, act, nullptr, mod.p, mod.h16, st);
+    launch_spade_mod(in, nf.scale, nf.shift, gbt[k]->p, act, nullptr, mod.p, mod.h16, st);
     return plain(mod);
   };
   const Src m0 = modulate(0, x, L.act);
@@ -733,7 +760,7 @@ Src Engine::spade_dense(const LayerDev& L, int li, const Src& x, const Src& seg,
   Dst d = to_dst(sum, kAddSrc);
   d.addend = addend;
   conv(m1, t3, L.conv2, d, st);
-  return plain(sum);
+  return plain(sum);  // (every branch event was waited on by a modulation: joined)
 }
 
 void Engine::dense_walk(const Src& input, int step, bool capture, bool reused, float* out_nchw,
@@ -1011,6 +1038,29 @@ struct ProgramBuilder {
   Program& P;
   const sige_run_config& cfg;
   std::map<std::tuple<int, int, int>, int> memo;
+  size_t br_next = 0;    // next branch event
+  bool br_forked = false;  // the SPADE branch stream has forked from the main chain
+  static bool branch_on() {
+    static const bool off = std::getenv("SIGE_NO_SPADE_BRANCH") != nullptr;  // A/B: one serial chain
+    return !off;
+  }
+  // Branch helpers: fork once (after the IndexPlan), record / wait events.
+  void br_fork() {
+    if (br_forked) return;
+    br_forked = true;
+    Engine* eng = &E;
+    const cudaEvent_t ev = E.br_event(br_next++);
+    add([eng, ev](cudaStream_t st) {
+      SIGE_CUDA(cudaEventRecord(ev, st));
+      SIGE_CUDA(cudaStreamWaitEvent(eng->br_stream_, ev, 0));
+    }, 0);
+  }
+  cudaEvent_t br_record() {
+    Engine* eng = &E;
+    const cudaEvent_t ev = E.br_event(br_next++);
+    add([eng, ev](cudaStream_t) { SIGE_CUDA(cudaEventRecord(ev, eng->br_stream_)); }, 0);
+    return ev;
+  }
 
   int entry(int h, int w, int b) {  // IndexPlan::at (graph.cpp:517-528)
     auto key = std::make_tuple(h, w, b);
@@ -1209,7 +1259,7 @@ struct ProgramBuilder {
           if (!seg_full && E.math_ == SIGE_MATH_F16 && !segb.h16)
             segb.h16 = E.alloc(static_cast<size_t>(N) * h * w * c16 * 2);
           const DevTensor segc = segb;
-          const bool seg_new = !seg_full && seg_keys.insert(seg_key).second;
+          const bool branch = ProgramBuilder::branch_on();
           auto add_trace = [&](int entry_idx) {
             for (int k = 0; k < L.n_spade; ++k) {
               P.trace.push_back({entry_idx, L.spade_shared[k].c_in, L.spade_shared[k].c_out, 3, 1, h, w, N});
@@ -1225,8 +1275,17 @@ struct ProgramBuilder {
             const LayerDev Lc = L;
             Src in_seg = in_src;
             in_seg.ptr = nullptr;
-            add([eng, Lc, li, x0, fin, bind, segc, key, seg_full, in_seg](cudaStream_t st) {
-              DevTensor seg_buf = segc;
+            DevTensor segfb = seg_full ? segc
+                                       : E.scratch("sparse.segfb@" + std::to_string(h) + "x" + std::to_string(w),
+                                                   E.in_c_, h, w, kNHWC);
+            if (!seg_full && E.math_ == SIGE_MATH_F16 && !segfb.h16) {
+              DevTensor& sf = E.scratch("sparse.segfb@" + std::to_string(h) + "x" + std::to_string(w), E.in_c_, h,
+                                        w, kNHWC);
+              sf.h16 = E.alloc(static_cast<size_t>(N) * h * w * c16 * 2);
+              segfb = sf;
+            }
+            add([eng, Lc, li, x0, fin, bind, segfb, key, seg_full, in_seg](cudaStream_t st) {
+              DevTensor seg_buf = segfb;
               const Src seg = seg_full ? bind(in_seg, true) : eng->seg_at(eng->cur_in_, x0.h, x0.w, seg_buf, st);
               auto tensor = [&](const std::string& sfx, int c, int half) -> DevTensor& {
                 return eng->scratch("sparse." + key + sfx, c, x0.h, x0.w, kNHWC, half);
@@ -1249,10 +1308,12 @@ struct ProgramBuilder {
               restore(wb, E.cache_tensor(step, key + sfx), em);
               return wb;
             };
+            const bool seg_new = !seg_full && seg_keys.insert(seg_key).second;
+            if (branch) br_fork();
             if (seg_new) {
-              add([eng, segc](cudaStream_t st) {  // this resolution's segmentation map
+              add([eng, segc, branch](cudaStream_t st) {  // this resolution's segmentation map
                 DevTensor seg_buf = segc;
-                eng->seg_at(eng->cur_in_, segc.h, segc.w, seg_buf, st);
+                eng->seg_at(eng->cur_in_, segc.h, segc.w, seg_buf, branch ? eng->br_stream_ : st);
               });
             }
             Src seg = plain(segb);
@@ -1277,14 +1338,18 @@ struct ProgramBuilder {
               } else {
                 epi_push_act(as.epi, SIGE_ACT_RELU);
               }
-              {
-                const ConvW sw = L.spade_shared[k];
-                add([eng, seg, tm, sw, da, bind, seg_full](cudaStream_t st) {
-                  eng->conv(bind(seg, seg_full), tm, sw, da, st);
-                });
-              }
+              // the label-map convs (input only): on the branch stream
               DevTensor& gb = W(sk + ".gb");
-              conv_step(as, tm, L.spade_gb[k], to_dst(gb));
+              {
+                const ConvW sw = L.spade_shared[k], gw = L.spade_gb[k];
+                const Dst dgb = to_dst(gb);
+                add([eng, seg, tm, sw, da, bind, seg_full, as, gw, dgb, branch](cudaStream_t st) {
+                  cudaStream_t bs = branch ? eng->br_stream_ : st;
+                  eng->conv(bind(seg, seg_full), tm, sw, da, bs);
+                  eng->conv(as, tm, gw, dgb, bs);
+                }, 2);
+              }
+              const cudaEvent_t gb_ready = branch ? br_record() : nullptr;
               const DevNorm& nf = E.cache_norm(step, key + sk + ".norm");
               DevTensor& mod = W(sk + ".mod");
               const float* scp = nf.scale;
@@ -1292,7 +1357,8 @@ struct ProgramBuilder {
               const float* gbp = gb.p;
               float* mp = mod.p;
               void* m16 = mod.h16;
-              add([in, in_is_input, bind, scp, shp, gbp, act, tm, mp, m16](cudaStream_t st) {
+              add([in, in_is_input, bind, scp, shp, gbp, act, tm, mp, m16, gb_ready](cudaStream_t st) {
+                if (gb_ready) SIGE_CUDA(cudaStreamWaitEvent(st, gb_ready, 0));
                 launch_spade_mod(bind(in, in_is_input), scp, shp, gbp, act, &tm, mp, m16, st);
               });
               return plain(mod);
@@ -1500,6 +1566,10 @@ struct ProgramBuilder {
           break;
         }
       }
+    }
+    if (br_forked) {  // the branch rejoins the main chain (before the final copy and the restores)
+      const cudaEvent_t ev = br_record();
+      add([ev](cudaStream_t st) { SIGE_CUDA(cudaStreamWaitEvent(st, ev, 0)); }, 0);
     }
     // Final output (graph.cpp:891-900).
     const DevTensor& cfin = E.cache_tensor(step, "final");

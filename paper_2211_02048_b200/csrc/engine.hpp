@@ -195,6 +195,21 @@ class Engine {
   // fork/join for work off the launch chain (the input twin)
   cudaStream_t side_stream_ = nullptr;
   cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
+  // Program branch (SPADE): the label-map convs of every SPADE norm depend on
+  // the input only and run on this stream ahead of the main chain; events
+  // order them (graph edges when captured). Created at program build time.
+  cudaStream_t br_stream_ = nullptr;
+  std::vector<cudaEvent_t> br_events_;
+  static constexpr size_t kBrDense = 64;  // spade_dense's events: [64, 68) (programs use 0..63)
+  cudaEvent_t br_event(size_t i) {
+    while (br_events_.size() <= i) {
+      cudaEvent_t e;
+      SIGE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      br_events_.push_back(e);
+    }
+    if (!br_stream_) SIGE_CUDA(cudaStreamCreateWithFlags(&br_stream_, cudaStreamNonBlocking));
+    return br_events_[i];
+  }
   void fold_norm(const LayerDev& L, const Src& x, DevNorm& out, cudaStream_t st);
   // Config 3: a SPADE residual block over every pixel (dense walk / dense
   // fallback; buffers from `tensor` / `norm`, statistics folded unless
