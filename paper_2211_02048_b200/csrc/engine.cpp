@@ -101,6 +101,11 @@ struct Program {
   int launches = 0;
   bool ran = false;
   bool grouped = false;  // per-sample masks (independent requests)
+  // Tile-based result: the call's output starts as a copy of the cached final
+  // (off the critical path, beside the mask / IndexPlan) and the last layer's
+  // tiles are written straight into it — no full-tensor finalize at the tail.
+  const float* out_from_cache = nullptr;
+  size_t out_bytes = 0;
   double* stats = nullptr;  // GroupNorm statistics arena (fused dense-fallback ResBlocks), zeroed per call
   size_t stats_len = 0, stats_used = 0;
   // captured calls keyed by (edited, mask, out, threshold bits): without a
@@ -1573,6 +1578,18 @@ struct ProgramBuilder {
     }
     // Final output (graph.cpp:891-900).
     const DevTensor& cfin = E.cache_tensor(step, "final");
+    static const bool old_tail = std::getenv("SIGE_FINALIZE_TAIL") != nullptr;  // A/B: the full-copy tail
+    if (has_blocks && !old_tail) {
+      // out = cached final (copied at the start of the call, run_program),
+      // then the last layer's tiles; empty masks / samples without an edit keep
+      // the copy (graph.cpp:665-668), exactly what the full finalize produced
+      P.out_from_cache = cfin.p;
+      P.out_bytes = cfin.numel() * sizeof(float);
+      const Tiles t = tiles(blocks_entry);
+      const Src sres = flow;
+      add([eng, sres, t](cudaStream_t st) { launch_tiles_apply(sres, t, eng->cur_out_, kNCHW, st); });
+      return;
+    }
     Src result = flow;
     bool result_is_input = flow_is_input;
     if (has_blocks) {
@@ -1722,7 +1739,11 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
     SIGE_CUDA(cudaEventRecord(fork_ev_, st));
     SIGE_CUDA(cudaStreamWaitEvent(side_stream_, fork_ev_, 0));
     launch_input_twin(edited, batch_, in_c_, in_h_, in_w_, in_twin_c_, in_twin_, side_stream_);
+    if (P.out_from_cache)
+      SIGE_CUDA(cudaMemcpyAsync(cur_out_, P.out_from_cache, P.out_bytes, cudaMemcpyDeviceToDevice, side_stream_));
     SIGE_CUDA(cudaEventRecord(join_ev_, side_stream_));
+  } else if (P.out_from_cache) {
+    SIGE_CUDA(cudaMemcpyAsync(cur_out_, P.out_from_cache, P.out_bytes, cudaMemcpyDeviceToDevice, st));
   }
   const int masks = P.grouped ? batch_ : 1;
   SIGE_CUDA(cudaMemsetAsync(P.any, 0, sizeof(int32_t) * masks, st));
