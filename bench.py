@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--cpu-sample-edits", type=int, default=2)
     ap.add_argument("--cpu-single-thread", type=int, default=1, help="also time one 1-thread reference edit")
     ap.add_argument("--cpu-procs", type=int, default=1, help="also time nproc concurrent 1-thread reference processes")
+    ap.add_argument("--strict-parity", type=int, default=1, help="also run the edit in FP32_FMA mode with parity")
     ap.add_argument("--requests", type=int, default=64, help="config 5: independent requests over all ranks")
     ap.add_argument("--group", type=int, default=32, help="config 5: requests per grouped engine")
     ap.add_argument("--sweep", type=int, default=1, help="config 4: edit-area x block sweep (N=1)")
@@ -515,6 +516,41 @@ def parity_block(R, rm, ref_out, got, mask, cfg, final):
             "against": "oracle/_ref sigeref::sparse_forward on the same cache (seeded from the device precompute)"}
 
 
+def strict_mode_parity(sb, torch, model, orig, edited, cfg, flush, nthreads, reps=3):
+    """The same edit in SIGE_MATH_FP32_FMA (fp32 CUDA cores, FMA contraction —
+    the mode that meets the north star's elementwise floor as well as the
+    normalised bound): its time and its parity against the reference's
+    sparse_forward on this engine's own cache."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    eng = sb.Engine(model, batch=1, math=sb.MATH_FP32_FMA)
+    eng.precompute(orig.to(dev))
+    x = edited.to(dev)
+    out = torch.empty(eng.output_shape(), device=dev)
+    for _ in range(2):
+        eng.sparse_forward(x, config=cfg, out=out)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.sparse_forward(x, config=cfg, out=out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    got = out.cpu().numpy()
+    R, rm, cache, _, e2, m2 = reference_setup(WORKLOAD["model"], WORKLOAD["fixture"], WORKLOAD["seed"], nthreads,
+                                              cache_from=eng)
+    ref_out, _ = rm.sparse_forward(cache, e2, m2, cfg)
+    pb = parity_block(R, rm, ref_out, got, m2, cfg, eng.get_tensor("final", got.shape).numpy())
+    pb["tolerance"] = 1e-4
+    pb["within_tolerance"] = pb["max_norm_err"] <= 1e-4
+    return {"ms": round(sorted(ts)[len(ts) // 2], 4), **pb,
+            "elementwise_floor_ok": pb["elementwise_floor_violations_frac"] == 0.0,
+            "mode": "SIGE_MATH_FP32_FMA (fp32 CUDA cores), same edit, L2 flushed"}
+
+
 def main_reference(args):
     rank, world, _ = dist_env()  # the line's config names the same workload as the B200 arm
     if rank != 0:
@@ -848,6 +884,11 @@ def main_ours(args):
                                                 "kind": "reference", "sample": "1 sparse_forward edit of config 2"}
             if args.cpu_procs:
                 line["cpu_baseline_procs"] = reference_procs(rm, cache, e2, m2, cfg, nthreads)
+            if args.strict_parity:
+                try:
+                    line["parity_fp32_fma"] = strict_mode_parity(sb, torch, model, orig, edited, cfg, flush, nthreads)
+                except Exception as e:  # report, never hide
+                    line["parity_fp32_fma"] = {"error": str(e)}
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"unavailable: {e}"}
