@@ -26,6 +26,7 @@ constexpr int kCC = 16;     // staged input channels per chunk
 constexpr int kOCC = 32;    // output channels per work item (one per lane)
 constexpr int kThr = 128;   // 4 warps
 constexpr int kMaxPix = 16; // output pixels per thread: bh*bw <= 4 * 16
+constexpr int kWRow = kCC * 9 + 1;  // staged weights per output channel (+1: conflict-free lane rows)
 
 __device__ __forceinline__ void write_out(const Dst& d, int n, int oc, int y, int x, float v) {
   const size_t p = ((static_cast<size_t>(n) * d.h + y) * d.w + x) * d.c + oc;
@@ -47,13 +48,15 @@ __device__ __forceinline__ void write_out(const Dst& d, int n, int oc, int y, in
 
 template <int MATH>
 __global__ void __launch_bounds__(kThr) k_conv_exact(Src src, Tiles t, ConvW cw, Dst dst) {
-  extern __shared__ float win_s[];  // [win_h * win_w][kCC], channel fastest
+  extern __shared__ float win_s[];  // [win_h * win_w][kCC], channel fastest; then w_s[kOCC][kWRow]
   const int count = t.count_dev ? *t.count_dev : t.count;
   const int ci = cw.c_in, co = cw.c_out, k = cw.k, s = cw.stride, pad = (k - 1) / 2;
   const int win_h = (t.bh - 1) * s + k, win_w = (t.bw - 1) * s + k;
   const int npix = t.bh * t.bw;
   const int nocc = (co + kOCC - 1) / kOCC;
   const int lane = threadIdx.x & 31, pg = threadIdx.x >> 5;
+  const int kk = k * k;
+  float* w_s = win_s + win_h * win_w * kCC;
   for (int item = blockIdx.x; item < count * nocc; item += gridDim.x) {
     const int g = item / nocc, j = item % nocc;
     const int n = t.idx[3 * g], r0 = t.idx[3 * g + 1], c0 = t.idx[3 * g + 2];
@@ -73,13 +76,22 @@ __global__ void __launch_bounds__(kThr) k_conv_exact(Src src, Tiles t, ConvW cw,
         if (ch < ci && y >= 0 && y < src.h && x >= 0 && x < src.w) v = src_val(src, n, ch, y, x);
         win_s[e] = v;
       }
-      __syncthreads();
+      // the chunk's weights of the item's 32 output channels: one contiguous
+      // run of cend * k * k floats per channel, read coalesced into shared memory
+      // (per-lane global reads were 36-byte pieces 4.6 KB apart)
       const int cend = min(kCC, ci - cb);
+      const int wrun = cend * kk;
+      for (int e = threadIdx.x; e < kOCC * wrun; e += kThr) {
+        const int row = e / wrun, col = e - row * wrun;
+        const int ocr = j * kOCC + row;
+        w_s[row * kWRow + col] = ocr < co ? __ldg(cw.w + (static_cast<size_t>(ocr) * ci + cb) * kk + col) : 0.0f;
+      }
+      __syncthreads();
       for (int cc = 0; cc < cend; ++cc) {
         float wk[9];
-        const float* wp = cw.w + (static_cast<size_t>(oc_ok ? oc : 0) * ci + cb + cc) * k * k;
+        const float* wp = w_s + lane * kWRow + cc * kk;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) wk[q] = q < k * k ? __ldg(wp + q) : 0.0f;
+        for (int q = 0; q < 9; ++q) wk[q] = q < kk ? wp[q] : 0.0f;
 #pragma unroll
         for (int i = 0; i < kMaxPix; ++i) {
           const int p = pg + 4 * i;
@@ -120,7 +132,7 @@ void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, cons
                       std::to_string(tiles.bw) + " exceeds 64 output pixels");
   if (tiles.capacity == 0) return;
   const int win_h = (tiles.bh - 1) * cw.stride + cw.k, win_w = (tiles.bw - 1) * cw.stride + cw.k;
-  const size_t smem = sizeof(float) * win_h * win_w * kCC;
+  const size_t smem = sizeof(float) * (win_h * win_w * kCC + kOCC * kWRow);
   const int nocc = (cw.c_out + kOCC - 1) / kOCC;
   const long long work = static_cast<long long>(tiles.capacity) * nocc;
   const int grid = static_cast<int>(std::max(1LL, std::min<long long>(work, sm_count() * 8LL)));
