@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(const float* __restrict__ x
 // mode 0 writes, mode 1 adds.
 __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ blocks, int count, int c, int b,
                                                       const int32_t* __restrict__ idx, float* __restrict__ base,
-                                                      int nsamp, int h, int w, int T, int cpi, int staged, int mode) {
+                                                      int nsamp, int h, int w, int T, int cpi, int staged, int mode,
+                                                      int pairs) {
   __shared__ int s_org[kMaxChunkTiles][3];
   __shared__ __align__(16) float s_buf[kStageFloats];
   const int bsz = b * b;
@@ -373,7 +374,40 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
       stack_to_smem(sb, slab, s_buf, tc, run, (bsz & 3) == 0);
       __syncthreads();
     }
-    // image side: rows (channel, tile row), cols (tile, tile column)
+    // image side: rows (channel, tile row), cols (tile, tile column). With
+    // an even block and width a thread owns a column PAIR (8-byte stores, the
+    // pairs never straddle the image edge): half the store instructions.
+    if (pairs) {
+      // (a whole 6-wide tile row per thread measured slower: 88 vs 68 us)
+      const int per = 2, hb = b / per, pcols = tc * hb;
+      ColWalk pw(pcols);
+      for (; pw.col < pcols; pw.col += pw.col_step) {
+        const int t = pw.col / hb, dx = (pw.col - t * hb) * per;
+        const int y0 = s_org[t][1], xx = s_org[t][2] + dx;
+        const bool inside = s_org[t][0] >= 0 && s_org[t][0] < nsamp && y0 >= 0 && s_org[t][2] >= 0;
+        const int dy_hi = inside && xx < w ? min(b, h - y0) : 0;
+        float* dpb = base + (static_cast<size_t>(s_org[t][0]) * c + c0) * plane + static_cast<size_t>(y0) * w + xx;
+        const float* sp = s_buf + t * run + dx;
+        for (int cl = pw.group; cl < ncl; cl += pw.groups) {
+          float* dc = dpb + static_cast<size_t>(cl) * plane;
+          const float* sc = sp + cl * bsz;
+#pragma unroll 6
+          for (int dy = 0; dy < dy_hi; ++dy) {
+            for (int q = 0; q < per; q += 2) {  // (a 6-wide row: the width check keeps the fringe)
+              if (xx + q >= w) break;
+              float2 v = *reinterpret_cast<const float2*>(sc + dy * b + q);
+              if (mode) {
+                const float2 cur = *reinterpret_cast<const float2*>(dc + dy * w + q);
+                v.x = __fadd_rn(cur.x, v.x);
+                v.y = __fadd_rn(cur.y, v.y);
+              }
+              *reinterpret_cast<float2*>(dc + dy * w + q) = v;
+            }
+          }
+        }
+      }
+      continue;
+    }
     const int cols = tc * b;
     ColWalk cw(cols);
     for (; cw.col < cols; cw.col += cw.col_step) {
@@ -701,8 +735,10 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
   if (count == 0) return;
   const ChunkPlan cp = chunk_plan(c, b);
   const long long items = static_cast<long long>((count + cp.T - 1) / cp.T) * ((c + cp.cpi - 1) / cp.cpi);
+  static const bool no_pairs = std::getenv("SIGE_SCATTER_SINGLE") != nullptr;  // A/B: one column per thread
+  const int pairs = !no_pairs && cp.staged && (b & 1) == 0 && (w & 1) == 0 ? 2 : 0;
   k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
-      blocks, count, c, b, idx, base, n, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0);
+      blocks, count, c, b, idx, base, n, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0, pairs);
   after_launch("k_scatter");
 }
 
