@@ -123,18 +123,7 @@ struct TcParams {
   int warm;                // epilogue warm-up pass (SIGE_NO_WARM=1 disables)
   unsigned long long* gtl;  // SIGE_TC_GTL: per-launch [first CTA start, last CTA end] (graph-safe)
   int gtl_idx;
-  const char* pf_ptr;       // next conv's packed weights (L2 prefetch), or nullptr
-  long long pf_bytes;
-  unsigned long long* gtl_marks;  // SIGE_TC_GTL: CTA 0's phase marks per launch (64 slots), or nullptr
-  // Conv -> conv handoff without waiting for grid completion: every CTA
-  // bumps sig_ctr once its global writes are fenced; a conv whose predecessor
-  // in the stream is a conv spins on that counter (wait_ctr >= wait_target,
-  // the predecessor's grid size) instead of griddepcontrol.wait, so the
-  // predecessor's teardown (cluster sync, TMEM dealloc, exit, grid drain)
-  // overlaps this layer. nullptr: plain programmatic dependent launch.
-  unsigned int* sig_ctr;
-  const unsigned int* wait_ctr;
-  unsigned int wait_target;
+  unsigned long long* gtl_marks;  // SIGE_TC_GTL: CTA 0's phase marks + per-CTA stamps per launch, or nullptr
 };
 
 // ------------------------------------------------------------- PTX ------
@@ -299,19 +288,8 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// The dependency wait of a conv launch (see TcParams::wait_ctr).
-__device__ __forceinline__ void dep_wait(const unsigned int* ctr, unsigned int target) {
-  if (!ctr) {
-    pdl_wait();
-    return;
-  }
-  uint32_t v;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    if (v >= target) break;
-    __nanosleep(40);
-  }
-}
+// The dependency wait of a conv launch: the previous grid's writes (PDL).
+__device__ __forceinline__ void dep_wait() { pdl_wait(); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // One lane of a converged warp (tcgen05.mma / commit are single-thread
 // instructions; the warp computes the descriptors uniformly).
@@ -1104,17 +1082,6 @@ __device__ __forceinline__ int nt_index(int nt) {
   return nt <= 16 ? 0 : nt <= 32 ? 1 : nt <= 64 ? 2 : nt <= 128 ? 3 : 4;
 }
 
-// This CTA's slice of the next conv's packed weights into L2 (one elected
-// thread; the next layer's weight TMA then streams from L2).
-__device__ __forceinline__ void prefetch_next_weights(const TcParams& p) {
-  if (!p.pf_ptr) return;
-  const long long per = ((p.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15LL;
-  const long long lo = per * blockIdx.x, hi = min(p.pf_bytes, lo + per);
-  for (long long o = lo; o < hi; o += 32768)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_ptr + o),
-                 "r"(static_cast<uint32_t>(min(32768LL, hi - o)))
-                 : "memory");
-}
 
 // MMA-issue state shared by the unrolled chunk bodies (uniform across the warp).
 struct MmaCtx {
@@ -1342,7 +1309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               prefetch_l2(fb + r * s.c + j);
             }
         }
-        dep_wait(p.wait_ctr, p.wait_target);  // the source / GroupNorm statistics were written by the previous kernel
+        dep_wait();  // the source / GroupNorm statistics were written by the previous kernel
         if (threadIdx.x == 0 && p.gtl) {
           unsigned long long t;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1513,7 +1480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // A CTA without items still orders its completion after the previous
     // grid's (the next kernel's dependency wait relies on this transitively).
-    if (it == 0) dep_wait(p.wait_ctr, p.wait_target);
+    if (it == 0) dep_wait();
     // cp.async arrivals are asynchronous: wait for this thread's copies before exit.
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kEpiBase / 32) {
@@ -1573,7 +1540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // transform ends, and a warm-up pass after it sits on the critical path —
     // measured 2 % per edit; SIGE_TC_DEBUG bit 64 restores it for A/B)
     bool dry = p.warm && cid < n_items && (!helpers || (p.dbg & 64));
-    if (!dry) dep_wait(p.wait_ctr, p.wait_target);  // the destination / residual inputs were written by earlier kernels
+    if (!dry) dep_wait();  // the destination / residual inputs were written by earlier kernels
     for (int item = cid; item < n_items;) {
       const int mi = static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices), ni = item - mi * n_slices;
       const int g = mi * p.T + t;
@@ -1753,7 +1720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (dry) {
         dry = false;
-        dep_wait(p.wait_ctr, p.wait_target);
+        dep_wait();
         continue;
       }
       if (threadIdx.x == kEpiBase && it < 2) tl_mark(p, it ? 57 : 47);
@@ -1895,7 +1862,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
       uint32_t b_iter = 0, bslot = 0, bphase = 0;
       const uint32_t b0 = smem_u32(bbuf);
-      if (cid >= n_items) prefetch_next_weights(p);  // no items of its own
       const uint32_t stage_bytes = b_stage;
       for (int item = cid; item < n_items; item += ncl) {
         const int ni = item - static_cast<int>((static_cast<float>(item) + 0.5f) * inv_slices) * n_slices;
@@ -1909,10 +1875,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mbar_expect_tx(&bar_bfull[st], stage_bytes);
             tma_3d(b0 + st * b_stage, map, 0, ni * n_tile, ch * p.ntaps + tg * tps, &bar_bfull[st]);
-            if (b_iter == 0) {
-              tl_mark(p, 10);
-              if (item == cid) prefetch_next_weights(p);  // behind this CTA's own first stage
-            }
+            if (b_iter == 0) tl_mark(p, 10);
           }
         if (item == cid) tl_mark(p, 11);
       }
@@ -1923,10 +1886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tl_clock(p, 61);
   }
   tc_fence_before();
-  if (p.sig_ctr) __threadfence();  // this thread's global writes, before the CTA's signal
   __syncthreads();
-  if (p.sig_ctr && threadIdx.x == 0)
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.sig_ctr) : "memory");
   if (p.ks > 1) cluster_sync();  // no CTA leaves while a peer may still touch its shared memory
   if (threadIdx.x == 0 && p.gtl) {
     unsigned long long t;
@@ -2112,18 +2072,13 @@ void pack_weights_tc(const float* w_dev, int c_out, int c_in, int k, int f16, Co
 }
 
 int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
-                   cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad,
-                   const void* pf_ptr, size_t pf_bytes, unsigned int* sig_ctr, const unsigned int* wait_ctr,
-                   unsigned int wait_target) {
+                   cudaStream_t st, int sm_budget, unsigned long long* gtl, int gtl_idx, int pad) {
   static_assert(kGtlLaunchesDev == kTimelineSlots, "timeline layout");
   const int sms_all = sm_count();
   const int sms_use = sm_budget > 0 ? std::min(sm_budget, sms_all) : sms_all;
   if (!cw.w_tc) throw ConfigError("conv (tensor core): weights were not packed for this path");
   if (tiles.capacity == 0) return 0;
   TcParams p{};
-  p.sig_ctr = sig_ctr;
-  p.wait_ctr = wait_ctr;
-  p.wait_target = wait_target;
   p.src = src;
   // Transform mode (F16): the fp16 twin streams by cp.async and the pending
   // chain — [scale-shift, act] or GroupNorm-from-statistics then act — is
@@ -2154,12 +2109,6 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
   p.k = cw.k;
   p.s = cw.stride;
   p.pad = pad >= 0 ? pad : (cw.k - 1) / 2;
-  // Opt-in (SIGE_L2_PREFETCH=1): measured 2.5 % slower per edit on config 2
-  // (profiles/r2_l2_prefetch_ab.txt) — the next layer's own weight TMA is
-  // already issued in its PDL prologue, before the dependency wait.
-  static const bool pf_on = std::getenv("SIGE_L2_PREFETCH") != nullptr;
-  p.pf_ptr = pf_on ? static_cast<const char*>(pf_ptr) : nullptr;
-  p.pf_bytes = pf_on ? static_cast<long long>(pf_bytes) & ~15LL : 0;
   p.n_pad = cw.n_pad;
   p.nchunks = cw.k_pad / (f16 ? 64 : 32);
   p.ntaps = cw.k * cw.k;
@@ -2399,8 +2348,6 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
       if (tunable) {
         double* const gn_saved = p.dst.gn_stats;
         p.dst.gn_stats = nullptr;  // trials must not accumulate statistics
-        p.sig_ctr = nullptr;       // nor signal the next conv (they run to completion here)
-        p.wait_ctr = nullptr;
         cudaEvent_t e0, e1;
         SIGE_CUDA(cudaEventCreate(&e0));
         SIGE_CUDA(cudaEventCreate(&e1));
@@ -2433,8 +2380,6 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
         SIGE_CUDA(cudaEventDestroy(e0));
         SIGE_CUDA(cudaEventDestroy(e1));
         p.dst.gn_stats = gn_saved;
-        p.sig_ctr = sig_ctr;
-        p.wait_ctr = wait_ctr;
         std::lock_guard<std::mutex> g(plans_mu);
         plans[key] = {nt_plan, ks_plan};
       }

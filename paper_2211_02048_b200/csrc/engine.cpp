@@ -93,8 +93,6 @@ struct Program {
   RestoreJob* restores_dev = nullptr;
   long long restore_max = 0;
   std::vector<TraceInfo> trace;
-  std::vector<WRef> wseq;  // packed weights of the tensor-core convs in launch order
-  unsigned int* ctrs = nullptr;  // conv handoff counters (Engine::kMaxCallConvs), zeroed per call
   uint32_t* bits = nullptr;
   int32_t* any = nullptr;
   int full_h = 0, full_w = 0, dilate_full = 0, dilate_scale = 0;
@@ -479,35 +477,6 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
     }
     SIGE_CUDA(cudaEventRecord(rec.a, st));
   }
-  const void* pf = nullptr;
-  size_t pf_bytes = 0;
-  unsigned int* sig = nullptr;
-  const unsigned int* wait = nullptr;
-  unsigned int wait_target = 0;
-  if (tensor_cores() && seq_) {
-    const size_t i = seq_next_;
-    // Opt-in (SIGE_CTR_HANDOFF=1): measured 2-3 % slower than the PDL wait on
-    // config 2 (profiles/r2_ctr_handoff_ab.txt) — the predecessor's teardown
-    // overlaps, but the dependents' spinning and the per-thread release fences
-    // cost more than the ~1 us teardown they hide.
-    static const bool handoff = std::getenv("SIGE_CTR_HANDOFF") != nullptr;
-    if (cur_ctrs_ && handoff && i < static_cast<size_t>(kMaxCallConvs)) {
-      sig = cur_ctrs_ + i;
-      // the previous kernel in the stream is a conv: wait on its counter
-      if (prev_ctr_ && g_launches.load() == prev_mark_) {
-        wait = prev_ctr_;
-        wait_target = prev_grid_;
-      }
-    }
-  }
-  if (tensor_cores() && seq_) {
-    const size_t i = seq_next_++;
-    if (seq_->size() == i) seq_->push_back({cw.w_tc, cw.w_tc_bytes});  // first run records the chain
-    if (i + 1 < seq_->size()) {
-      pf = (*seq_)[i + 1].p;
-      pf_bytes = (*seq_)[i + 1].bytes;
-    }
-  }
   if (tensor_cores() && timeline_) {
     const int idx = tl_next_++;
     if (idx < kTimelineSlots) {
@@ -522,11 +491,9 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
       m.sparse = t.count_dev ? 1 : 0;
       tl_meta_.push_back(m);
     }
-    record_handoff(sig, launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, tl_buf_, idx,
-                                       -1, pf, pf_bytes, sig, wait, wait_target));
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, tl_buf_, idx);
   } else if (tensor_cores())
-    record_handoff(sig, launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_, nullptr, 0,
-                                       -1, pf, pf_bytes, sig, wait, wait_target));
+    launch_conv_tc(src, t, cw, dst, math_ == SIGE_MATH_F16 ? 1 : 0, st, sm_budget_);
   else
     launch_conv_exact(src, t, cw, dst, math_, st);
   if (profiling_) {
@@ -545,16 +512,6 @@ void Engine::conv(const Src& src, const Tiles& t, const ConvW& cw, const Dst& ds
 }
 
 void Engine::set_profiling(bool on) { profiling_ = on; }
-
-void Engine::record_handoff(unsigned int* sig, int grid) const {
-  if (sig && grid > 0) {
-    prev_ctr_ = sig;
-    prev_grid_ = static_cast<unsigned int>(grid);
-    prev_mark_ = g_launches.load();
-  } else {
-    prev_ctr_ = nullptr;  // nothing launched / no counter: the next conv waits the PDL way
-  }
-}
 
 void Engine::timeline_reset() {
   std::vector<unsigned long long> init(3 * kTimelineSlots, ~0ull);  // [start, end] pairs, then wait exits
@@ -1711,20 +1668,6 @@ void Engine::run_program(Program& P, const float* edited, const uint8_t* mask,
                          const sige_run_config& cfg, cudaStream_t st) {
   tl_next_ = 0;
   tl_meta_.clear();
-  seq_ = &P.wseq;
-  seq_next_ = 0;
-  if (!P.ctrs) P.ctrs = static_cast<unsigned int*>(alloc(kMaxCallConvs * sizeof(unsigned int)));
-  cur_ctrs_ = P.ctrs;
-  prev_ctr_ = nullptr;
-  SIGE_CUDA(cudaMemsetAsync(P.ctrs, 0, kMaxCallConvs * sizeof(unsigned int), st));
-  struct SeqReset {  // the sequence belongs to this call only
-    Engine* e;
-    ~SeqReset() {
-      e->seq_ = nullptr;
-      e->cur_ctrs_ = nullptr;
-      e->prev_ctr_ = nullptr;
-    }
-  } seq_reset{this};
   static const bool no_fork = std::getenv("SIGE_NO_FORK") != nullptr;  // A/B switch
   const bool fork = in_twin_ && !no_fork;
   if (fork) {

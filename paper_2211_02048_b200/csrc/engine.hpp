@@ -72,11 +72,6 @@ struct TraceInfo {
 
 struct Program;
 
-// A packed weight tensor (L2 prefetch target).
-struct WRef {
-  const void* p;
-  size_t bytes;
-};
 
 class Engine {
  public:
@@ -267,24 +262,11 @@ class Engine {
     double flops_per_tile;
     int sparse;
   };
-  // Weight L2 prefetch along the launch chain: the packed weights of every
-  // tensor-core conv in call order (recorded by the first run of a program),
-  // so conv i prefetches conv i+1's weights while it runs.
-  std::vector<WRef>* seq_ = nullptr;  // the running call's sequence (nullptr: none)
-  mutable size_t seq_next_ = 0;
-  // Counter handoff between consecutive tensor-core convs of a sparse call
-  // (TcParams::sig_ctr): one counter per conv launch, zeroed at call start.
-  static constexpr int kMaxCallConvs = 1024;
-  unsigned int* cur_ctrs_ = nullptr;
-  mutable const unsigned int* prev_ctr_ = nullptr;  // the last conv's counter ...
-  mutable unsigned int prev_grid_ = 0;               // ... its grid ...
-  mutable uint64_t prev_mark_ = ~0ull;               // ... and the launch count right after it
   bool timeline_ = false;
   unsigned long long* tl_buf_ = nullptr;
   mutable int tl_next_ = 0;
   mutable std::vector<TlMeta> tl_meta_;
   void timeline_reset();
-  void record_handoff(unsigned int* sig, int grid) const;
   void drop_graphs();
   mutable std::vector<cudaEvent_t> ev_pool_;
   // per-call bindings read by program steps

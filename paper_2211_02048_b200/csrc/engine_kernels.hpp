@@ -143,16 +143,10 @@ void launch_conv_exact(const Src& src, const Tiles& tiles, const ConvW& cw, cons
 constexpr int kTimelineSlots = 1024;
 // pad >= 0 overrides the conv padding (k - 1) / 2 (op-level conv_on_blocks:
 // the gathered window already carries the halo, kernels.cpp:391-421).
-// sig_ctr / wait_ctr / wait_target: counter handoff between consecutive
-// conv launches (TcParams). Returns the launch's grid size (0: nothing launched).
+// Returns the launch's grid size (0: nothing launched).
 int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Dst& dst, int f16,
                    cudaStream_t st, int sm_budget = 0, unsigned long long* gtl = nullptr, int gtl_idx = 0,
-                   int pad = -1, const void* pf_ptr = nullptr, size_t pf_bytes = 0, unsigned int* sig_ctr = nullptr,
-                   const unsigned int* wait_ctr = nullptr, unsigned int wait_target = 0);
-// pf_ptr / pf_bytes: the packed weights of the NEXT conv of the launch chain;
-// the launch's CTAs prefetch them into L2 (cp.async.bulk.prefetch.L2, one
-// slice per CTA) while this layer runs, so the next layer's weight stream
-// starts from L2 instead of HBM.
+                   int pad = -1);
 // Packs reference-layout weights for launch_conv_tc (fills w_tc, n_pad,
 // k_pad and the TMA descriptors of `cw`).
 // Developer instrumentation (SIGE_TC_GTL=1): per-launch conv spans, read + reset.
