@@ -1145,7 +1145,12 @@ __device__ __forceinline__ void mma_chunk(MmaCtx& c, uint32_t abase, bool first_
 // SYNC: the instantiation carries the synchronous (converting / chained)
 // staging path; the F16 production kernels (every source an fp16 twin or act
 // buffer) are built without it — half the code, fewer cold instruction fetches.
-template <bool F16, int K, int S, bool SYNC>
+// AM (A-operand staging mode, compile time): 0 = synchronous (converting /
+// chained sources; SYNC), 1 = cp.async from an fp16 / fp32 channels-last
+// source, 2 = TMA windows. Each launch runs one mode, so each instantiation
+// carries only its own staging code (smaller kernels: dormant branches cost
+// instruction-cache and issue time, profiles/r2_*).
+template <bool F16, int K, int S, int AM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_tc(const __grid_constant__ TcParams p, const __grid_constant__ TcMaps maps,
               const __grid_constant__ CUtensorMap amap) {
@@ -1195,7 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane >= 16 && lane - 16 < p.na) {
       const int i = lane - 16;
-      mbar_init(&bar_afull[i], p.tma_a && !p.xform ? 1 : kProdThreads);
+      mbar_init(&bar_afull[i], AM == 2 && !p.xform ? 1 : kProdThreads);
       mbar_init(&bar_aland[i], 1);  // TMA + transform: the boxes landed (before the in-smem chain)
       mbar_init(&bar_afree[i], 1);
     }
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 26) {
       mbar_init(&bar_red_full, 1);  // the owner's arrive.expect_tx; the peers' st.async complete the bytes
       mbar_init(&bar_red_empty, (p.ks - 1) * (kEpiThreads / 32));  // one lane per epilogue warp of every owner
-      if (p.tma_a && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
+      if (AM == 2 && (smem_u32(smem) & 1023u)) __trap();  // 128-byte-swizzled boxes want 1 KB-aligned stages
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (lane == 0) tl_mark(p, 7);
@@ -1239,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const float inv_slices = p.w_inv_slices[nti];
   const int n_items = items_m * n_slices;
   // Epilogue warps help the producers transform the first item's chunks (see the epilogue branch).
-  const bool helpers = p.xform && p.tma_a && cid < n_items && p.dbg != 12;
+  const bool helpers = p.xform && AM == 2 && cid < n_items && p.dbg != 12;
   const int tps = p.tps[nti];
   const int tgroups = p.w_tgroups[nti];
   const uint32_t tap_b = static_cast<uint32_t>(n_tile * 128);  // one tap of B in smem
@@ -1267,8 +1272,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // The first item's first chunk is requested right after the dependency
     // wait, ahead of the GroupNorm fold (the windows do not depend on it).
-    const bool early_a = p.tma_a && c_begin < c_end;
-    if (threadIdx.x == 0 && p.tma_a) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+    const bool early_a = AM == 2 && c_begin < c_end;
+    if (threadIdx.x == 0 && AM == 2) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
     uint32_t a_iter = 0, it = 0, aphase = 0;
     int aslot = 0;
     for (int item = cid; item < n_items; item += ncl, ++it) {
@@ -1285,7 +1290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0 && it == 0) tl_mark(p, 50);
       uint32_t pix_off[kUnitRegs];
       int unit_n[kUnitRegs];
-      const bool fast_units = F16 && p.async_a && !p.tma_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
+      const bool fast_units = F16 && AM == 1 && p.async_a && p.phases * p.T * p.Mt * 8 <= kUnitRegs * kProdThreads;
       if (fast_units) unit_pixels(p, row_tab, s_tile, pix_off, unit_n);
       if (p.xform) {
         fill_row_samples(p, row_tab, s_tile, s_rown);
@@ -1378,7 +1383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (helpers) asm volatile("bar.sync 3, %0;" ::"n"(kProdThreads + kEpiThreads));
         }
       }
-      if (p.tma_a) {
+      if constexpr (AM == 2) {
         // One thread streams the item's windows: per chunk one 4-D box
         // (64 channels x plane) per tile and phase plane, 128-byte rows;
         // out-of-canvas cells and channels >= C come back zero-filled
@@ -1421,7 +1426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             prev_phase = sphase;
           }
         }
-      } else if (p.xform) {
+      } else if (AM == 1 && p.xform) {
         // Async copy of chunk c, then transform of chunk c-1 (landed: this
         // thread's copies are complete after wait_group 1, the other
         // producers' after the named barrier), fence, arrive. Drained at the
@@ -1460,7 +1465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             aslot = 0;
             aphase ^= 1;
           }
-          if (p.async_a) {
+          if (AM == 1 && p.async_a) {
             // The arrival fires when this thread's copies have landed, so the
             // producers run ahead to the next free stage without waiting.
             if (fast_units)
@@ -1469,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               stage_a_async<F16>(p, a0 + sidx * p.a_bytes, ch, row_tab, s_tile);
             cp_async_arrive(&bar_afull[sidx]);
           } else {
-            if constexpr (SYNC) stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
+            if constexpr (AM == 0) stage_a_sync<F16>(p, abuf0 + sidx * p.a_bytes, ch, row_tab, s_tile);
             fence_proxy_async();
             mbar_arrive(&bar_afull[sidx]);
           }
@@ -1803,9 +1808,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.b0 = smem_u32(bbuf) >> 4;
     // A rows are 16 bytes apart in the interleaved layout (k-steps LBO apart),
     // 128 bytes apart in the TMA mode's 128-byte-swizzled rows (k-steps 32 B).
-    c.row16 = p.tma_a ? 8u : 1u;
-    c.kstep16 = p.tma_a ? 2u : 2u * (p.lbo_a >> 4);
-    c.adesc0 = p.tma_a ? umma_desc_sw128(0) : umma_desc(0, p.lbo_a, 128);
+    c.row16 = AM == 2 ? 8u : 1u;
+    c.kstep16 = AM == 2 ? 2u : 2u * (p.lbo_a >> 4);
+    c.adesc0 = AM == 2 ? umma_desc_sw128(0) : umma_desc(0, p.lbo_a, 128);
     c.bdesc0 = umma_desc_sw128(0);
     c.tap_b16 = tap_b >> 4;
     c.plane16 = static_cast<uint32_t>(p.T * p.Mt) * c.row16;
@@ -2273,20 +2278,22 @@ int launch_conv_tc(const Src& src, const Tiles& tiles, const ConvW& cw, const Ds
 
   using KernelFn = void (*)(TcParams, TcMaps, CUtensorMap);
   KernelFn fn = nullptr;
-  const bool sync = !p.async_a;
-#define SIGE_TC_PICK(F, KK, SS) (sync ? k_conv_tc<F, KK, SS, true> : k_conv_tc<F, KK, SS, false>)
+  const int am = !p.async_a ? 0 : p.tma_a ? 2 : 1;
+#define SIGE_TC_PICK(F, KK, SS) \
+  (am == 0 ? k_conv_tc<F, KK, SS, 0> : am == 1 ? k_conv_tc<F, KK, SS, 1> : k_conv_tc<F, KK, SS, 2>)
   if (cw.k == 1)
-    fn = f16 ? SIGE_TC_PICK(true, 1, 1) : SIGE_TC_PICK(false, 1, 1);
+    fn = f16 ? SIGE_TC_PICK(true, 1, 1) : k_conv_tc<false, 1, 1, 0>;
   else if (cw.stride == 1)
-    fn = f16 ? SIGE_TC_PICK(true, 3, 1) : SIGE_TC_PICK(false, 3, 1);
+    fn = f16 ? SIGE_TC_PICK(true, 3, 1) : k_conv_tc<false, 3, 1, 0>;
   else
-    fn = f16 ? SIGE_TC_PICK(true, 3, 2) : SIGE_TC_PICK(false, 3, 2);
+    fn = f16 ? SIGE_TC_PICK(true, 3, 2) : k_conv_tc<false, 3, 2, 0>;
 #undef SIGE_TC_PICK
   static std::atomic<uint64_t> attr_done{0};
   if (first_on_device(attr_done)) {
-    for (KernelFn f : {k_conv_tc<true, 1, 1, true>, k_conv_tc<false, 1, 1, true>, k_conv_tc<true, 3, 1, true>,
-                       k_conv_tc<false, 3, 1, true>, k_conv_tc<true, 3, 2, true>, k_conv_tc<false, 3, 2, true>,
-                       k_conv_tc<true, 1, 1, false>, k_conv_tc<true, 3, 1, false>, k_conv_tc<true, 3, 2, false>})
+    for (KernelFn f : {k_conv_tc<true, 1, 1, 0>, k_conv_tc<false, 1, 1, 0>, k_conv_tc<true, 3, 1, 0>,
+                       k_conv_tc<false, 3, 1, 0>, k_conv_tc<true, 3, 2, 0>, k_conv_tc<false, 3, 2, 0>,
+                       k_conv_tc<true, 1, 1, 1>, k_conv_tc<true, 3, 1, 1>, k_conv_tc<true, 3, 2, 1>,
+                       k_conv_tc<true, 1, 1, 2>, k_conv_tc<true, 3, 1, 2>, k_conv_tc<true, 3, 2, 2>})
       SIGE_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
   }
   static const bool no_pdl = std::getenv("SIGE_NO_PDL") != nullptr;
