@@ -223,8 +223,8 @@ struct ColWalk {
 // Contiguous per-tile runs of a block stack (tile t's `run` floats at
 // stack + t * slab) into shared memory (sbuf + t * run), 16-byte vectors when
 // the geometry keeps them aligned.
-__device__ __forceinline__ void stack_to_smem(const float* stack, size_t slab, float* sbuf, int tc, int run,
-                                              bool vec) {
+__device__ __forceinline__ void stack_to_smem_issue(const float* stack, size_t slab, float* sbuf, int tc, int run,
+                                                    bool vec) {
   const int v = vec ? 4 : 1, rv = run / v;
   const int tpp = rv >= static_cast<int>(blockDim.x) ? 1 : static_cast<int>(blockDim.x) / rv;
   int t = tpp > 1 ? static_cast<int>(threadIdx.x) / rv : 0;
@@ -235,12 +235,21 @@ __device__ __forceinline__ void stack_to_smem(const float* stack, size_t slab, f
     const float* g = stack + t * slab;
     float* sm = sbuf + t * run;
     for (int j = j0; j < rv; j += jstep) {
+      // cp.async: no register round trip per copy, so all of a thread's
+      // copies are in flight at once (a dependent ld -> st per iteration
+      // left ~1 load per thread outstanding: latency-bound staging)
+      const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(vec ? sm + 4 * j : sm + j));
       if (vec)
-        reinterpret_cast<float4*>(sm)[j] = __ldg(reinterpret_cast<const float4*>(g) + j);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g + 4 * j) : "memory");
       else
-        sm[j] = __ldg(g + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(g + j) : "memory");
     }
   }
+}
+__device__ __forceinline__ void stack_to_smem(const float* stack, size_t slab, float* sbuf, int tc, int run,
+                                              bool vec) {
+  stack_to_smem_issue(stack, slab, sbuf, tc, run, vec);
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // gather (kernels.cpp:39-86): one thread per output value; out-of-canvas
@@ -431,6 +440,82 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
         }
       }
     }
+  }
+}
+
+// scatter with the staging double-buffered (a persistent CTA stages item
+// i + 1 with cp.async while it stores item i): the staged column-pair walk of
+// k_scatter (above) behind a two-deep copy pipeline. Item = (chunk of T tiles,
+// slice of cpi channels); the stack side of an item is T runs of cpi * b^2
+// contiguous floats, the origins 3 T contiguous ints.
+constexpr int kPipeFloats = 4096;  // per buffer (two buffers: 32 KB)
+__global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restrict__ blocks, int count, int c,
+                                                           int b, const int32_t* __restrict__ idx,
+                                                           float* __restrict__ base, int nsamp, int h, int w,
+                                                           int T, int cpi, int mode) {
+  __shared__ __align__(16) int s_org[2][kMaxChunkTiles * 3];
+  __shared__ __align__(16) float s_buf[2][kPipeFloats];
+  const int bsz = b * b;
+  const size_t slab = static_cast<size_t>(c) * bsz, plane = static_cast<size_t>(h) * w;
+  const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi, items = chunks * slices;
+  const bool vec = (bsz & 3) == 0;
+  auto issue = [&](int it, int sbi) {
+    const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
+    const int i0 = ck * T, tc = min(T, count - i0);
+    for (int j = threadIdx.x; j < 3 * tc; j += blockDim.x) {
+      const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(&s_org[sbi][j]));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(idx + 3 * i0 + j) : "memory");
+    }
+    stack_to_smem_issue(blocks + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * bsz, slab,
+                        s_buf[sbi], tc, ncl * bsz, vec);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int sbi = 0;
+  if (blockIdx.x < items) issue(blockIdx.x, 0);
+  for (int it = blockIdx.x; it < items; it += gridDim.x, sbi ^= 1) {
+    if (it + static_cast<int>(gridDim.x) < items) {
+      issue(it + gridDim.x, sbi ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
+    const int i0 = ck * T, tc = min(T, count - i0), run = ncl * bsz;
+    const int* org = s_org[sbi];
+    const float* buf = s_buf[sbi];
+    // column pairs (8-byte stores) when the block and width are even
+    const int per = (b & 1) == 0 && (w & 1) == 0 ? 2 : 1, hb = b / per, pcols = tc * hb;
+    ColWalk pw(pcols);
+    for (; pw.col < pcols; pw.col += pw.col_step) {
+      const int t = pw.col / hb, dx = (pw.col - t * hb) * per;
+      const int y0 = org[3 * t + 1], xx = org[3 * t + 2] + dx;
+      // fringe clipping; an index outside the tensor never writes
+      const bool inside = org[3 * t] >= 0 && org[3 * t] < nsamp && y0 >= 0 && org[3 * t + 2] >= 0;
+      const int dy_hi = inside && xx < w ? min(b, h - y0) : 0;
+      float* dpb = base + (static_cast<size_t>(org[3 * t]) * c + c0) * plane + static_cast<size_t>(y0) * w + xx;
+      const float* sp = buf + t * run + dx;
+      for (int cl = pw.group; cl < ncl; cl += pw.groups) {
+        float* dc = dpb + static_cast<size_t>(cl) * plane;
+        const float* sc = sp + cl * bsz;
+        if (per == 2) {
+#pragma unroll 6
+          for (int dy = 0; dy < dy_hi; ++dy) {
+            float2 v = *reinterpret_cast<const float2*>(sc + dy * b);
+            if (mode) {
+              const float2 cur = *reinterpret_cast<const float2*>(dc + dy * w);
+              v.x = __fadd_rn(cur.x, v.x);
+              v.y = __fadd_rn(cur.y, v.y);
+            }
+            *reinterpret_cast<float2*>(dc + dy * w) = v;
+          }
+        } else {
+#pragma unroll 4
+          for (int dy = 0; dy < dy_hi; ++dy) dc[dy * w] = mode ? __fadd_rn(dc[dy * w], sc[dy * b]) : sc[dy * b];
+        }
+      }
+    }
+    __syncthreads();  // buffer sbi is refilled by the next iteration's issue
   }
 }
 
@@ -735,6 +820,22 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
   if (count == 0) return;
   const ChunkPlan cp = chunk_plan(c, b);
   const long long items = static_cast<long long>((count + cp.T - 1) / cp.T) * ((c + cp.cpi - 1) / cp.cpi);
+  static const bool no_pipe = std::getenv("SIGE_SCATTER_NOPIPE") != nullptr;  // A/B: the single-buffered kernel
+  const int bsz = b * b;
+  if (!no_pipe && bsz <= kPipeFloats) {
+    const int T = std::max(1, std::min({kMaxChunkTiles, kChunkCols / b, kPipeFloats / bsz}));
+    const int cpi = std::max(1, std::min(c, kPipeFloats / (T * bsz)));
+    const long long pitems = static_cast<long long>((count + T - 1) / T) * ((c + cpi - 1) / cpi);
+    static int per_sm = [] {
+      int n = 0;
+      SIGE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_scatter_pipe, kThreads, 0));
+      return std::max(1, n);
+    }();
+    k_scatter_pipe<<<static_cast<int>(std::min<long long>(pitems, static_cast<long long>(sm_count()) * per_sm)),
+                     kThreads, 0, st>>>(blocks, count, c, b, idx, base, n, h, w, T, cpi, add ? 1 : 0);
+    after_launch("k_scatter_pipe");
+    return;
+  }
   static const bool no_pairs = std::getenv("SIGE_SCATTER_SINGLE") != nullptr;  // A/B: one column per thread
   const int pairs = !no_pairs && cp.staged && (b & 1) == 0 && (w & 1) == 0 ? 2 : 0;
   k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
