@@ -320,14 +320,27 @@ __global__ void __launch_bounds__(256) k_gather_rows(const float* __restrict__ x
                                                      const int32_t* __restrict__ idx, int count, long long rows,
                                                      int stride, int pad, DevEpilogue epi, float* __restrict__ out) {
   constexpr int kChunks = WIN / 4 + 1;  // aligned float4 chunks covering WIN floats at any phase
-  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < rows;
-       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+  // warp-uniform trip count (the tile origin is fetched once per warp when
+  // the warp's rows share a tile: the LSU data pipe, not DRAM, bounds this kernel)
+  const int lane = threadIdx.x & 31;
+  for (long long rb = blockIdx.x * static_cast<long long>(blockDim.x) + (threadIdx.x & ~31); rb < rows;
+       rb += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = rb + lane;
+    if (r >= rows) continue;  // (tail warp: no shuffles below depend on inactive lanes)
     const int wy = static_cast<int>(r % WIN);
     const long long gc = r / WIN;  // tile * c + channel (the output is written in order)
     const int ch = static_cast<int>(gc % c);
     const int i = static_cast<int>(gc / c);
-    const int n = __ldg(idx + 3 * i), sy = __ldg(idx + 3 * i + 1) * stride - pad + wy,
-              sx0 = __ldg(idx + 3 * i + 2) * stride - pad;
+    const unsigned act = __activemask();
+    const int i0 = __shfl_sync(act, i, __ffs(act) - 1);
+    int n, oy, ox;
+    if ((act & 7u) == 7u && __all_sync(act, i == i0)) {  // lanes 0-2 fetch (n, y, x)
+      const int v = lane < 3 ? __ldg(idx + 3 * i0 + lane) : 0;
+      n = __shfl_sync(act, v, 0), oy = __shfl_sync(act, v, 1), ox = __shfl_sync(act, v, 2);
+    } else {
+      n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1), ox = __ldg(idx + 3 * i + 2);
+    }
+    const int sy = oy * stride - pad + wy, sx0 = ox * stride - pad;
     float v[WIN];
 #pragma unroll
     for (int k = 0; k < WIN; ++k) v[k] = 0.0f;
