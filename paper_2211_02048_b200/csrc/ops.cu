@@ -461,13 +461,14 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
 // k_scatter (above) behind a two-deep copy pipeline. Item = (chunk of T tiles,
 // slice of cpi channels); the stack side of an item is T runs of cpi * b^2
 // contiguous floats, the origins 3 T contiguous ints.
-constexpr int kPipeFloats = 4096;  // per buffer (two buffers: 32 KB)
+constexpr int kPipeFloats = 6144;     // per buffer (two buffers in dynamic shared memory: 48 KB)
+constexpr int kPipeMaxFloats = 16384;  // SIGE_SCATTER_STAGE cap
 __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restrict__ blocks, int count, int c,
                                                            int b, const int32_t* __restrict__ idx,
                                                            float* __restrict__ base, int nsamp, int h, int w,
-                                                           int T, int cpi, int mode) {
+                                                           int T, int cpi, int mode, int buf_floats) {
   __shared__ __align__(16) int s_org[2][kMaxChunkTiles * 3];
-  __shared__ __align__(16) float s_buf[2][kPipeFloats];
+  extern __shared__ __align__(16) float s_dyn[];
   const int bsz = b * b;
   const size_t slab = static_cast<size_t>(c) * bsz, plane = static_cast<size_t>(h) * w;
   const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi, items = chunks * slices;
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(idx + 3 * i0 + j) : "memory");
     }
     stack_to_smem_issue(blocks + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * bsz, slab,
-                        s_buf[sbi], tc, ncl * bsz, vec);
+                        s_dyn + sbi * buf_floats, tc, ncl * bsz, vec);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int sbi = 0;
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
     const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
     const int i0 = ck * T, tc = min(T, count - i0), run = ncl * bsz;
     const int* org = s_org[sbi];
-    const float* buf = s_buf[sbi];
+    const float* buf = s_dyn + sbi * buf_floats;
     // column pairs (8-byte stores) when the block and width are even
     const int per = (b & 1) == 0 && (w & 1) == 0 ? 2 : 1, hb = b / per, pcols = tc * hb;
     ColWalk pw(pcols);
@@ -835,17 +836,27 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
   const long long items = static_cast<long long>((count + cp.T - 1) / cp.T) * ((c + cp.cpi - 1) / cp.cpi);
   static const bool no_pipe = std::getenv("SIGE_SCATTER_NOPIPE") != nullptr;  // A/B: the single-buffered kernel
   const int bsz = b * b;
-  if (!no_pipe && bsz <= kPipeFloats) {
-    const int T = std::max(1, std::min({kMaxChunkTiles, kChunkCols / b, kPipeFloats / bsz}));
-    const int cpi = std::max(1, std::min(c, kPipeFloats / (T * bsz)));
+  static const int stage = [] {  // floats per buffer (A/B: SIGE_SCATTER_STAGE)
+    const char* e = std::getenv("SIGE_SCATTER_STAGE");
+    const int v = e ? std::atoi(e) : kPipeFloats;
+    return std::max(1024, std::min(kPipeMaxFloats, v / 4 * 4));
+  }();
+  if (!no_pipe && bsz <= stage) {
+    const int T = std::max(1, std::min({kMaxChunkTiles, kChunkCols / b, stage / bsz}));
+    const int cpi = std::max(1, std::min(c, stage / (T * bsz)));
     const long long pitems = static_cast<long long>((count + T - 1) / T) * ((c + cpi - 1) / cpi);
-    static int per_sm = [] {
+    const size_t dyn = 2 * static_cast<size_t>(stage) * sizeof(float);
+    static std::atomic<uint64_t> attr_done{0};
+    if (first_on_device(attr_done))
+      SIGE_CUDA(cudaFuncSetAttribute(k_scatter_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(2 * kPipeMaxFloats * sizeof(float))));
+    static int per_sm = [dyn] {
       int n = 0;
-      SIGE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_scatter_pipe, kThreads, 0));
+      SIGE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_scatter_pipe, kThreads, dyn));
       return std::max(1, n);
     }();
     k_scatter_pipe<<<static_cast<int>(std::min<long long>(pitems, static_cast<long long>(sm_count()) * per_sm)),
-                     kThreads, 0, st>>>(blocks, count, c, b, idx, base, n, h, w, T, cpi, add ? 1 : 0);
+                     kThreads, dyn, st>>>(blocks, count, c, b, idx, base, n, h, w, T, cpi, add ? 1 : 0, stage);
     after_launch("k_scatter_pipe");
     return;
   }
