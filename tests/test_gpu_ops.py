@@ -192,6 +192,23 @@ def test_scatter_family_matches_oracle(orc):
         assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
 
 
+@pytest.mark.parametrize("n,c,hw,b,dens", [
+    (2, 256, 128, 4, 1.0),   # ~1400 (tiles x channels) items: the persistent kernel alternates its two buffers
+    (2, 96, 70, 6, 0.3),     # ragged chunks and channel slices, fringe tiles
+    (1, 2, 170, 80, 1.0),    # 80x80 blocks exceed a staging buffer: the single-buffered kernel
+])
+def test_scatter_pipeline_sizes_match_oracle(orc, n, c, hw, b, dens):
+    rng = np.random.default_rng(hw + b)
+    m = (rng.random((hw, hw)) < dens).astype(np.uint8)
+    idx, _ = orc.mask_to_block_indices(m, b, n)
+    blocks = rng.uniform(-1, 1, (len(idx), c, b, b)).astype(np.float32)
+    base = rng.uniform(-1, 1, (n, c, hw, hw)).astype(np.float32)
+    assert bits_equal(host(sb.scatter(cu(blocks), cu(idx), cu(base))), orc.scatter(blocks, idx, base))
+    tb = cu(base)
+    sb.scatter_add_inplace(cu(blocks), cu(idx), tb)
+    assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
+
+
 def test_scatter_clips_fringe_tiles():
     # test_kernels.cpp:136-145
     base = cu(np.zeros((1, 1, 5, 5), np.float32))
