@@ -473,8 +473,18 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
   const size_t slab = static_cast<size_t>(c) * bsz, plane = static_cast<size_t>(h) * w;
   const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi, items = chunks * slices;
   const bool vec = (bsz & 3) == 0;
-  auto issue = [&](int it, int sbi) {
-    const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
+  // items advance by gridDim.x: (chunk, slice) stepped without divisions
+  const int dq = gridDim.x / slices, dr = gridDim.x - dq * slices;
+  auto step = [&](int& ck, int& sl) {
+    ck += dq, sl += dr;
+    if (sl >= slices) sl -= slices, ++ck;
+  };
+  // the column walk of a full chunk, decoded once (this kernel is issue-bound)
+  const int per = (b & 1) == 0 && (w & 1) == 0 ? 2 : 1, hb = b / per;
+  const ColWalk pw_full(T * hb);
+  const int t_full = pw_full.col / hb;
+  auto issue = [&](int ck, int sl, int sbi) {
+    const int c0 = sl * cpi, ncl = min(c, c0 + cpi) - c0;
     const int i0 = ck * T, tc = min(T, count - i0);
     for (int j = threadIdx.x; j < 3 * tc; j += blockDim.x) {
       const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(&s_org[sbi][j]));
@@ -485,24 +495,28 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int sbi = 0;
-  if (blockIdx.x < items) issue(blockIdx.x, 0);
-  for (int it = blockIdx.x; it < items; it += gridDim.x, sbi ^= 1) {
+  int ck = blockIdx.x / slices, sl = blockIdx.x - (blockIdx.x / slices) * slices;
+  if (blockIdx.x < items) issue(ck, sl, 0);
+  for (int it = blockIdx.x; it < items; it += gridDim.x, sbi ^= 1, step(ck, sl)) {
     if (it + static_cast<int>(gridDim.x) < items) {
-      issue(it + gridDim.x, sbi ^ 1);
+      int nck = ck, nsl = sl;
+      step(nck, nsl);
+      issue(nck, nsl, sbi ^ 1);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const int ck = it / slices, c0 = (it - ck * slices) * cpi, ncl = min(c, c0 + cpi) - c0;
+    const int c0 = sl * cpi, ncl = min(c, c0 + cpi) - c0;
     const int i0 = ck * T, tc = min(T, count - i0), run = ncl * bsz;
     const int* org = s_org[sbi];
     const float* buf = s_dyn + sbi * buf_floats;
     // column pairs (8-byte stores) when the block and width are even
-    const int per = (b & 1) == 0 && (w & 1) == 0 ? 2 : 1, hb = b / per, pcols = tc * hb;
-    ColWalk pw(pcols);
-    for (; pw.col < pcols; pw.col += pw.col_step) {
-      const int t = pw.col / hb, dx = (pw.col - t * hb) * per;
+    const int pcols = tc * hb;
+    ColWalk pw = tc == T ? pw_full : ColWalk(pcols);
+    int t = tc == T ? t_full : pw.col / hb;
+    for (; pw.col < pcols;) {
+      const int dx = (pw.col - t * hb) * per;
       const int y0 = org[3 * t + 1], xx = org[3 * t + 2] + dx;
       // fringe clipping; an index outside the tensor never writes
       const bool inside = org[3 * t] >= 0 && org[3 * t] < nsamp && y0 >= 0 && org[3 * t + 2] >= 0;
@@ -528,6 +542,8 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
           for (int dy = 0; dy < dy_hi; ++dy) dc[dy * w] = mode ? __fadd_rn(dc[dy * w], sc[dy * b]) : sc[dy * b];
         }
       }
+      pw.col += pw.col_step;
+      if (pw.col < pcols) t = pw.col / hb;
     }
     __syncthreads();  // buffer sbi is refilled by the next iteration's issue
   }
