@@ -262,7 +262,7 @@ __global__ void k_gather(const float* __restrict__ x, int c, int h, int w,
   // one 16-byte store each) and keeps two quads = 8 loads in flight.
   constexpr int kQ = 2;
   const int wsz = win * win, slab = c * wsz;
-  const bool vec = (slab & 3) == 0;
+  const bool vec = (slab & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   for (int i = blockIdx.x; i < count; i += gridDim.x) {
     const int n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1) * stride - pad,
               ox = __ldg(idx + 3 * i + 2) * stride - pad;
@@ -375,6 +375,86 @@ __global__ void __launch_bounds__(256) k_gather_rows(const float* __restrict__ x
   }
 }
 
+// gather, 8-wide window rows with 256-bit loads (sm_100 LDG.256): the row
+// form above is bound by L1 LSU wavefronts (one per touched line per load
+// instruction); two 32-byte-aligned loads cover 8 floats at any phase where
+// the row form needs three 16-byte ones. Needs w % 8 == 0 and a 32-byte
+// aligned x (checked on the host).
+__device__ __forceinline__ void ldg256(const float* p, float* v) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__global__ void __launch_bounds__(256) k_gather_rows8w(const float* __restrict__ x, int c, int h, int w,
+                                                       const int32_t* __restrict__ idx, long long rows, int stride,
+                                                       int pad, DevEpilogue epi, float* __restrict__ out) {
+  constexpr int WIN = 8;
+  const int lane = threadIdx.x & 31;
+  for (long long rb = blockIdx.x * static_cast<long long>(blockDim.x) + (threadIdx.x & ~31); rb < rows;
+       rb += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = rb + lane;
+    if (r >= rows) continue;
+    const int wy = static_cast<int>(r % WIN);
+    const long long gc = r / WIN;
+    const int ch = static_cast<int>(gc % c);
+    const int i = static_cast<int>(gc / c);
+    const unsigned act = __activemask();
+    const int i0 = __shfl_sync(act, i, __ffs(act) - 1);
+    int n, oy, ox;
+    if ((act & 7u) == 7u && __all_sync(act, i == i0)) {
+      const int v = lane < 3 ? __ldg(idx + 3 * i0 + lane) : 0;
+      n = __shfl_sync(act, v, 0), oy = __shfl_sync(act, v, 1), ox = __shfl_sync(act, v, 2);
+    } else {
+      n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1), ox = __ldg(idx + 3 * i + 2);
+    }
+    const int sy = oy * stride - pad + wy, sx0 = ox * stride - pad;
+    float v[WIN];
+#pragma unroll
+    for (int k = 0; k < WIN; ++k) v[k] = 0.0f;
+    if (sy >= 0 && sy < h) {
+      const float* row = x + ((static_cast<size_t>(n) * c + ch) * h + sy) * w;
+      const int base = sx0 & ~7;  // 32-byte aligned start (sx0 may be negative)
+      const int ph = sx0 - base;  // 0..7
+      float buf[16];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int xs = base + 8 * q;
+        if (xs >= 0 && xs < w && (q == 0 || ph > 0)) {
+          ldg256(row + xs, buf + 8 * q);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) buf[8 * q + k] = 0.0f;
+        }
+      }
+      // v[k] = buf[ph + k]: a 3-stage barrel shift (compile-time indices only)
+      if (ph & 4) {
+#pragma unroll
+        for (int k = 0; k < 12; ++k) buf[k] = buf[k + 4];
+      }
+      if (ph & 2) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) buf[k] = buf[k + 2];
+      }
+      if (ph & 1) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) buf[k] = buf[k + 1];
+      }
+#pragma unroll
+      for (int k = 0; k < WIN; ++k) v[k] = buf[k];
+      if (epi.num_steps) {
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) {
+          const int sx = sx0 + k;
+          if (sx >= 0 && sx < w) v[k] = dev_epi(epi, v[k], ch, c, n);
+        }
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(out + ((static_cast<size_t>(i) * c + ch) * WIN + wy) * WIN);
+    o[0] = make_float4(v[0], v[1], v[2], v[3]);
+    o[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
 // scatter_inplace / scatter_add_inplace: tile values clipped at the fringe;
 // mode 0 writes, mode 1 adds.
 __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ blocks, int count, int c, int b,
@@ -393,7 +473,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const float* __restrict__ 
     const float* sb = blocks + static_cast<size_t>(i0) * slab + static_cast<size_t>(c0) * bsz;
     const int run = ncl * bsz;
     if (staged) {
-      stack_to_smem(sb, slab, s_buf, tc, run, (bsz & 3) == 0);
+      stack_to_smem(sb, slab, s_buf, tc, run, (bsz & 3) == 0 && (reinterpret_cast<uintptr_t>(blocks) & 15) == 0);
       __syncthreads();
     }
     // image side: rows (channel, tile row), cols (tile, tile column). With
@@ -472,7 +552,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
   const int bsz = b * b;
   const size_t slab = static_cast<size_t>(c) * bsz, plane = static_cast<size_t>(h) * w;
   const int chunks = (count + T - 1) / T, slices = (c + cpi - 1) / cpi, items = chunks * slices;
-  const bool vec = (bsz & 3) == 0;
+  const bool vec = (bsz & 3) == 0 && (reinterpret_cast<uintptr_t>(blocks) & 15) == 0;
   // items advance by gridDim.x: (chunk, slice) stepped without divisions
   const int dq = gridDim.x / slices, dr = gridDim.x - dq * slices;
   auto step = [&](int& ck, int& sl) {
@@ -480,7 +560,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_pipe(const float* __restri
     if (sl >= slices) sl -= slices, ++ck;
   };
   // the column walk of a full chunk, decoded once (this kernel is issue-bound)
-  const int per = (b & 1) == 0 && (w & 1) == 0 ? 2 : 1, hb = b / per;
+  const int per = (b & 1) == 0 && (w & 1) == 0 && (reinterpret_cast<uintptr_t>(base) & 7) == 0 ? 2 : 1, hb = b / per;
   const ColWalk pw_full(T * hb);
   const int t_full = pw_full.col / hb;
   auto issue = [&](int ck, int sl, int sbi) {
@@ -829,7 +909,18 @@ void op_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, i
   if (count == 0) return;
   int win = s * b + k - s;
   static const bool rows_off = std::getenv("SIGE_GATHER_TILES") != nullptr;  // A/B: the per-tile walk
-  if (!rows_off && (w & 3) == 0 && (win == 8 || win == 4)) {
+  static const bool v8_off = std::getenv("SIGE_GATHER_128") != nullptr;  // A/B: 16-byte loads for win 8
+  // vector paths only on aligned tensors (a C-ABI caller may pass any float pointer)
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x), oa = reinterpret_cast<uintptr_t>(out);
+  const bool out16 = (oa & 15) == 0;
+  if (!rows_off && !v8_off && win == 8 && (w & 7) == 0 && (xa & 31) == 0 && out16) {
+    const long long rows = static_cast<long long>(count) * c * win;
+    const int grid = static_cast<int>(std::min<long long>((rows + 255) / 256, sm_count() * 16LL));
+    k_gather_rows8w<<<grid, 256, 0, st>>>(x, c, h, w, idx, rows, s, (k - 1) / 2, epi, out);
+    after_launch("k_gather_rows8w");
+    return;
+  }
+  if (!rows_off && (w & 3) == 0 && (win == 8 || win == 4) && (xa & 15) == 0 && out16) {
     const long long rows = static_cast<long long>(count) * c * win;
     const int grid = static_cast<int>(std::min<long long>((rows + 255) / 256, sm_count() * 16LL));
     if (win == 8)
@@ -877,7 +968,8 @@ void op_scatter(const float* blocks, int count, int channels, int b, const int32
     return;
   }
   static const bool no_pairs = std::getenv("SIGE_SCATTER_SINGLE") != nullptr;  // A/B: one column per thread
-  const int pairs = !no_pairs && cp.staged && (b & 1) == 0 && (w & 1) == 0 ? 2 : 0;
+  const int pairs =
+      !no_pairs && cp.staged && (b & 1) == 0 && (w & 1) == 0 && (reinterpret_cast<uintptr_t>(base) & 7) == 0 ? 2 : 0;
   k_scatter<<<static_cast<int>(std::min<long long>(items, sm_count() * 8LL)), kThreads, 0, st>>>(
       blocks, count, c, b, idx, base, n, h, w, cp.T, cp.cpi, cp.staged ? 1 : 0, add ? 1 : 0, pairs);
   after_launch("k_scatter");

@@ -163,6 +163,25 @@ def test_gather_with_epilogue_matches_oracle(orc, k, s):
         assert bits_equal(got, want)
 
 
+@pytest.mark.parametrize("k,b,w,offset", [(3, 6, 64, 0), (1, 8, 40, 0), (3, 6, 48, 1)])
+def test_gather_wide_rows_match_oracle(orc, k, b, w, offset):
+    """8-wide window rows with w % 8 == 0 take the 256-bit-load kernel (every
+    phase 0-7 of the window start, fringe windows at both image edges); a base
+    pointer off 32-byte alignment (offset 1) takes the 16-byte-load kernel."""
+    rng = np.random.default_rng(w + b + offset)
+    n, c, h = 2, 5, 29
+    flat = rng.uniform(-3, 3, n * c * h * w + offset).astype(np.float32)
+    x = flat[offset:].reshape(n, c, h, w)
+    m = (rng.random((h, w)) < 0.3).astype(np.uint8)
+    m[:, 0] = m[:, -1] = m[0, :] = m[-1, :] = 1
+    idx, _ = orc.mask_to_block_indices(m, b, n)
+    for epi in ([], rand_epi_np(rng, c, n, silu=True, per_sample=True)):
+        want = orc.gather(np.ascontiguousarray(x), idx, b, h, w, k, 1, epi)
+        xd = cu(flat)[offset:].view(n, c, h, w)
+        got = host(sb.gather(xd, cu(idx), b, k, 1, to_dev_epi(epi)))
+        assert bits_equal(got, want)
+
+
 def test_silu_relu_epilogue_zero_fill_untouched(orc):
     # test_kernels.cpp:94-112
     rng = np.random.default_rng(5)
@@ -207,6 +226,24 @@ def test_scatter_pipeline_sizes_match_oracle(orc, n, c, hw, b, dens):
     tb = cu(base)
     sb.scatter_add_inplace(cu(blocks), cu(idx), tb)
     assert bits_equal(host(tb), orc.scatter_add_inplace(blocks, idx, base.copy()))
+
+
+def test_scatter_misaligned_tensors_match_oracle(orc):
+    """Block stacks and bases that start off 16- / 8-byte alignment (views at a
+    one-float offset) take the scalar paths and give the same bits."""
+    rng = np.random.default_rng(5)
+    n, c, hw, b = 2, 12, 40, 6
+    m = (rng.random((hw, hw)) < 0.4).astype(np.uint8)
+    idx, _ = orc.mask_to_block_indices(m, b, n)
+    blocks = rng.uniform(-1, 1, (len(idx), c, b, b)).astype(np.float32)
+    base = rng.uniform(-1, 1, (n, c, hw, hw)).astype(np.float32)
+    bl = cu(np.concatenate([[0.0], blocks.ravel()]).astype(np.float32))[1:].view(blocks.shape)
+    tb = cu(np.concatenate([[0.0], base.ravel()]).astype(np.float32))[1:].view(base.shape)
+    sb.scatter_inplace(bl, cu(idx), tb)
+    assert bits_equal(host(tb), orc.scatter(blocks, idx, base))
+    tb2 = cu(np.concatenate([[0.0], base.ravel()]).astype(np.float32))[1:].view(base.shape)
+    sb.scatter_add_inplace(bl, cu(idx), tb2)
+    assert bits_equal(host(tb2), orc.scatter_add_inplace(blocks, idx, base.copy()))
 
 
 def test_scatter_clips_fringe_tiles():
