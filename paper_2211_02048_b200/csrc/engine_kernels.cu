@@ -36,7 +36,8 @@ __global__ void k_mask_bits(const float* __restrict__ o, const float* __restrict
   any += blockIdx.z;
   if (mask_u8) mask_u8 += blockIdx.z * hw;
   const int p0 = blockIdx.y * ppy, p1 = min(planes, p0 + ppy);
-  const bool vec = (w & 3) == 0;
+  // (the edited input is the caller's tensor: vector loads only when aligned)
+  const bool vec = (w & 3) == 0 && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(e)) & 15) == 0;
   const long long nq = vec ? hw >> 2 : hw;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq;
        q += (long long)gridDim.x * blockDim.x) {
@@ -697,7 +698,7 @@ void launch_mask_bits(const float* orig, const float* edited, int n, int c, int 
   SIGE_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * h * wpr * masks, st));
   if (mask_u8) SIGE_CUDA(cudaMemsetAsync(mask_u8, 0, static_cast<size_t>(h) * w * masks, st));
   const long long hw = static_cast<long long>(h) * w;
-  const long long nq = (w & 3) == 0 ? hw / 4 : hw;
+  const long long nq = (w & 3) == 0 ? hw / 4 : hw;  // (grid sizing only: the kernel may fall back to scalar)
   const int planes = per_sample ? c : n * c;
   const int gx = static_cast<int>(std::min<long long>((nq + 255) / 256, 4096));
   int gy = std::min(planes, std::max(1, sm_count() * 8 / (gx * masks)));

@@ -36,7 +36,7 @@ __global__ void k_difference_mask(const float* __restrict__ o, const float* __re
                                   uint8_t* __restrict__ mask) {
   int p0 = blockIdx.y * planes_per_y;
   int p1 = min(planes, p0 + planes_per_y);
-  bool vec = (hw & 3) == 0;
+  const bool vec = (hw & 3) == 0 && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(e)) & 15) == 0;
   long long nq = vec ? hw / 4 : hw;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nq;
        q += (long long)gridDim.x * blockDim.x) {
@@ -852,7 +852,8 @@ void op_difference_mask(const float* o, const float* e, int n, int c, int h, int
   long long hw = (long long)h * w;
   SIGE_CUDA(cudaMemsetAsync(mask, 0, hw, st));
   int planes = n * c;
-  long long nq = (hw & 3) == 0 ? hw / 4 : hw;
+  const bool vec = (hw & 3) == 0 && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(e)) & 15) == 0;
+  long long nq = vec ? hw / 4 : hw;
   int gx = static_cast<int>(std::min<long long>((nq + 255) / 256, 1 << 16));
   // enough CTAs for ~4 waves: split the planes across grid.y
   int want_y = std::max(1, (sm_count() * 8) / std::max(1, gx));

@@ -368,3 +368,19 @@ def test_offload_and_prefetch_steps(orc, math):
         want, _ = om.sparse_forward(cache, b_edit, orc.difference_mask(b_orig, b_edit),
                                     sb.default_config(dilate_full=om.required_dilation()))
         assert np.array_equal(want_b.numpy(), want)
+
+
+@pytest.mark.parametrize("math", [sb.MATH_EXACT, sb.MATH_F16])
+def test_misaligned_edited_input_same_bits(orc, math):
+    """The edited input is the caller's tensor: a view at a one-float offset
+    (off 16-byte alignment) takes the scalar mask loads and gives the aligned
+    tensor's bits."""
+    orig, edited = orc.make_edit_fixture("rect5", 1, 3, 64, 64, 43)
+    eng = sb.Engine(sb.Model("mini_unet_gn"), math=math)
+    eng.precompute(torch.from_numpy(orig).cuda())
+    cfg = sb.default_config(dilate_full=1, min_sparse_res=1)
+    want = eng.sparse_forward(torch.from_numpy(edited).cuda(), config=cfg).clone()
+    flat = torch.from_numpy(np.concatenate([[0.0], edited.ravel()]).astype(np.float32)).cuda()
+    xv = flat[1:].view(edited.shape)
+    assert xv.data_ptr() % 16 != 0
+    assert torch.equal(eng.sparse_forward(xv, config=cfg), want)

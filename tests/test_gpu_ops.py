@@ -77,6 +77,10 @@ def test_difference_mask_matches_oracle(orc, kind, n, c, h, w, seed):
     want = orc.difference_mask(o, e, 1e-3)
     got = host(sb.compute_difference_mask(cu(o), cu(e), 1e-3))
     assert np.array_equal(got, want)
+    # inputs at a one-float offset (off 16-byte alignment): the scalar path, same mask
+    ov = cu(np.concatenate([[0.0], o.ravel()]).astype(np.float32))[1:].view(o.shape)
+    ev = cu(np.concatenate([[0.0], e.ravel()]).astype(np.float32))[1:].view(e.shape)
+    assert np.array_equal(host(sb.compute_difference_mask(ov, ev, 1e-3)), want)
 
 
 def test_difference_mask_golden_hash(orc):
