@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(256) k_gather_rows8w(const float* __restrict__
                                                        int pad, DevEpilogue epi, float* __restrict__ out) {
   constexpr int WIN = 8;
   const int lane = threadIdx.x & 31;
+  const bool st256 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;  // one 256-bit store per row
   for (long long rb = blockIdx.x * static_cast<long long>(blockDim.x) + (threadIdx.x & ~31); rb < rows;
        rb += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = rb + lane;
@@ -449,9 +450,15 @@ __global__ void __launch_bounds__(256) k_gather_rows8w(const float* __restrict__
         }
       }
     }
-    float4* o = reinterpret_cast<float4*>(out + ((static_cast<size_t>(i) * c + ch) * WIN + wy) * WIN);
-    o[0] = make_float4(v[0], v[1], v[2], v[3]);
-    o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    float* o = out + ((static_cast<size_t>(i) * c + ch) * WIN + wy) * WIN;
+    if (st256) {
+      asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                   "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                   : "memory");
+    } else {
+      reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
   }
 }
 
