@@ -386,26 +386,31 @@ __device__ __forceinline__ void ldg256(const float* p, float* v) {
                : "l"(p));
 }
 __global__ void __launch_bounds__(256) k_gather_rows8w(const float* __restrict__ x, int c, int h, int w,
-                                                       const int32_t* __restrict__ idx, long long rows, int stride,
+                                                       const int32_t* __restrict__ idx, int count, long long rows,
+                                                       int stride,
                                                        int pad, DevEpilogue epi, float* __restrict__ out) {
   constexpr int WIN = 8;
   const int lane = threadIdx.x & 31;
   const bool st256 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;  // one 256-bit store per row
   for (long long rb = blockIdx.x * static_cast<long long>(blockDim.x) + (threadIdx.x & ~31); rb < rows;
        rb += static_cast<long long>(gridDim.x) * blockDim.x) {
+    // a warp = 4 consecutive tiles (usually horizontal neighbours) x 8 window
+    // rows of one channel: each load instruction touches ~16 lines instead of
+    // the 32 of a one-tile warp (the LSU data pipe bounds this kernel)
     const long long r = rb + lane;
     if (r >= rows) continue;
-    const int wy = static_cast<int>(r % WIN);
-    const long long gc = r / WIN;
-    const int ch = static_cast<int>(gc % c);
-    const int i = static_cast<int>(gc / c);
+    const int wy = static_cast<int>(r & 7), j = static_cast<int>((r >> 3) & 3);
+    const long long gq = r >> 5;  // tile quad * c + channel
+    const int ch = static_cast<int>(gq % c);
+    const int i = static_cast<int>(gq / c) * 4 + j;
     const unsigned act = __activemask();
-    const int i0 = __shfl_sync(act, i, __ffs(act) - 1);
+    const int t0 = (static_cast<int>(gq / c)) * 4;
     int n, oy, ox;
-    if ((act & 7u) == 7u && __all_sync(act, i == i0)) {
-      const int v = lane < 3 ? __ldg(idx + 3 * i0 + lane) : 0;
-      n = __shfl_sync(act, v, 0), oy = __shfl_sync(act, v, 1), ox = __shfl_sync(act, v, 2);
+    if (act == 0xffffffffu && t0 + 4 <= count) {  // lanes 0-11 fetch the quad's origins
+      const int v = lane < 12 ? __ldg(idx + 3 * t0 + lane) : 0;
+      n = __shfl_sync(act, v, 3 * j), oy = __shfl_sync(act, v, 3 * j + 1), ox = __shfl_sync(act, v, 3 * j + 2);
     } else {
+      if (i >= count) continue;
       n = __ldg(idx + 3 * i), oy = __ldg(idx + 3 * i + 1), ox = __ldg(idx + 3 * i + 2);
     }
     const int sy = oy * stride - pad + wy, sx0 = ox * stride - pad;
@@ -922,9 +927,9 @@ void op_gather(const float* x, int n, int c, int h, int w, const int32_t* idx, i
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x), oa = reinterpret_cast<uintptr_t>(out);
   const bool out16 = (oa & 15) == 0;
   if (!rows_off && !v8_off && win == 8 && (w & 7) == 0 && (xa & 31) == 0 && out16) {
-    const long long rows = static_cast<long long>(count) * c * win;
+    const long long rows = static_cast<long long>((count + 3) / 4) * c * 32;  // tile quads x channels x 4 x 8 rows
     const int grid = static_cast<int>(std::min<long long>((rows + 255) / 256, sm_count() * 16LL));
-    k_gather_rows8w<<<grid, 256, 0, st>>>(x, c, h, w, idx, rows, s, (k - 1) / 2, epi, out);
+    k_gather_rows8w<<<grid, 256, 0, st>>>(x, c, h, w, idx, count, rows, s, (k - 1) / 2, epi, out);
     after_launch("k_gather_rows8w");
     return;
   }
